@@ -1,0 +1,31 @@
+"""Seeded synthetic input generators shared by the oracle and the product path.
+
+Holds no tensor-network arithmetic (no network build, no contraction, no slicing):
+only circuits (gate matrices + wires) and output digits, drawn from splitmix64.
+"""
+
+from .circuit import Circuit, Gate, random_bitstring
+from .gbs import generate_gbs
+from .rng import SplitMix64
+from .sycamore import grid_rqc, random_circuit, sycamore53, sycamore_qubits, grid_qubits
+
+__all__ = ["Circuit", "Gate", "random_bitstring", "generate_gbs", "SplitMix64",
+           "grid_rqc", "random_circuit", "sycamore53", "sycamore_qubits", "grid_qubits",
+           "workload"]
+
+
+def workload(name: str, seed: int = 1):
+    """The BASELINE.json configs as (circuit, bitstring) pairs."""
+    if name == "C1":
+        c = grid_rqc(3, 3, 8, seed)
+    elif name == "C2":
+        c = sycamore53(10, seed)
+    elif name == "C3":
+        c = sycamore53(14, seed)
+    elif name == "C5":
+        c = sycamore53(20, seed)
+    elif name == "C4":
+        c = generate_gbs(3, 4, 1, 0.5, 4, seed)
+    else:
+        raise ValueError(name)
+    return c, random_bitstring(c.n_wires, c.d, seed)
