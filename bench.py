@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the Jet hot path on B200: sliced single-amplitude contraction of Sycamore-53
+(BASELINE.json metric "Sycamore-53 m=14 amplitude time; slices/s and cGEMM TFLOP/s at
+1/2/4/8 B200").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+A step = one pass of the whole hot path (every executed contraction node, the slice
+accumulate and the all-reduce) over one block of consecutive slices of the amplitude; the
+prefix cache persists across steps exactly as inside one amplitude run.  Rank g contracts
+the g-th contiguous block of the canonical slice order (weak scaling: fixed slices per GPU
+per step).  Timing: CUDA events on the exec stream, barrier + synchronize on both sides,
+max over ranks.  Rank 0 prints ONE JSON line.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: circuit key, sliced labels, dtype, slices per step, workload name
+    "C2": dict(circ="C2", k=6, dtype="c64", sps=64, workload="sycamore53_m10_2^6slices"),
+    "C3": dict(circ="C3", k=10, dtype="c64", sps=16, workload="sycamore53_m14_2^10slices"),
+    "C5": dict(circ="C5", k=None, dtype="c64", sps=4, workload="sycamore53_m20_subset"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--slices-per-step", type=int, default=0)
+    ap.add_argument("--trials", type=int, default=256)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--width-cap", type=int, default=31)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_plan(jet, cfg, args):
+    from circuits import workload
+
+    circ, bits = workload(cfg["circ"], args.seed)
+    net = jet.Network.from_circuit(circ, bits)
+    k = cfg["k"]
+    t0 = time.time()
+    plan = jet.Plan.greedy(net, seed=args.seed, trials=args.trials, n_sliced=k if k is not None else -1,
+                           width_cap=args.width_cap if k is None else 0)
+    return circ, bits, net, plan, time.time() - t0
+
+
+# ------------------------------------------------------------------ oracle (CPU) sampling
+def oracle_sample(circ, bits, plan, budget_s, max_out_log2=27):
+    """The oracle as it stands (oracle.contract.contract_pair, complex128 numpy) evaluating
+    slice 0 of the plan step by step in path order for about budget_s seconds.  Returns
+    (FLOP done, seconds, steps done).  Steps whose output exceeds 2^max_out_log2 elements
+    end the sample (host-memory guard)."""
+    from oracle import contract, cost
+    from oracle.network import build_network
+
+    onet = build_network(circ, bits)
+    sl = plan.sliced_labels
+    path = plan.ssa_path
+    steps = cost.tree_info(onet, path, sl)
+    assign = {l: 0 for l in sl}
+    vals, labs = {}, {}
+    for t in range(onet.n_tensors):
+        vals[t], labs[t] = contract.restrict(onet.tensors[t], onet.labels[t], assign)
+    nid = onet.n_tensors
+    done_flop, n_done = 0, 0
+    t0 = time.perf_counter()
+    for (i, j), (flop, _) in zip(path, steps):
+        out_labels = [l for l in labs[i] if l not in labs[j]] + [l for l in labs[j] if l not in labs[i]]
+        if len(out_labels) * (onet.dims[out_labels[0]].bit_length() - 1 if out_labels else 0) > max_out_log2:
+            break
+        vals[nid], labs[nid] = contract.contract_pair(vals.pop(i), labs.pop(i), vals.pop(j), labs.pop(j))
+        nid += 1
+        done_flop += flop
+        n_done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    return done_flop, time.perf_counter() - t0, n_done
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline_entry(circ, bits, plan, budget_s):
+    c = plan.cost()
+    flop_per_slice = c["prefix"] / c["n_sl"]
+    fl, sec, n = oracle_sample(circ, bits, plan, budget_s)
+    rate = fl / sec if sec > 0 else 0.0
+    return {
+        "value": rate / flop_per_slice,
+        "unit": "slices/s",
+        "cores": blas_threads(),
+        "kind": "oracle",
+        "sample": (f"oracle (numpy complex128 pairwise steps) on slice 0 of the same plan, first {n} path "
+                   f"steps ({fl:.3g} FLOP in {sec:.1f} s = {rate / 1e9:.2f} GFLOP/s), scaled by the plan's "
+                   f"prefix-cache FLOP per slice {flop_per_slice:.3g}"),
+        "oracle_gflops": rate / 1e9,
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+def profile_traffic(cfg_name):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(cfg_name)
+    return None
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("CUDA_VISIBLE_DEVICES", "")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2107_09793_b200 import jet
+
+    circ, bits, net, plan, _ = make_plan(jet, cfg, args)
+    c = plan.cost()
+    flop_per_slice = c["prefix"] / c["n_sl"]
+    budget = max(2.0, min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(circ, bits, plan, budget)
+    fl_tot, sec_tot, n = 0, 0.0, 0
+    for _ in range(args.steps):
+        fl, sec, n = oracle_sample(circ, bits, plan, budget)
+        fl_tot += fl
+        sec_tot += sec
+    rate = fl_tot / sec_tot
+    value = rate / flop_per_slice
+    cores = blas_threads()
+    sample = (f"each step: oracle on slice 0 of the plan, first {n} path steps for ~{budget:.0f} s; "
+              f"{rate / 1e9:.2f} GFLOP/s scaled by {flop_per_slice:.3g} prefix FLOP per slice")
+    print(json.dumps({
+        "impl": "reference", "metric": "Sycamore-53 m=14 amplitude time; slices/s and cGEMM TFLOP/s",
+        "value": value, "unit": "slices/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sec_tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded Sycamore-style RQC)",
+        "config": {"workload": cfg["workload"], "n_sl": c["n_sl"], "flop_per_slice_prefix": flop_per_slice},
+        "cpu_baseline": {"value": value, "unit": "slices/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "amplitude_time_s": c["n_sl"] / value,
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        log(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2107_09793_b200 import jet
+    from paper_2107_09793_b200.runtime import allreduce_amplitude, shard_range
+
+    circ, bits, net, plan, t_plan = make_plan(jet, cfg, args)
+    c = plan.cost()
+    n_sl = c["n_sl"]
+    b0, e0 = shard_range(n_sl, rank, world)
+    rng_len = e0 - b0
+    sps = args.slices_per_step or cfg["sps"]
+    sps = max(1, min(sps, rng_len))
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ex = jet.Exec(plan, cfg["dtype"], stream=stream)
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    pos = [0]
+
+    def next_block():
+        b = b0 + pos[0]
+        e = min(b + sps, e0)
+        pos[0] = (e - b0) % rng_len
+        return b, e
+
+    def step():
+        b, e = next_block()
+        ex.contract(b, e, acc)
+        with torch.cuda.stream(stream):
+            allreduce_amplitude(acc)
+        return e - b
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ex.reset_stats()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    slices = 0
+    for _ in range(args.steps):
+        slices += step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    st = ex.stats()
+    t = torch.tensor([ms, float(slices), st["flop_executed"], st["bytes_executed"], float(st["kernel_launches"])],
+                     dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_max = tmax[0].item()
+        tot_slices, tot_flop, tot_bytes, tot_launch = (tsum[i].item() for i in range(1, 5))
+    else:
+        ms_max = ms
+        tot_slices, tot_flop, tot_bytes, tot_launch = slices, st["flop_executed"], st["bytes_executed"], st[
+            "kernel_launches"]
+    value = tot_slices / (ms_max / 1e3)
+
+    # profiled pass (not timed): CUDA events around every K2 launch on the exec stream
+    ex.reset_stats()
+    ex.set_profiling(True)
+    for _ in range(max(1, min(args.steps, 2))):
+        step()
+    ex.set_profiling(False)
+    pst = ex.stats()
+    k2_gbs = pst["k2_timed_bytes"] / (pst["k2_time_ms"] / 1e3) / 1e9 if pst["k2_time_ms"] > 0 else None
+
+    # end-to-end through the public API with host buffers: per step, H2D of the network
+    # leaves (pinned) + the step's slices + D2H of the step's partial amplitude
+    e2e = None
+    if not args.no_e2e:
+        ex.reset_stats()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_slices = 0
+        h2d = 0
+        for _ in range(args.steps):
+            ex.upload_leaves()
+            b, e = next_block()
+            part = ex.contract_host(b, e)
+            e_slices += e - b
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        h2d = ex.stats()["h2d_bytes"] / args.steps
+        tt = torch.tensor([el, float(e_slices)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            tm = tt.clone()
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            ts = tt.clone()
+            dist.all_reduce(ts, op=dist.ReduceOp.SUM)
+            el, e_slices = tm[0].item(), ts[1].item()
+        e2e = {"value": e_slices / el, "unit": "slices/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 16}
+
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_entry(circ, bits, plan, args.cpu_budget_s)
+        flop_rate = tot_flop / (ms_max / 1e3)
+        out = {
+            "metric": "Sycamore-53 m=14 amplitude time; slices/s and cGEMM TFLOP/s",
+            "value": value, "unit": "slices/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (seeded Sycamore-style RQC, A1-A5)",
+            "config": {
+                "workload": cfg["workload"], "n_sl": n_sl, "slices_per_step_per_gpu": sps,
+                "flop_per_slice": c["flop_sl"], "prefix_flop_total": c["prefix"], "max_width": c["max_width"],
+                "parallelism": f"slice-shard x{world}", "l2": "inputs larger than L2 (intermediates up to "
+                f"2^{int(c['max_width'])} elements)", "plan_seconds": round(t_plan, 2),
+                "step": "block of consecutive slices of one amplitude, prefix cache persists",
+            },
+            "cgemm_tflops": flop_rate / 1e12,
+            "amplitude_time_s_extrapolated": c["prefix"] / max(world, 1) / (flop_rate / max(world, 1)),
+            "gpu_launches": int(tot_launch),
+            "clocks": clk,
+            "roofline": {
+                "bound": "hbm", "achieved": k2_gbs, "peak": peak, "unit": "GB/s",
+                "frac": (k2_gbs / peak) if k2_gbs else None,
+                "traffic": profile_traffic(args.config),
+                "kernel": "K2 gett_kernel (c64), algorithmic bytes |A|+|B|+|C| per launch / CUDA-event time",
+                "peak_kind": peak_kind, "k2_launches_profiled": pst["k2_timed_launches"],
+                "k2_share_of_step": (pst["k2_time_ms"] / (ms_max / args.steps * max(1, min(args.steps, 2))))
+                if ms_max > 0 else None,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "algorithmic_gbs_step": tot_bytes / (ms_max / 1e3) / 1e9,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+/*
+ * libjetb200 -- C ABI of the B200-native Jet hot path (arXiv 2107.09793).
+ *
+ * The calls follow the paper's problem statement:
+ *   build a network from gates and a bitstring      PAPER.md l.72-85  (Sec. II.B.1)
+ *   take a contraction path and a set of sliced indices
+ *                                                   l.94-105 (Eq. sequence), l.116-133 (Eq. sliced_sum), l.176
+ *   return the amplitude(s)                         l.83-85  (<a|U|0>)
+ *
+ * Conventions
+ *   - Every call returns jt_status; nothing throws across the ABI.  On a non-zero
+ *     status, jt_last_error() returns a thread-local message valid until the next
+ *     jt_* call on that thread.  Codes: 0 OK, 2 usage (bad argument),
+ *     3 validation (bad network / path / slices), 4 resource (device OOM, workspace
+ *     too small, width over cap), 5 CUDA error, 6 internal.
+ *   - Host inputs are copied; handles are opaque and freed by *_destroy.
+ *   - Device memory and CUDA streams belong to the caller (PyTorch in the Python
+ *     binding): the library never allocates device memory except in the
+ *     self-contained convenience call jt_amplitude.
+ *   - Complex numbers are interleaved (re, im) pairs of double (host) or of the
+ *     execution dtype (device).
+ *
+ * Id conventions (shared by definition with the oracle):
+ *   tensors: 0..n-1 = the |0> ket of wires 0..n-1 (l.81), then one tensor per gate in
+ *            the order added, then (after jt_network_close) the bra of wire 0..n-1 (l.83).
+ *   labels:  0..n-1 = the ket legs; then every gate creates one new label per wire, in
+ *            the order of its `wires` argument ("w.k" scheme, numbered).
+ *   A k-qudit gate tensor has labels (out_0..out_{k-1}, in_0..in_{k-1}) and data
+ *   U[out][in] row-major, wires[0] most significant (reading A7, P:81 B_cfbe).
+ *   SSA path: step s consumes ids (p[2s], p[2s+1]) and creates id n_tensors + s.
+ *   Slice index <-> assignment: lexicographic, sliced_labels[0] most significant
+ *   (reading A12); the same order is the prefix-cache loop order.
+ */
+#ifndef JETB200_H
+#define JETB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t jt_status;
+enum { JT_OK = 0, JT_EUSAGE = 2, JT_EVALIDATION = 3, JT_ERESOURCE = 4, JT_ECUDA = 5, JT_EINTERNAL = 6 };
+
+typedef enum { JT_C64 = 0, JT_C128 = 1 } jt_dtype;
+
+typedef struct jt_network jt_network;
+typedef struct jt_plan jt_plan;
+typedef struct jt_exec jt_exec;
+
+/* Host planner options.  Zero-initialise and set what you need. */
+typedef struct {
+  uint64_t seed;          /* deterministic given the seed */
+  int32_t trials;         /* greedy trials (randomised); <=0 -> 64 */
+  int32_t threads;        /* host threads; <=0 -> hardware concurrency */
+  int32_t n_sliced;       /* number of sliced labels k (N_sl = d^k); -1 -> slice until width <= width_cap */
+  int32_t width_cap;      /* max intermediate size in log2(elements) after slicing; <=0 -> no cap */
+  int32_t reconf_sweeps;  /* subtree-reconfiguration sweeps; <0 -> default 2 */
+  int32_t reconf_leaves;  /* frontier size of the subset DP, <=10; <=0 -> 8 */
+  double time_budget_s;   /* soft wall-clock budget for the greedy trials; <=0 -> none */
+} jt_planner_opts;
+
+/* Cost counters (PAPER.md l.140-146 Eq. sliced_flops, l.205-212 Eq. task_based;
+   FLOP convention: 8 real FLOP x prod(distinct dims) per pairwise step, reading A11). */
+typedef struct {
+  int64_t n_sl;            /* N_sl = prod of sliced dims */
+  double flop_sl;          /* FLOP of one slice */
+  double flop_shared;      /* FLOP of nodes with S(v) = {} (f_sl = flop_shared / flop_sl) */
+  double e_flsl;           /* N_sl * FLOP_sl */
+  double e_fltask;         /* f_sl FLOP_sl + N_sl (1 - f_sl) FLOP_sl */
+  double exact_reuse;      /* sum_v flop_v prod_{l in S(v)} d_l  (dedup by task name) */
+  double prefix;           /* executed FLOP of the one-copy prefix cache over all slices */
+  double max_width;        /* log2 elements of the largest intermediate of one slice */
+  double bytes_sl;         /* algorithmic bytes of one slice at 8 B/elem: sum_v (|A|+|B|+|C|) */
+  int64_t n_steps;         /* SSA path length */
+  int32_t n_sliced;
+} jt_cost;
+
+/* Execution statistics accumulated by jt_exec_contract. */
+typedef struct {
+  int64_t slices_done;
+  int64_t node_launches;   /* contraction nodes executed */
+  int64_t kernel_launches; /* every kernel launched (contractions, reductions, accumulate) */
+  double flop_executed;    /* algorithmic FLOP of the executed nodes (compare with jt_cost.prefix) */
+  double bytes_executed;   /* algorithmic bytes of the executed nodes, at the exec dtype size */
+  /* filled only while profiling is on (jt_exec_set_profiling): CUDA-event time of every K2
+     contraction launch on the exec stream, and the algorithmic bytes/FLOP of those launches */
+  double k2_time_ms;
+  int64_t k2_timed_launches;
+  double k2_timed_bytes;
+  double k2_timed_flop;
+  int64_t h2d_bytes;       /* host->device bytes copied by jt_exec_create / jt_exec_upload_leaves */
+} jt_exec_stats;
+
+const char* jt_last_error(void);
+const char* jt_version(void);
+
+/* ---- network ----------------------------------------------------- */
+/* n_wires >= 1, d >= 2.  Every wire starts in |0> (l.53, l.81). */
+jt_status jt_network_create(int32_t n_wires, int32_t d, jt_network** out);
+/* k in {1,2}; wires[k] distinct in [0,n_wires); u: d^k x d^k complex, row-major U[out][in],
+   interleaved (re,im) doubles, wires[0] most significant; copied.  Error 3 after close. */
+jt_status jt_network_add_gate(jt_network* net, int32_t k, const int32_t* wires, const double* u);
+/* Attach <x_w| to every wire (l.83); x: n_wires digits in [0,d); copied; once. */
+jt_status jt_network_close(jt_network* net, const int32_t* x);
+/* Counts of the raw network (kets + gates + bras) and labels. */
+jt_status jt_network_info(const jt_network* net, int64_t* n_tensors, int64_t* n_labels);
+/* Neutral JSON file: wires, d, per tensor its labels (data are not written). */
+jt_status jt_network_export(const jt_network* net, const char* path);
+void jt_network_destroy(jt_network* net);
+
+/* ---- plan (path + slices) ------------------------------- */
+/* ssa_path: 2*n_steps ids; sliced_labels: n_sliced bond labels in loop order.  The network
+   must be closed.  Validation (error 3): ids consumed once, one tensor left, sliced labels
+   are bonds, no duplicates. */
+jt_status jt_plan_create(const jt_network* net, const int64_t* ssa_path, int64_t n_steps,
+                         const int64_t* sliced_labels, int32_t n_sliced, jt_plan** out);
+/* Host greedy planner: absorption of rank<=2 tensors, randomised greedy, subtree
+   reconfiguration, greedy slicing, slice-loop order. */
+jt_status jt_plan_greedy(const jt_network* net, const jt_planner_opts* opts, jt_plan** out);
+/* Sizes for jt_plan_get. */
+jt_status jt_plan_sizes(const jt_plan* plan, int64_t* n_steps, int32_t* n_sliced);
+/* Caller-sized buffers: ssa_path[2*n_steps], sliced_labels[n_sliced]. */
+jt_status jt_plan_get(const jt_plan* plan, int64_t* ssa_path, int64_t* sliced_labels);
+jt_status jt_plan_cost(const jt_plan* plan, jt_cost* out);
+/* Prefix-cache FLOP of the slice range [begin,end) starting with a cold cache. */
+jt_status jt_plan_prefix_flop(const jt_plan* plan, int64_t begin, int64_t end, double* flop);
+/* Neutral JSON plan file (n_tensors, ssa_path, sliced_labels) for the oracle. */
+jt_status jt_plan_export(const jt_plan* plan, const char* path);
+void jt_plan_destroy(jt_plan* plan);
+
+/* ---- execution on one B200 (the hot path) ----------------------------------------- */
+/* Device workspace bytes for this plan and dtype (leaves + intermediates with lifetime
+   reuse + prefix cache + split-K scratch + slice values). */
+jt_status jt_exec_workspace_bytes(const jt_plan* plan, jt_dtype dtype, int64_t* bytes);
+/* Caller owns d_ws (>= workspace bytes, 256-B aligned) and the stream (cudaStream_t or
+   NULL for the legacy stream).  Uploads the leaves (H2D on the stream).  Error 4 if
+   ws_bytes is too small; error 2 if d is not a power of two. */
+jt_status jt_exec_create(const jt_plan* plan, jt_dtype dtype, int32_t device, void* d_ws,
+                         int64_t ws_bytes, void* cuda_stream, jt_exec** out);
+/* Contract slices [slice_begin, slice_end) in canonical order with the prefix cache,
+   adding sum s_sigma into d_acc (device complex128, 2 doubles) in order -- async on the
+   stream.  If h_slice_vals is non-NULL the call synchronises the stream and writes
+   (end-begin) complex128 values s_sigma there.  The cache persists across calls. */
+jt_status jt_exec_contract(jt_exec* ex, int64_t slice_begin, int64_t slice_end, double* d_acc,
+                           double* h_slice_vals);
+/* Same with the prefix cache disabled: every node is recomputed for every slice (E-flsl). */
+jt_status jt_exec_contract_noreuse(jt_exec* ex, int64_t slice_begin, int64_t slice_end,
+                                   double* d_acc, double* h_slice_vals);
+/* Host-buffer path: copies nothing else; equals jt_exec_contract + D2H of the sum.  h_acc
+   receives the complex128 sum of the range (synchronous). */
+jt_status jt_exec_contract_host(jt_exec* ex, int64_t slice_begin, int64_t slice_end, double* h_acc);
+/* Re-upload the leaf tensors (the network data) from host memory through a pinned staging
+   buffer, H2D on the stream (the per-step input copy of the end-to-end path). */
+jt_status jt_exec_upload_leaves(jt_exec* ex);
+/* Profiling: bracket every K2 launch with CUDA events on the exec stream; each
+   jt_exec_contract call then synchronises and adds the event times to the stats. */
+jt_status jt_exec_set_profiling(jt_exec* ex, int32_t on);
+jt_status jt_exec_stats_get(const jt_exec* ex, jt_exec_stats* out);
+jt_status jt_exec_stats_reset(jt_exec* ex);
+/* Drop the prefix cache (next call recomputes everything). */
+jt_status jt_exec_invalidate(jt_exec* ex);
+void jt_exec_destroy(jt_exec* ex);
+
+/* 1-GPU convenience, synchronous: allocates its own workspace. out = (re, im). */
+jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, double out[2]);
+
+/* ---- K1 index permutation ("two (partial) tensor transposes") ------- */
+/* dst[pi(i)] = src[i] for a tensor of 2^n_bits elements of the dtype, where the address
+   bit b of src moves to bit perm[b] of dst (perm is a permutation of 0..n_bits-1).
+   Device pointers, async on the stream; src and dst must not overlap. */
+jt_status jt_permute(jt_dtype dtype, const void* d_src, void* d_dst, int32_t n_bits,
+                     const int32_t* perm, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JETB200_H */

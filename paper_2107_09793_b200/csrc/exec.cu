@@ -1,0 +1,669 @@
+// Slice executor: compiles a plan into per-node K2 launch
+// descriptors (bit layouts, tiles, workspace offsets) and runs the sliced contraction with
+// the one-copy prefix cache -- the paper's shared-work reuse: a node
+// v depends only on the slice digits of S(v); with slices in lexicographic order, v is
+// recomputed only when a digit at a position <= maxpos(S(v)) changes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <mutex>
+
+#include "jt_internal.hpp"
+#include "kernels.cuh"
+
+#define JT_CUDA(x)                                                                        \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      ::jt::fail(e_ == cudaErrorMemoryAllocation ? JT_ERESOURCE : JT_ECUDA,               \
+                 std::string(#x) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+
+namespace jt {
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+inline int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// A tensor view: (bit label, element stride) per address bit, unsliced bits only.
+struct View {
+  std::vector<std::pair<int64_t, int64_t>> bits;
+};
+
+struct ExecNode {
+  int64_t v = -1;
+  int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
+  std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
+  GettArgs args{};
+  int RM = 1, RN = 1, block = 32;
+  size_t smem = 0;
+  int64_t out_off = 0;   // byte offset of the output in the workspace
+  int64_t part_off = 0;  // byte offset of split-K partials
+  int64_t n_out = 1;     // output elements
+  double flop = 0, bytes = 0;
+  int maxpos = -1;
+};
+
+struct Layout {
+  int esize = 8;
+  std::vector<ExecNode> order;        // execution order (internal nodes)
+  std::vector<int64_t> leaf_off;      // byte offset of every leaf (full, unsliced data)
+  std::vector<int64_t> node_off;      // byte offset of every node output (leaves: leaf_off)
+  int64_t leaf_bytes = 0, inter_bytes = 0, scratch_bytes = 0;
+  int64_t inter_base = 0, scratch_base = 0, vals_base = 0, acc_base = 0, total = 0;
+};
+
+using GettFn = void (*)(GettArgs);
+
+template <typename R>
+GettFn pick_gett(int RM, int RN) {
+#define JT_CASE(a, b) \
+  if (RM == a && RN == b) return gett_kernel<R, a, b>;
+  JT_CASE(1, 1) JT_CASE(1, 2) JT_CASE(1, 4) JT_CASE(2, 1) JT_CASE(2, 2) JT_CASE(2, 4)
+  JT_CASE(4, 1) JT_CASE(4, 2) JT_CASE(4, 4)
+#undef JT_CASE
+  fail(JT_EINTERNAL, "no gett instance");
+}
+
+void set_smem_attrs() {
+  static std::once_flag once;
+  std::call_once(once, []() {
+    const int rms[3] = {1, 2, 4};
+    for (int a : rms)
+      for (int b : rms) {
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<float>(a, b)),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+}
+
+int ilog2_exact(int d) {
+  int b = 0;
+  while ((1 << b) < d) ++b;
+  if ((1 << b) != d) fail(JT_EUSAGE, "exec: the GPU path needs a power-of-two qudit dimension d");
+  return b;
+}
+
+// Tile selection and argument fill for one contraction (K2).  Returns the output view.
+View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
+  std::map<int64_t, int64_t> sa, sb;
+  for (auto& x : va.bits) sa[x.first] = x.second;
+  for (auto& x : vb.bits) sb[x.first] = x.second;
+  std::vector<std::pair<int64_t, int64_t>> M, N, K;  // (stride key, bit)
+  for (auto& x : va.bits) {
+    if (sb.count(x.first)) K.push_back({std::min(x.second, sb[x.first]), x.first});
+    else M.push_back({x.second, x.first});
+  }
+  for (auto& x : vb.bits)
+    if (!sa.count(x.first)) N.push_back({x.second, x.first});
+  std::sort(M.begin(), M.end());
+  std::sort(N.begin(), N.end());
+  std::sort(K.begin(), K.end());
+  const int coal = esize == 8 ? 4 : 3;
+  const int lim = esize == 8 ? 12 : 11;  // max tile bits per operand / C tile
+  std::vector<char> inM(M.size(), 0), inN(N.size(), 0), inK(K.size(), 0);
+  auto idx_of = [](const std::vector<std::pair<int64_t, int64_t>>& v, int64_t bit) {
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i].second == bit) return (int)i;
+    return -1;
+  };
+  // mandatory: the lowest `coal` address bits of each operand
+  auto mandatory = [&](const View& vw) {
+    std::vector<std::pair<int64_t, int64_t>> s;
+    for (auto& x : vw.bits) s.push_back({x.second, x.first});
+    std::sort(s.begin(), s.end());
+    for (size_t i = 0; i < s.size() && (int)i < coal; ++i) {
+      int j;
+      if ((j = idx_of(M, s[i].second)) >= 0) inM[j] = 1;
+      else if ((j = idx_of(N, s[i].second)) >= 0) inN[j] = 1;
+      else if ((j = idx_of(K, s[i].second)) >= 0) inK[j] = 1;
+    }
+  };
+  mandatory(va);
+  mandatory(vb);
+  auto cnt = [](const std::vector<char>& v) { int c = 0; for (char x : v) c += x; return c; };
+  auto add_first = [](std::vector<char>& in) {
+    for (size_t i = 0; i < in.size(); ++i)
+      if (!in[i]) { in[i] = 1; return true; }
+    return false;
+  };
+  // K: all if small, else at least up to 4 bits
+  const int kfull = esize == 8 ? 5 : 4;
+  if ((int)K.size() <= kfull)
+    for (auto& x : inK) x = 1;
+  // M up to 6 (or all), N fills the C tile, then M again
+  while (cnt(inM) < std::min<int>((int)M.size(), 6) && cnt(inM) + cnt(inN) < lim && add_first(inM)) {}
+  while (cnt(inM) + cnt(inN) < lim && add_first(inN)) {}
+  while (cnt(inM) + cnt(inN) < lim && add_first(inM)) {}
+  while (cnt(inK) < 4 && cnt(inK) + std::max(cnt(inM), cnt(inN)) < lim && add_first(inK)) {}
+  // enforce operand tile limits by dropping non-mandatory bits from the high end
+  auto drop_last = [](std::vector<char>& in, const std::vector<char>& keep) {
+    for (int i = (int)in.size() - 1; i >= 0; --i)
+      if (in[i] && !keep[i]) { in[i] = 0; return true; }
+    return false;
+  };
+  std::vector<char> keepM(M.size(), 0), keepN(N.size(), 0), keepK(K.size(), 0);
+  {  // recompute mandatory sets as keep masks
+    std::vector<char> sM = inM, sN = inN, sK = inK;
+    std::fill(inM.begin(), inM.end(), 0);
+    std::fill(inN.begin(), inN.end(), 0);
+    std::fill(inK.begin(), inK.end(), 0);
+    mandatory(va);
+    mandatory(vb);
+    keepM = inM; keepN = inN; keepK = inK;
+    inM = sM; inN = sN; inK = sK;
+  }
+  for (int guard = 0; guard < 200; ++guard) {
+    int tm = cnt(inM), tn = cnt(inN), tk = cnt(inK);
+    bool ok = tm + tk <= lim && tk + tn <= lim && tm + tn <= lim;
+    // thread-layout limit: C tile / (RM*RN) <= 256
+    int RM = std::min(4, 1 << tm), RN = std::min(4, 1 << tn);
+    ok = ok && ((1 << (tm + tn)) / (RM * RN) <= 256);
+    if (ok) break;
+    if (tm + tk > lim || tk + tn > lim) {
+      if (drop_last(inK, keepK)) continue;
+    }
+    if (tn >= tm) {
+      if (drop_last(inN, keepN)) continue;
+      if (drop_last(inM, keepM)) continue;
+    } else {
+      if (drop_last(inM, keepM)) continue;
+      if (drop_last(inN, keepN)) continue;
+    }
+    if (drop_last(inK, keepK)) continue;
+    fail(JT_EINTERNAL, "exec: cannot fit a contraction tile");
+  }
+  std::vector<int64_t> tM, tN, tK, oM, oN, oK;
+  for (size_t i = 0; i < M.size(); ++i) (inM[i] ? tM : oM).push_back(M[i].second);
+  for (size_t i = 0; i < N.size(); ++i) (inN[i] ? tN : oN).push_back(N[i].second);
+  for (size_t i = 0; i < K.size(); ++i) (inK[i] ? tK : oK).push_back(K[i].second);
+  GettArgs& g = en.args;
+  std::memset(&g, 0, sizeof(g));
+  g.tm = (int)tM.size();
+  g.tn = (int)tN.size();
+  g.tk = (int)tK.size();
+  g.nA = g.tm + g.tk;
+  g.nB = g.tk + g.tn;
+  if (g.nA > 12 || g.nB > 12) fail(JT_EINTERNAL, "exec: tile too large");
+  // A tile bits (sorted by A stride): smem index = m + (k << tm)
+  {
+    std::vector<std::pair<int64_t, std::pair<int64_t, int32_t>>> ta;
+    for (int i = 0; i < g.tm; ++i) ta.push_back({sa[tM[i]], {sa[tM[i]], 1 << i}});
+    for (int i = 0; i < g.tk; ++i) ta.push_back({sa[tK[i]], {sa[tK[i]], 1 << (g.tm + i)}});
+    std::sort(ta.begin(), ta.end());
+    for (size_t i = 0; i < ta.size(); ++i) { g.gA[i] = ta[i].second.first; g.sA[i] = ta[i].second.second; }
+    std::vector<std::pair<int64_t, std::pair<int64_t, int32_t>>> tb;
+    for (int i = 0; i < g.tn; ++i) tb.push_back({sb[tN[i]], {sb[tN[i]], 1 << i}});
+    for (int i = 0; i < g.tk; ++i) tb.push_back({sb[tK[i]], {sb[tK[i]], 1 << (g.tn + i)}});
+    std::sort(tb.begin(), tb.end());
+    for (size_t i = 0; i < tb.size(); ++i) { g.gB[i] = tb[i].second.first; g.sB[i] = tb[i].second.second; }
+  }
+  // outer bits: N (B-stride order) then M (A-stride order) -> blockIdx.x bits
+  std::vector<int64_t> outer;
+  for (auto b : oN) outer.push_back(b);
+  for (auto b : oM) outer.push_back(b);
+  if ((int)outer.size() > 31) fail(JT_ERESOURCE, "exec: too many output tiles");
+  if ((int)outer.size() > kMaxOuter || (int)oK.size() > kMaxOuter) fail(JT_EINTERNAL, "exec: too many bits");
+  g.n_outer = (int)outer.size();
+  for (int j = 0; j < g.n_outer; ++j) {
+    g.o_sA[j] = sa.count(outer[j]) ? sa[outer[j]] : 0;
+    g.o_sB[j] = sb.count(outer[j]) ? sb[outer[j]] : 0;
+  }
+  g.n_ok = (int)oK.size();
+  if (g.n_ok > 40) fail(JT_ERESOURCE, "exec: contraction too large");
+  for (int j = 0; j < g.n_ok; ++j) {
+    g.ok_sA[j] = sa[oK[j]];
+    g.ok_sB[j] = sb[oK[j]];
+  }
+  g.n_tiles = int64_t(1) << g.n_outer;
+  g.k_iters = int64_t(1) << g.n_ok;
+  en.RM = std::min(4, 1 << g.tm);
+  en.RN = std::min(4, 1 << g.tn);
+  g.TX = (1 << g.tn) / en.RN;
+  g.TY = (1 << g.tm) / en.RM;
+  const int TXY = g.TX * g.TY;
+  g.KG = std::max(1, std::min(256 / TXY, 1 << g.tk));
+  en.block = std::max(32, (TXY * g.KG + 31) / 32 * 32);
+  // cross-CTA split-K when the grid is small and the K loop is long
+  const int64_t target = 148 * 4;
+  int64_t splits = 1;
+  if (g.n_tiles < target && g.k_iters > 1) {
+    splits = std::min<int64_t>(g.k_iters, (target + g.n_tiles - 1) / g.n_tiles);
+    const int64_t cbytes = (g.n_tiles << (g.tm + g.tn)) * esize;
+    const int64_t cap = int64_t(1) << 31;  // partial buffer <= 2 GiB
+    while (splits > 1 && splits * cbytes > cap) splits /= 2;
+  }
+  g.splits = (int32_t)splits;
+  const int64_t ab = (int64_t(1) << g.nA) + (int64_t(1) << g.nB);
+  const int64_t red = (int64_t)g.KG * (int64_t(1) << (g.tm + g.tn));
+  en.smem = (size_t)(std::max(ab, red) * esize);
+  en.n_out = g.n_tiles << (g.tm + g.tn);
+  // output view: [tile N bits][tile M bits][outer bits]
+  View vc;
+  int64_t st = 1;
+  for (auto b : tN) { vc.bits.push_back({b, st}); st <<= 1; }
+  for (auto b : tM) { vc.bits.push_back({b, st}); st <<= 1; }
+  for (auto b : outer) { vc.bits.push_back({b, st}); st <<= 1; }
+  return vc;
+}
+
+Layout compile(const jt_plan& plan, int esize) {
+  Layout L;
+  L.esize = esize;
+  const jt_network& net = plan.net;
+  const int lb = ilog2_exact(net.d);
+  const int64_t nt = (int64_t)net.tensors.size();
+  const int64_t NN = (int64_t)plan.nodes.size();
+  std::vector<View> views(NN);
+  std::vector<std::vector<std::pair<int, int64_t>>> leaf_slices(nt);
+  L.leaf_off.assign(nt, 0);
+  L.node_off.assign(NN, -1);
+  int64_t off = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    const auto& ls = net.tensors[t].labels;
+    int64_t stride = 1;
+    for (int i = (int)ls.size() - 1; i >= 0; --i) {  // row-major: last label fastest
+      auto it = plan.slice_pos.find(ls[i]);
+      if (it != plan.slice_pos.end()) {
+        leaf_slices[t].push_back({it->second, stride});
+      } else {
+        for (int j = 0; j < lb; ++j) views[t].bits.push_back({ls[i] * lb + j, stride << j});
+      }
+      stride *= net.d;
+    }
+    L.leaf_off[t] = off;
+    L.node_off[t] = off;
+    off += align_up((int64_t)net.tensors[t].data.size() * esize);
+  }
+  L.leaf_bytes = off;
+  // execution order: post-order, the child with the larger peak first (Sethi-Ullman style)
+  std::vector<double> sz(NN), peak(NN);
+  for (int64_t v = 0; v < NN; ++v) sz[v] = std::exp2(plan.nodes[v].log2size);
+  for (int64_t v = 0; v < nt; ++v) peak[v] = 0;
+  for (int64_t v = nt; v < NN; ++v) {
+    const PlanNode& n = plan.nodes[v];
+    double p1 = std::max({peak[n.left], sz[n.left] + peak[n.right], sz[n.left] + sz[n.right] + sz[v]});
+    double p2 = std::max({peak[n.right], sz[n.right] + peak[n.left], sz[n.left] + sz[n.right] + sz[v]});
+    peak[v] = std::min(p1, p2);
+  }
+  std::vector<int64_t> ord;
+  {
+    std::vector<std::pair<int64_t, int>> st;
+    st.push_back({NN - 1, 0});
+    while (!st.empty()) {
+      auto& top = st.back();
+      int64_t v = top.first;
+      if (v < nt) { st.pop_back(); continue; }
+      const PlanNode& n = plan.nodes[v];
+      double p1 = std::max({peak[n.left], sz[n.left] + peak[n.right]});
+      double p2 = std::max({peak[n.right], sz[n.right] + peak[n.left]});
+      int64_t first = p1 <= p2 ? n.left : n.right, second = p1 <= p2 ? n.right : n.left;
+      if (top.second == 0) { top.second = 1; st.push_back({first, 0}); }
+      else if (top.second == 1) { top.second = 2; st.push_back({second, 0}); }
+      else { ord.push_back(v); st.pop_back(); }
+    }
+  }
+  // per node descriptors
+  std::vector<int64_t> pos(NN, -1);
+  for (size_t i = 0; i < ord.size(); ++i) pos[ord[i]] = (int64_t)i;
+  for (int64_t v : ord) {
+    const PlanNode& n = plan.nodes[v];
+    ExecNode en;
+    en.v = v;
+    auto nfree = [&](int64_t x, int64_t y) {
+      std::map<int64_t, int> s;
+      for (auto& b : views[y].bits) s[b.first] = 1;
+      int c = 0;
+      for (auto& b : views[x].bits) c += !s.count(b.first);
+      return c;
+    };
+    int fl = nfree(n.left, n.right), fr = nfree(n.right, n.left);
+    en.opA = fl <= fr ? n.left : n.right;
+    en.opB = fl <= fr ? n.right : n.left;
+    if (en.opA < nt) en.sliceA = leaf_slices[en.opA];
+    if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
+    views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
+    en.maxpos = n.maxpos;
+    en.flop = n.flop;
+    en.bytes = n.bytes8 / 8.0 * esize;
+    L.order.push_back(en);
+  }
+  // workspace: interval allocation of node outputs over execution positions.
+  // A node whose parent is recomputed more often than itself (maxpos(v) < maxpos(parent))
+  // is a prefix-cache entry and lives for the whole run.
+  struct Buf { int64_t v, size, start, end, off; };
+  std::vector<Buf> bufs;
+  const int64_t INF = std::numeric_limits<int64_t>::max();
+  for (const ExecNode& en : L.order) {
+    const int64_t v = en.v;
+    const PlanNode& n = plan.nodes[v];
+    Buf b{v, align_up(en.n_out * esize), pos[v], 0, 0};
+    if (n.parent < 0) { b.start = 0; b.end = INF; }
+    else if (plan.nodes[n.parent].maxpos > n.maxpos) { b.start = 0; b.end = INF; }
+    else b.end = pos[n.parent];
+    bufs.push_back(b);
+  }
+  std::vector<size_t> bi(bufs.size());
+  for (size_t i = 0; i < bi.size(); ++i) bi[i] = i;
+  std::sort(bi.begin(), bi.end(), [&](size_t x, size_t y) {
+    return bufs[x].size > bufs[y].size || (bufs[x].size == bufs[y].size && x < y);
+  });
+  std::vector<size_t> placed;
+  int64_t inter = 0;
+  for (size_t i : bi) {
+    Buf& b = bufs[i];
+    std::vector<std::pair<int64_t, int64_t>> occ;
+    for (size_t j : placed) {
+      const Buf& o = bufs[j];
+      if (o.start <= b.end && b.start <= o.end) occ.push_back({o.off, o.off + o.size});
+    }
+    std::sort(occ.begin(), occ.end());
+    int64_t cand = 0;
+    for (auto& iv : occ) {
+      if (cand + b.size <= iv.first) break;
+      cand = std::max(cand, iv.second);
+    }
+    b.off = cand;
+    inter = std::max(inter, cand + b.size);
+    placed.push_back(i);
+  }
+  L.inter_base = align_up(L.leaf_bytes);
+  L.inter_bytes = inter;
+  for (const Buf& b : bufs) L.node_off[b.v] = L.inter_base + b.off;
+  L.scratch_base = align_up(L.inter_base + L.inter_bytes);
+  int64_t scratch = 0;
+  for (ExecNode& en : L.order) {
+    if (en.args.splits > 1) scratch = std::max(scratch, align_up(en.n_out * esize * en.args.splits));
+    en.out_off = L.node_off[en.v];
+    en.part_off = L.scratch_base;
+  }
+  L.scratch_bytes = scratch;
+  L.vals_base = align_up(L.scratch_base + L.scratch_bytes);
+  L.acc_base = align_up(L.vals_base + plan.n_sl * 16);
+  L.total = align_up(L.acc_base + 16);
+  return L;
+}
+
+}  // namespace
+
+}  // namespace jt
+
+struct jt_exec {
+  jt::Layout L;
+  jt_dtype dtype = JT_C64;
+  int device = 0;
+  char* ws = nullptr;
+  int64_t ws_bytes = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n_sl = 1;
+  int k = 0, d = 2;
+  int64_t last = -1;  // last slice whose values are in the prefix cache, -1 = cold
+  jt_exec_stats stats{};
+  std::vector<char> host_leaves;   // leaf data converted to the exec dtype
+  char* pinned = nullptr;          // pinned staging buffer for uploads
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // event pool for K2 timing
+  size_t ev_used = 0;
+  std::vector<std::pair<double, double>> ev_work;        // (bytes, flop) of each timed launch
+  ~jt_exec() {
+    for (auto& e : ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+namespace jt {
+
+int64_t workspace_bytes(const jt_plan& plan, jt_dtype dt) {
+  return compile(plan, dt == JT_C64 ? 8 : 16).total;
+}
+
+void upload_leaves(jt_exec* ex) {
+  // the pinned buffer is reused: wait for the previous upload to finish before refilling
+  JT_CUDA(cudaStreamSynchronize(ex->stream));
+  std::memcpy(ex->pinned, ex->host_leaves.data(), ex->host_leaves.size());
+  JT_CUDA(cudaMemcpyAsync(ex->ws, ex->pinned, ex->host_leaves.size(), cudaMemcpyHostToDevice, ex->stream));
+  ex->stats.h2d_bytes += (int64_t)ex->host_leaves.size();
+}
+
+jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, int64_t ws_bytes, void* stream) {
+  if (dt != JT_C64 && dt != JT_C128) fail(JT_EUSAGE, "exec: bad dtype");
+  const int esize = dt == JT_C64 ? 8 : 16;
+  Layout L = compile(plan, esize);
+  if (!d_ws) fail(JT_EUSAGE, "exec: null workspace");
+  if ((reinterpret_cast<uintptr_t>(d_ws) % kAlign) != 0) fail(JT_EUSAGE, "exec: workspace must be 256-B aligned");
+  if (ws_bytes < L.total)
+    fail(JT_ERESOURCE, "exec: workspace too small (" + std::to_string(ws_bytes) + " < " + std::to_string(L.total) + ")");
+  JT_CUDA(cudaSetDevice(device));
+  set_smem_attrs();
+  auto* ex = new jt_exec();
+  ex->L = std::move(L);
+  ex->dtype = dt;
+  ex->device = device;
+  ex->ws = static_cast<char*>(d_ws);
+  ex->ws_bytes = ws_bytes;
+  ex->stream = static_cast<cudaStream_t>(stream);
+  ex->n_sl = plan.n_sl;
+  ex->k = (int)plan.sliced.size();
+  ex->d = plan.net.d;
+  // leaves converted to the exec dtype, uploaded through a pinned staging buffer
+  ex->host_leaves.assign(ex->L.leaf_bytes, 0);
+  const int64_t nt = (int64_t)plan.net.tensors.size();
+  for (int64_t t = 0; t < nt; ++t) {
+    const auto& data = plan.net.tensors[t].data;
+    char* dst = ex->host_leaves.data() + ex->L.leaf_off[t];
+    for (size_t i = 0; i < data.size(); ++i) {
+      if (esize == 8) {
+        float2 f = make_float2((float)data[i].real(), (float)data[i].imag());
+        std::memcpy(dst + i * 8, &f, 8);
+      } else {
+        double2 f = make_double2(data[i].real(), data[i].imag());
+        std::memcpy(dst + i * 16, &f, 16);
+      }
+    }
+  }
+  try {
+    JT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ex->pinned), std::max<int64_t>(ex->L.leaf_bytes, 16),
+                          cudaHostAllocDefault));
+    upload_leaves(ex);
+    JT_CUDA(cudaStreamSynchronize(ex->stream));
+  } catch (...) {
+    delete ex;
+    throw;
+  }
+  return ex;
+}
+
+template <typename R>
+void launch_node(jt_exec* ex, ExecNode& en, const std::vector<int>& dig) {
+  using C2 = typename V2<R>::t;
+  const Layout& L = ex->L;
+  GettArgs& g = en.args;
+  int64_t offA = 0, offB = 0;
+  for (auto& s : en.sliceA) offA += (int64_t)dig[s.first] * s.second;
+  for (auto& s : en.sliceB) offB += (int64_t)dig[s.first] * s.second;
+  g.A = reinterpret_cast<const C2*>(ex->ws + L.node_off[en.opA]) + offA;
+  g.B = reinterpret_cast<const C2*>(ex->ws + L.node_off[en.opB]) + offB;
+  g.C = ex->ws + en.out_off;
+  g.P = ex->ws + en.part_off;
+  dim3 grid((unsigned)g.n_tiles, (unsigned)g.splits);
+  GettFn fn = pick_gett<R>(en.RM, en.RN);
+  if (ex->profiling) {
+    if (ex->ev_used == ex->ev.size()) {
+      cudaEvent_t a, b;
+      JT_CUDA(cudaEventCreate(&a));
+      JT_CUDA(cudaEventCreate(&b));
+      ex->ev.push_back({a, b});
+    }
+    JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].first, ex->stream));
+  }
+  fn<<<grid, en.block, en.smem, ex->stream>>>(g);
+  if (ex->profiling) {
+    JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].second, ex->stream));
+    ex->ev_work.push_back({en.bytes, en.flop});
+    ex->ev_used++;
+  }
+  ex->stats.kernel_launches++;
+  if (g.splits > 1) {
+    int64_t n = en.n_out;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    reduce_splits_kernel<R><<<blocks, 256, 0, ex->stream>>>(reinterpret_cast<const C2*>(g.P),
+                                                             reinterpret_cast<C2*>(g.C), n, g.splits);
+    ex->stats.kernel_launches++;
+  }
+  ex->stats.node_launches++;
+  ex->stats.flop_executed += en.flop;
+  ex->stats.bytes_executed += en.bytes;
+}
+
+template <typename R>
+void contract_range(jt_exec* ex, int64_t b, int64_t e, double* d_acc, bool reuse) {
+  using C2 = typename V2<R>::t;
+  std::vector<int> dig(ex->k), prev(ex->k);
+  auto digits = [&](int64_t s, std::vector<int>& out) {
+    for (int p = ex->k - 1; p >= 0; --p) { out[p] = (int)(s % ex->d); s /= ex->d; }
+  };
+  if (ex->last >= 0) digits(ex->last, prev);
+  for (int64_t s = b; s < e; ++s) {
+    digits(s, dig);
+    int j;
+    if (!reuse || ex->last < 0) {
+      j = -1;
+    } else {
+      j = ex->k;  // nothing changed
+      for (int p = 0; p < ex->k; ++p)
+        if (dig[p] != prev[p]) { j = p; break; }
+    }
+    for (ExecNode& en : ex->L.order)
+      if (en.maxpos >= j) launch_node<R>(ex, en, dig);
+    const ExecNode& root = ex->L.order.back();
+    accumulate_kernel<R><<<1, 32, 0, ex->stream>>>(reinterpret_cast<const C2*>(ex->ws + root.out_off), d_acc,
+                                                   reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), s);
+    ex->stats.kernel_launches++;
+    ex->stats.slices_done++;
+    ex->last = s;
+    prev = dig;
+  }
+  JT_CUDA(cudaGetLastError());
+}
+
+void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_vals, bool reuse) {
+  if (b < 0 || e > ex->n_sl || b > e) fail(JT_EUSAGE, "exec: slice range out of bounds");
+  if (!d_acc) fail(JT_EUSAGE, "exec: null accumulator");
+  JT_CUDA(cudaSetDevice(ex->device));
+  ex->ev_used = 0;
+  ex->ev_work.clear();
+  if (ex->dtype == JT_C64) contract_range<float>(ex, b, e, d_acc, reuse);
+  else contract_range<double>(ex, b, e, d_acc, reuse);
+  if (ex->profiling && ex->ev_used) {
+    JT_CUDA(cudaStreamSynchronize(ex->stream));
+    for (size_t i = 0; i < ex->ev_used; ++i) {
+      float ms = 0;
+      JT_CUDA(cudaEventElapsedTime(&ms, ex->ev[i].first, ex->ev[i].second));
+      ex->stats.k2_time_ms += ms;
+      ex->stats.k2_timed_launches++;
+      ex->stats.k2_timed_bytes += ex->ev_work[i].first;
+      ex->stats.k2_timed_flop += ex->ev_work[i].second;
+    }
+  }
+  if (h_vals && e > b) {
+    JT_CUDA(cudaMemcpyAsync(h_vals, ex->ws + ex->L.vals_base + b * 16, (e - b) * 16, cudaMemcpyDeviceToHost,
+                            ex->stream));
+    JT_CUDA(cudaStreamSynchronize(ex->stream));
+  }
+}
+
+void exec_contract_host(jt_exec* ex, int64_t b, int64_t e, double* h_acc) {
+  double* d_acc = reinterpret_cast<double*>(ex->ws + ex->L.acc_base);
+  JT_CUDA(cudaSetDevice(ex->device));
+  JT_CUDA(cudaMemsetAsync(d_acc, 0, 16, ex->stream));
+  exec_contract(ex, b, e, d_acc, nullptr, true);
+  JT_CUDA(cudaMemcpyAsync(h_acc, d_acc, 16, cudaMemcpyDeviceToHost, ex->stream));
+  JT_CUDA(cudaStreamSynchronize(ex->stream));
+}
+
+void exec_invalidate(jt_exec* ex) { ex->last = -1; }
+void exec_set_profiling(jt_exec* ex, bool on) { ex->profiling = on; }
+void exec_stats(const jt_exec* ex, jt_exec_stats* out) { *out = ex->stats; }
+void exec_stats_reset(jt_exec* ex) { ex->stats = jt_exec_stats{}; }
+void exec_destroy(jt_exec* ex) { delete ex; }
+
+void amplitude(const jt_plan& plan, jt_dtype dt, int device, double out[2]) {
+  JT_CUDA(cudaSetDevice(device));
+  int64_t bytes = workspace_bytes(plan, dt);
+  void* ws = nullptr;
+  JT_CUDA(cudaMalloc(&ws, bytes));
+  jt_exec* ex = nullptr;
+  try {
+    ex = exec_create(plan, dt, device, ws, bytes, nullptr);
+    exec_contract_host(ex, 0, plan.n_sl, out);
+  } catch (...) {
+    delete ex;
+    cudaFree(ws);
+    throw;
+  }
+  delete ex;
+  JT_CUDA(cudaFree(ws));
+}
+
+// K1: dst[pi(i)] = src[i]; bit b of the source address moves to bit perm[b].
+void permute(jt_dtype dt, const void* src, void* dst, int n, const int32_t* perm, void* stream) {
+  if (n < 0 || n > 40) fail(JT_EUSAGE, "permute: n_bits out of range");
+  std::vector<int> inv(n, -1);
+  for (int b = 0; b < n; ++b) {
+    if (perm[b] < 0 || perm[b] >= n || inv[perm[b]] >= 0) fail(JT_EUSAGE, "permute: not a permutation");
+    inv[perm[b]] = b;
+  }
+  const int esize = dt == JT_C64 ? 8 : 16;
+  set_smem_attrs();
+  PermArgs p;
+  std::memset(&p, 0, sizeof(p));
+  p.src = src;
+  p.dst = dst;
+  // tile: the lowest input bits and the lowest output bits (as input bits)
+  const int half = esize == 8 ? 5 : 4;
+  std::vector<char> in_tile(n, 0);
+  for (int b = 0; b < std::min(n, half); ++b) in_tile[b] = 1;          // low input bits
+  for (int o = 0; o < std::min(n, half); ++o) in_tile[inv[o]] = 1;     // low output bits
+  for (int b = 0; b < n && std::count(in_tile.begin(), in_tile.end(), 1) < std::min(n, 2 * half); ++b)
+    in_tile[b] = 1;
+  std::vector<int> tbits, obits;
+  for (int b = 0; b < n; ++b) (in_tile[b] ? tbits : obits).push_back(b);
+  p.nt = (int)tbits.size();
+  if (p.nt > 12) fail(JT_EINTERNAL, "permute: tile too large");
+  for (int i = 0; i < p.nt; ++i) p.in_g[i] = int64_t(1) << tbits[i];
+  std::vector<std::pair<int, int>> byout;  // (output position, tile index)
+  for (int i = 0; i < p.nt; ++i) byout.push_back({perm[tbits[i]], i});
+  std::sort(byout.begin(), byout.end());
+  for (int i = 0; i < p.nt; ++i) {
+    p.out_g[i] = int64_t(1) << byout[i].first;
+    p.out_s[i] = 1 << byout[i].second;
+  }
+  p.n_outer = (int)obits.size();
+  for (int j = 0; j < p.n_outer; ++j) {
+    p.o_src[j] = int64_t(1) << obits[j];
+    p.o_dst[j] = int64_t(1) << perm[obits[j]];
+  }
+  const int64_t nblk = int64_t(1) << p.n_outer;
+  if (nblk > (int64_t(1) << 31) - 1) fail(JT_EUSAGE, "permute: tensor too large");
+  const size_t smem = (size_t)(int64_t(1) << p.nt) * esize;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (esize == 8) permute_kernel<float2><<<(unsigned)nblk, 256, smem, s>>>(p);
+  else permute_kernel<double2><<<(unsigned)nblk, 256, smem, s>>>(p);
+  JT_CUDA(cudaGetLastError());
+}
+
+}  // namespace jt

@@ -1,0 +1,84 @@
+// Circuit -> tensor network (Sec. II.B.1).
+#include <cstdio>
+#include <fstream>
+
+#include "jt_internal.hpp"
+
+using namespace jt;
+
+namespace jt {
+
+jt_network* network_create(int32_t n_wires, int32_t d) {
+  if (n_wires < 1 || d < 2) fail(JT_EUSAGE, "jt_network_create: need n_wires >= 1 and d >= 2");
+  auto* net = new jt_network();
+  net->n_wires = n_wires;
+  net->d = d;
+  net->cur.resize(n_wires);
+  for (int w = 0; w < n_wires; ++w) {  // |0>_w, rank 1 (l.81)
+    HostTensor t;
+    t.labels = {w};
+    t.data.assign(d, cplx(0, 0));
+    t.data[0] = 1.0;
+    net->tensors.push_back(std::move(t));
+    net->cur[w] = w;
+  }
+  net->n_labels = n_wires;
+  return net;
+}
+
+void network_add_gate(jt_network* net, int32_t k, const int32_t* wires, const double* u) {
+  if (!net || !wires || !u) fail(JT_EUSAGE, "jt_network_add_gate: null argument");
+  if (net->closed) fail(JT_EVALIDATION, "jt_network_add_gate: network already closed");
+  if (k != 1 && k != 2) fail(JT_EUSAGE, "jt_network_add_gate: k must be 1 or 2");
+  for (int i = 0; i < k; ++i) {
+    if (wires[i] < 0 || wires[i] >= net->n_wires) fail(JT_EUSAGE, "jt_network_add_gate: wire out of range");
+    for (int j = 0; j < i; ++j)
+      if (wires[j] == wires[i]) fail(JT_EUSAGE, "jt_network_add_gate: repeated wire");
+  }
+  const int64_t dim = (k == 1) ? net->d : int64_t(net->d) * net->d;
+  HostTensor t;
+  // labels (out_0..out_{k-1}, in_0..in_{k-1}), reading A7 (P:81 B_cfbe: outs c,f then ins b,e)
+  std::vector<int64_t> outs(k), ins(k);
+  for (int i = 0; i < k; ++i) {
+    outs[i] = net->n_labels++;
+    ins[i] = net->cur[wires[i]];
+  }
+  for (int i = 0; i < k; ++i) t.labels.push_back(outs[i]);
+  for (int i = 0; i < k; ++i) t.labels.push_back(ins[i]);
+  t.data.resize(dim * dim);
+  for (int64_t i = 0; i < dim * dim; ++i) t.data[i] = cplx(u[2 * i], u[2 * i + 1]);
+  for (int i = 0; i < k; ++i) net->cur[wires[i]] = outs[i];
+  net->tensors.push_back(std::move(t));
+  net->n_gates++;
+}
+
+void network_close(jt_network* net, const int32_t* x) {
+  if (!net || !x) fail(JT_EUSAGE, "jt_network_close: null argument");
+  if (net->closed) fail(JT_EVALIDATION, "jt_network_close: already closed");
+  for (int w = 0; w < net->n_wires; ++w)
+    if (x[w] < 0 || x[w] >= net->d) fail(JT_EUSAGE, "jt_network_close: digit out of range");
+  for (int w = 0; w < net->n_wires; ++w) {  // <x_w|, rank 1 (l.83)
+    HostTensor t;
+    t.labels = {net->cur[w]};
+    t.data.assign(net->d, cplx(0, 0));
+    t.data[x[w]] = 1.0;
+    net->tensors.push_back(std::move(t));
+  }
+  net->closed = true;
+}
+
+void network_export(const jt_network* net, const char* path) {
+  std::ofstream f(path);
+  if (!f) fail(JT_EUSAGE, std::string("cannot open ") + path);
+  f << "{\"n_wires\": " << net->n_wires << ", \"d\": " << net->d << ", \"closed\": "
+    << (net->closed ? "true" : "false") << ", \"n_labels\": " << net->n_labels << ", \"tensors\": [";
+  for (size_t t = 0; t < net->tensors.size(); ++t) {
+    f << (t ? ", " : "") << "[";
+    const auto& ls = net->tensors[t].labels;
+    for (size_t i = 0; i < ls.size(); ++i) f << (i ? ", " : "") << ls[i];
+    f << "]";
+  }
+  f << "]}\n";
+}
+
+}  // namespace jt

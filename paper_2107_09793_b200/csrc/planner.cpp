@@ -1,0 +1,685 @@
+// Host path/slice planner.  Not the hot path: the paper takes its
+// paths and slices from CoTenGra ("Our code does not perform the search
+// for optimal slices or paths"); this is a plain greedy planner so the build is
+// self-contained:
+//   1. absorb every rank<=2 tensor (kets, 1-qudit gates, bras) into a neighbour
+//      (exact re-association, emitted as the first SSA steps);
+//   2. randomised greedy pair selection (Gumbel noise, two score functions), best of
+//      many seeded trials by total FLOP, run on host threads;
+//   3. subtree reconfiguration: optimal re-contraction of <=F-subtree frontiers by
+//      subset DP (the local optimisation of Huang et al.);
+//   4. greedy slicing of labels on the largest intermediates, each pick followed by a
+//      reconfiguration sweep of the sliced tree;
+//   5. slice-loop order for the prefix cache (heaviest label outermost + local search).
+// Deterministic given the seed.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <functional>
+#include <limits>
+#include <queue>
+#include <thread>
+#include <unordered_map>
+
+#include "jt_internal.hpp"
+
+namespace jt {
+namespace {
+
+struct SplitMix {
+  uint64_t s;
+  explicit SplitMix(uint64_t seed) : s(seed) {}
+  uint64_t next() {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  double uniform() { return ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
+};
+
+// ---------------------------------------------------------------- bitsets over labels
+struct BitPool {
+  int W = 1;
+  std::vector<uint64_t> v;
+  uint64_t* at(size_t i) { return v.data() + i * W; }
+  const uint64_t* at(size_t i) const { return v.data() + i * W; }
+  size_t add() {
+    v.resize(v.size() + W, 0);
+    return v.size() / W - 1;
+  }
+};
+
+inline int pc(const uint64_t* a, int W) {
+  int c = 0;
+  for (int i = 0; i < W; ++i) c += __builtin_popcountll(a[i]);
+  return c;
+}
+inline int pc_and_not(const uint64_t* a, const uint64_t* m, int W) {
+  int c = 0;
+  for (int i = 0; i < W; ++i) c += __builtin_popcountll(a[i] & ~m[i]);
+  return c;
+}
+inline int pc_union_not(const uint64_t* a, const uint64_t* b, const uint64_t* m, int W) {
+  int c = 0;
+  for (int i = 0; i < W; ++i) c += __builtin_popcountll((a[i] | b[i]) & ~m[i]);
+  return c;
+}
+inline int pc_xor_not(const uint64_t* a, const uint64_t* b, const uint64_t* m, int W) {
+  int c = 0;
+  for (int i = 0; i < W; ++i) c += __builtin_popcountll((a[i] ^ b[i]) & ~m[i]);
+  return c;
+}
+
+// ---------------------------------------------------------------- contraction tree
+struct TNode {
+  int left = -1, right = -1, parent = -1;
+};
+
+struct Tree {
+  int W = 1;
+  int n_leaves = 0;
+  std::vector<TNode> nodes;
+  std::vector<uint64_t> lab;  // nodes.size() * W, output labels of each node
+  int root = -1;
+  uint64_t* L(int i) { return lab.data() + (size_t)i * W; }
+  const uint64_t* L(int i) const { return lab.data() + (size_t)i * W; }
+  bool leaf(int i) const { return nodes[i].left < 0; }
+};
+
+struct CostModel {
+  double log2d = 1.0;
+  std::vector<double> dpow;  // d^n
+  int cap = std::numeric_limits<int>::max();  // max output width in labels
+  double node_cost(int n_union, int n_out) const {
+    double c = dpow[n_union];
+    if (n_out > cap) c *= 1e6;  // soft width cap (in labels)
+    return c;
+  }
+};
+
+double tree_cost(const Tree& T, const CostModel& cm, const uint64_t* mask, int* maxw) {
+  double tot = 0;
+  int mw = 0;
+  for (size_t i = T.n_leaves; i < T.nodes.size(); ++i) {
+    const TNode& n = T.nodes[i];
+    if (n.left < 0) continue;
+    int u = pc_union_not(T.L(n.left), T.L(n.right), mask, T.W);
+    int o = pc_and_not(T.L((int)i), mask, T.W);
+    tot += cm.node_cost(u, o);
+    mw = std::max(mw, o);
+  }
+  for (int i = 0; i < T.n_leaves; ++i) mw = std::max(mw, pc_and_not(T.L(i), mask, T.W));
+  if (maxw) *maxw = mw;
+  return tot;
+}
+
+// post-order of internal nodes
+void postorder(const Tree& T, std::vector<int>& out) {
+  out.clear();
+  std::vector<std::pair<int, int>> st;
+  st.push_back({T.root, 0});
+  while (!st.empty()) {
+    auto& top = st.back();
+    int v = top.first;
+    if (T.leaf(v)) {
+      st.pop_back();
+      continue;
+    }
+    if (top.second == 0) {
+      top.second = 1;
+      st.push_back({T.nodes[v].left, 0});
+    } else if (top.second == 1) {
+      top.second = 2;
+      st.push_back({T.nodes[v].right, 0});
+    } else {
+      out.push_back(v);
+      st.pop_back();
+    }
+  }
+}
+
+// ---------------------------------------------------------------- greedy
+struct GreedyResult {
+  std::vector<std::pair<int, int>> pairs;  // over leaf ids then new ids n_leaves + s
+  double cost = std::numeric_limits<double>::infinity();
+};
+
+GreedyResult greedy_once(const BitPool& leaves, int n_leaves, const CostModel& cm, int variant,
+                         double temperature, uint64_t seed,
+                         const std::vector<std::vector<int>>& carriers0) {
+  const int W = leaves.W;
+  SplitMix rng(seed);
+  BitPool lab;
+  lab.W = W;
+  lab.v = leaves.v;
+  lab.v.reserve((size_t)W * 2 * n_leaves);
+  std::vector<int> size(n_leaves);
+  std::vector<char> alive(n_leaves, 1);
+  for (int i = 0; i < n_leaves; ++i) size[i] = pc(lab.at(i), W);
+  std::vector<std::vector<int>> carriers = carriers0;  // label -> tensors holding it
+  struct Cand {
+    double score;
+    int a, b;
+    bool operator<(const Cand& o) const {
+      if (score != o.score) return score > o.score;  // min-heap
+      if (a != o.a) return a > o.a;
+      return b > o.b;
+    }
+  };
+  std::priority_queue<Cand> heap;
+  std::vector<uint64_t> tmp(W);
+  auto score = [&](int a, int b) {
+    int so = 0;
+    const uint64_t* A = lab.at(a);
+    const uint64_t* B = lab.at(b);
+    for (int i = 0; i < W; ++i) so += __builtin_popcountll(A[i] ^ B[i]);
+    int sa = size[a], sb = size[b];
+    double s;
+    if (variant == 0) {
+      int mx = std::max(sa, sb);
+      s = (cm.dpow[so] - cm.dpow[sa] - cm.dpow[sb]) / cm.dpow[mx];
+    } else {
+      s = (double)(so - std::max(sa, sb));
+    }
+    if (temperature > 0) s -= temperature * std::log(-std::log(rng.uniform()));
+    return s;
+  };
+  auto push_neighbours = [&](int t) {
+    const uint64_t* A = lab.at(t);
+    std::vector<int> nb;
+    for (int w = 0; w < W; ++w) {
+      uint64_t x = A[w];
+      while (x) {
+        int bit = __builtin_ctzll(x);
+        x &= x - 1;
+        int l = w * 64 + bit;
+        for (int o : carriers[l])
+          if (o != t && alive[o]) nb.push_back(o);
+      }
+    }
+    std::sort(nb.begin(), nb.end());
+    nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+    for (int o : nb) heap.push({score(std::min(t, o), std::max(t, o)), std::min(t, o), std::max(t, o)});
+  };
+  for (int t = 0; t < n_leaves; ++t) {
+    const uint64_t* A = lab.at(t);
+    for (int w = 0; w < W; ++w) {
+      uint64_t x = A[w];
+      while (x) {
+        int bit = __builtin_ctzll(x);
+        x &= x - 1;
+        int l = w * 64 + bit;
+        for (int o : carriers[l])
+          if (o > t) heap.push({score(t, o), t, o});
+      }
+    }
+  }
+  GreedyResult res;
+  int n_alive = n_leaves;
+  double cost = 0;
+  while (n_alive > 1) {
+    int a = -1, b = -1;
+    while (!heap.empty()) {
+      Cand c = heap.top();
+      heap.pop();
+      if (alive[c.a] && alive[c.b]) {
+        a = c.a;
+        b = c.b;
+        break;
+      }
+    }
+    if (a < 0) {  // disconnected: contract the two smallest alive tensors
+      std::vector<std::pair<int, int>> al;
+      for (size_t i = 0; i < alive.size(); ++i)
+        if (alive[i]) al.push_back({size[i], (int)i});
+      std::sort(al.begin(), al.end());
+      a = std::min(al[0].second, al[1].second);
+      b = std::max(al[0].second, al[1].second);
+    }
+    size_t c = lab.add();
+    const uint64_t* A = lab.at(a);
+    const uint64_t* B = lab.at(b);
+    uint64_t* C = lab.at(c);
+    int un = 0;
+    for (int i = 0; i < W; ++i) {
+      C[i] = A[i] ^ B[i];
+      un += __builtin_popcountll(A[i] | B[i]);
+    }
+    int so = pc(C, W);
+    cost += cm.node_cost(un, so);
+    alive[a] = alive[b] = 0;
+    alive.push_back(1);
+    size.push_back(so);
+    for (int w = 0; w < W; ++w) {
+      uint64_t x = C[w];
+      while (x) {
+        int bit = __builtin_ctzll(x);
+        x &= x - 1;
+        for (int& o : carriers[w * 64 + bit])
+          if (o == a || o == b) o = (int)c;
+      }
+    }
+    res.pairs.push_back({a, b});
+    --n_alive;
+    push_neighbours((int)c);
+  }
+  res.cost = cost;
+  return res;
+}
+
+Tree tree_from_pairs(const BitPool& leaves, int n_leaves, const std::vector<std::pair<int, int>>& pairs) {
+  Tree T;
+  T.W = leaves.W;
+  T.n_leaves = n_leaves;
+  T.nodes.assign(n_leaves + pairs.size(), TNode());
+  T.lab.assign(T.nodes.size() * T.W, 0);
+  std::copy(leaves.v.begin(), leaves.v.begin() + (size_t)n_leaves * T.W, T.lab.begin());
+  for (size_t s = 0; s < pairs.size(); ++s) {
+    int v = n_leaves + (int)s;
+    auto [a, b] = pairs[s];
+    T.nodes[v].left = a;
+    T.nodes[v].right = b;
+    T.nodes[a].parent = v;
+    T.nodes[b].parent = v;
+    for (int i = 0; i < T.W; ++i) T.L(v)[i] = T.L(a)[i] ^ T.L(b)[i];
+  }
+  T.root = pairs.empty() ? 0 : n_leaves + (int)pairs.size() - 1;
+  return T;
+}
+
+// ---------------------------------------------------------------- subtree reconfiguration
+bool reconf_node(Tree& T, int v, int F, const CostModel& cm, const uint64_t* mask) {
+  const int W = T.W;
+  auto ncost = [&](int u) {
+    const TNode& n = T.nodes[u];
+    return cm.node_cost(pc_union_not(T.L(n.left), T.L(n.right), mask, W), pc_and_not(T.L(u), mask, W));
+  };
+  std::vector<int> frontier{v}, removed;
+  while ((int)frontier.size() < F) {
+    int best = -1;
+    double bc = -1;
+    for (size_t i = 0; i < frontier.size(); ++i) {
+      int u = frontier[i];
+      if (T.leaf(u)) continue;
+      double c = ncost(u);
+      if (c > bc) {
+        bc = c;
+        best = (int)i;
+      }
+    }
+    if (best < 0) break;
+    int u = frontier[best];
+    removed.push_back(u);
+    frontier[best] = T.nodes[u].left;
+    frontier.push_back(T.nodes[u].right);
+  }
+  if (removed.size() <= 1) return false;
+  double old = 0;
+  for (int u : removed) old += ncost(u);
+  const int f = (int)frontier.size();
+  const int NS = 1 << f;
+  std::vector<uint64_t> lab((size_t)NS * W, 0);
+  std::vector<double> best(NS, std::numeric_limits<double>::infinity());
+  std::vector<int> split(NS, 0);
+  for (int S = 1; S < NS; ++S) {
+    int low = __builtin_ctz(S);
+    uint64_t* LS = lab.data() + (size_t)S * W;
+    if (S == (1 << low)) {
+      std::copy(T.L(frontier[low]), T.L(frontier[low]) + W, LS);
+      best[S] = 0;
+      continue;
+    }
+    const uint64_t* Lrest = lab.data() + (size_t)(S ^ (1 << low)) * W;
+    const uint64_t* Llow = lab.data() + (size_t)(1 << low) * W;
+    for (int i = 0; i < W; ++i) LS[i] = Lrest[i] ^ Llow[i];
+    int out = pc_and_not(LS, mask, W);
+    // enumerate S1 subset of S containing the low bit, S1 != S
+    int rest = S ^ (1 << low);
+    for (int sub = rest;; sub = (sub - 1) & rest) {
+      int S1 = sub | (1 << low);
+      if (S1 != S) {
+        int S2 = S ^ S1;
+        double c1 = best[S1], c2 = best[S2];
+        if (c1 + c2 < best[S]) {
+          int un = pc_union_not(lab.data() + (size_t)S1 * W, lab.data() + (size_t)S2 * W, mask, W);
+          double c = c1 + c2 + cm.node_cost(un, out);
+          if (c < best[S]) {
+            best[S] = c;
+            split[S] = S1;
+          }
+        }
+      }
+      if (sub == 0) break;
+    }
+  }
+  if (!(best[NS - 1] < old * (1.0 - 1e-9))) return false;
+  // rebuild, reusing the removed internal ids; v stays on top
+  std::vector<int> pool(removed.rbegin(), removed.rend());  // removed[0] == v -> popped last
+  std::function<int(int, bool)> build = [&](int S, bool top) -> int {
+    if (__builtin_popcount(S) == 1) return frontier[__builtin_ctz(S)];
+    int id;
+    if (top) {
+      id = v;
+      pool.erase(std::find(pool.begin(), pool.end(), v));
+    } else {
+      id = pool.back();
+      pool.pop_back();
+      if (id == v) {  // never hand v to a non-top subset
+        int other = pool.back();
+        pool.pop_back();
+        pool.push_back(v);
+        id = other;
+      }
+    }
+    int a = build(split[S], false);
+    int b = build(S ^ split[S], false);
+    T.nodes[id].left = a;
+    T.nodes[id].right = b;
+    T.nodes[a].parent = id;
+    T.nodes[b].parent = id;
+    for (int i = 0; i < W; ++i) T.L(id)[i] = T.L(a)[i] ^ T.L(b)[i];
+    return id;
+  };
+  int parent = T.nodes[v].parent;
+  build(NS - 1, true);
+  T.nodes[v].parent = parent;
+  return true;
+}
+
+void reconf_sweeps(Tree& T, int sweeps, int F, const CostModel& cm, const uint64_t* mask) {
+  std::vector<int> order;
+  for (int s = 0; s < sweeps; ++s) {
+    postorder(T, order);
+    bool any = false;
+    for (int v : order) any |= reconf_node(T, v, F, cm, mask);
+    if (!any) break;
+  }
+}
+
+// ---------------------------------------------------------------- absorption
+struct Absorbed {
+  std::vector<int64_t> pre_path;        // SSA steps over raw ids
+  std::vector<int64_t> comp_ssa;        // SSA id of each composite tensor
+  std::vector<std::vector<int64_t>> comp_labels;
+};
+
+Absorbed absorb(const jt_network& net) {
+  const int64_t nt = (int64_t)net.tensors.size();
+  Absorbed ab;
+  std::vector<std::vector<int64_t>> labs(nt);
+  for (int64_t t = 0; t < nt; ++t) labs[t] = net.tensors[t].labels;
+  std::unordered_map<int64_t, std::vector<int64_t>> carriers;
+  for (int64_t t = 0; t < nt; ++t)
+    for (int64_t l : labs[t]) carriers[l].push_back(t);
+  std::vector<char> alive(nt, 1);
+  int64_t n_alive = nt;
+  std::vector<int64_t> queue;
+  for (int64_t t = 0; t < nt; ++t)
+    if (labs[t].size() <= 2) queue.push_back(t);
+  size_t qi = 0;
+  while (qi < queue.size() && n_alive > 1) {
+    int64_t t = queue[qi++];
+    if (!alive[t] || labs[t].size() > 2) continue;
+    // neighbour with the largest rank (ties: smallest id)
+    int64_t best = -1;
+    size_t br = 0;
+    for (int64_t l : labs[t])
+      for (int64_t o : carriers[l])
+        if (o != t && alive[o] && (best < 0 || labs[o].size() > br || (labs[o].size() == br && o < best))) {
+          best = o;
+          br = labs[o].size();
+        }
+    if (best < 0) continue;  // isolated scalar: left to the main tree
+    int64_t nid = (int64_t)labs.size();
+    std::vector<int64_t> out;
+    for (int64_t l : labs[t])
+      if (std::find(labs[best].begin(), labs[best].end(), l) == labs[best].end()) out.push_back(l);
+    for (int64_t l : labs[best])
+      if (std::find(labs[t].begin(), labs[t].end(), l) == labs[t].end()) out.push_back(l);
+    ab.pre_path.push_back(t);
+    ab.pre_path.push_back(best);
+    alive[t] = alive[best] = 0;
+    alive.push_back(1);
+    labs.push_back(out);
+    for (int64_t l : out)
+      for (auto& o : carriers[l])
+        if (o == t || o == best) o = nid;
+    --n_alive;
+    if (out.size() <= 2) queue.push_back(nid);
+  }
+  for (size_t i = 0; i < alive.size(); ++i)
+    if (alive[i]) {
+      ab.comp_ssa.push_back((int64_t)i);
+      ab.comp_labels.push_back(labs[i]);
+    }
+  return ab;
+}
+
+}  // namespace
+
+void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<int64_t>& path,
+                 std::vector<int64_t>& sliced) {
+  const int64_t nt = (int64_t)net.tensors.size();
+  Absorbed ab = absorb(net);
+  const int n_leaves = (int)ab.comp_ssa.size();
+  // compact labels
+  std::unordered_map<int64_t, int> cid;
+  std::vector<int64_t> raw_of;
+  for (auto& ls : ab.comp_labels)
+    for (int64_t l : ls)
+      if (!cid.count(l)) {
+        cid[l] = (int)raw_of.size();
+        raw_of.push_back(l);
+      }
+  const int NL = (int)raw_of.size();
+  BitPool leaves;
+  leaves.W = std::max(1, (NL + 63) / 64);
+  std::vector<std::vector<int>> carriers(NL);
+  for (int i = 0; i < n_leaves; ++i) {
+    size_t k = leaves.add();
+    for (int64_t l : ab.comp_labels[i]) {
+      int c = cid[l];
+      leaves.at(k)[c / 64] |= uint64_t(1) << (c % 64);
+      carriers[c].push_back(i);
+    }
+  }
+  CostModel cm;
+  cm.log2d = std::log2((double)net.d);
+  cm.dpow.resize(NL + 2);
+  for (int i = 0; i <= NL + 1; ++i) cm.dpow[i] = std::pow((double)net.d, (double)i);
+
+  const int trials = o.trials > 0 ? o.trials : 64;
+  int nthreads = o.threads > 0 ? o.threads : (int)std::thread::hardware_concurrency();
+  nthreads = std::max(1, std::min(nthreads, trials));
+  const int F = o.reconf_leaves > 0 ? std::min(o.reconf_leaves, 10) : 8;
+  const int sweeps = o.reconf_sweeps >= 0 ? o.reconf_sweeps : 2;
+  std::vector<uint64_t> nomask(leaves.W, 0);
+
+  Tree best_tree;
+  if (n_leaves == 1) {
+    best_tree = tree_from_pairs(leaves, 1, {});
+  } else {
+    // trials: greedy, then reconfiguration of each trial's tree; best by total cost
+    std::vector<double> tcost(trials, std::numeric_limits<double>::infinity());
+    std::vector<std::vector<std::pair<int, int>>> tpairs(trials);
+    const double temps[4] = {0.1, 0.25, 0.5, 1.0};
+    std::atomic<int> next{0};
+    auto t0 = std::chrono::steady_clock::now();
+    auto worker = [&]() {
+      for (;;) {
+        int i = next.fetch_add(1);
+        if (i >= trials) break;
+        if (o.time_budget_s > 0 && i >= nthreads) {
+          double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          if (el > o.time_budget_s) break;
+        }
+        int variant = i % 2;
+        double temp = (i < 2) ? 0.0 : temps[(i / 2) % 4];
+        GreedyResult g = greedy_once(leaves, n_leaves, cm, variant, temp,
+                                     o.seed * 0x9E3779B97F4A7C15ULL + (uint64_t)i, carriers);
+        tcost[i] = g.cost;
+        tpairs[i] = std::move(g.pairs);
+      }
+    };
+    {
+      std::vector<std::thread> th;
+      for (int t = 0; t < nthreads; ++t) th.emplace_back(worker);
+      for (auto& t : th) t.join();
+    }
+    // reconfigure the best few greedy trees (parallel), keep the best
+    std::vector<int> idx;
+    for (int i = 0; i < trials; ++i)
+      if (std::isfinite(tcost[i])) idx.push_back(i);
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return tcost[a] < tcost[b] || (tcost[a] == tcost[b] && a < b); });
+    int nre = std::min<int>((int)idx.size(), std::max(4, nthreads));
+    std::vector<Tree> trees(nre);
+    std::vector<double> rcost(nre);
+    std::atomic<int> nx{0};
+    auto rworker = [&]() {
+      for (;;) {
+        int i = nx.fetch_add(1);
+        if (i >= nre) break;
+        trees[i] = tree_from_pairs(leaves, n_leaves, tpairs[idx[i]]);
+        reconf_sweeps(trees[i], sweeps, F, cm, nomask.data());
+        rcost[i] = tree_cost(trees[i], cm, nomask.data(), nullptr);
+      }
+    };
+    {
+      std::vector<std::thread> th;
+      for (int t = 0; t < std::min(nthreads, nre); ++t) th.emplace_back(rworker);
+      for (auto& t : th) t.join();
+    }
+    int bi = 0;
+    for (int i = 1; i < nre; ++i)
+      if (rcost[i] < rcost[bi]) bi = i;
+    best_tree = std::move(trees[bi]);
+  }
+
+  // ---- slicing (labels in compact ids)
+  std::vector<uint64_t> mask(leaves.W, 0);
+  std::vector<int> chosen;
+  const int kmax = o.n_sliced;  // -1: until width cap
+  const int capw = o.width_cap > 0 ? (int)std::floor(o.width_cap / cm.log2d + 1e-9) : -1;
+  if (kmax != 0 && n_leaves > 1) {
+    for (int iter = 0; iter < 62; ++iter) {
+      int mw;
+      double cur = tree_cost(best_tree, cm, mask.data(), &mw);
+      (void)cur;
+      if (kmax >= 0 && (int)chosen.size() >= kmax) break;
+      if (kmax < 0 && (capw < 0 || mw <= capw)) break;
+      // candidates: labels on intermediates within 1 of the max width
+      std::vector<char> cand(NL, 0);
+      for (size_t v = 0; v < best_tree.nodes.size(); ++v) {
+        if (pc_and_not(best_tree.L((int)v), mask.data(), leaves.W) >= mw - 1) {
+          const uint64_t* A = best_tree.L((int)v);
+          for (int w = 0; w < leaves.W; ++w) {
+            uint64_t x = A[w] & ~mask[w];
+            while (x) {
+              int bit = __builtin_ctzll(x);
+              x &= x - 1;
+              cand[w * 64 + bit] = 1;
+            }
+          }
+        }
+      }
+      int bl = -1;
+      double bc = 0;
+      int bw = 0;
+      const bool width_first = (capw < 0) || (mw > capw);
+      for (int l = 0; l < NL; ++l) {
+        if (!cand[l]) continue;
+        mask[l / 64] |= uint64_t(1) << (l % 64);
+        int nw;
+        double c = tree_cost(best_tree, cm, mask.data(), &nw);
+        mask[l / 64] &= ~(uint64_t(1) << (l % 64));
+        bool better;
+        if (bl < 0) better = true;
+        else if (width_first) better = (nw < bw) || (nw == bw && c < bc);
+        else better = (c < bc) || (c == bc && nw < bw);
+        if (better) {
+          bl = l;
+          bc = c;
+          bw = nw;
+        }
+      }
+      if (bl < 0) break;
+      mask[bl / 64] |= uint64_t(1) << (bl % 64);
+      chosen.push_back(bl);
+      if (sweeps > 0) {
+        CostModel cmc = cm;
+        if (capw > 0) cmc.cap = capw;
+        reconf_sweeps(best_tree, 1, F, cmc, mask.data());
+      }
+    }
+  }
+
+  // ---- slice loop order: heaviest dependent FLOP outermost, then adjacent-swap search
+  const int k = (int)chosen.size();
+  std::vector<int> order(k);
+  if (k > 0) {
+    const int NN = (int)best_tree.nodes.size();
+    std::vector<uint64_t> dep(NN, 0);  // S(v) over chosen positions (chosen index)
+    std::vector<double> ncost(NN, 0);
+    std::vector<int> po;
+    postorder(best_tree, po);
+    for (int i = 0; i < n_leaves; ++i)
+      for (int c = 0; c < k; ++c)
+        if (best_tree.L(i)[chosen[c] / 64] & (uint64_t(1) << (chosen[c] % 64))) dep[i] |= uint64_t(1) << c;
+    for (int v : po) {
+      const TNode& n = best_tree.nodes[v];
+      dep[v] = dep[n.left] | dep[n.right];
+      ncost[v] = cm.dpow[pc_union_not(best_tree.L(n.left), best_tree.L(n.right), mask.data(), leaves.W)];
+    }
+    std::vector<double> wt(k, 0);
+    for (int v : po)
+      for (int c = 0; c < k; ++c)
+        if (dep[v] & (uint64_t(1) << c)) wt[c] += ncost[v];
+    for (int c = 0; c < k; ++c) order[c] = c;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return wt[a] > wt[b]; });
+    auto prefix_cost = [&](const std::vector<int>& ord) {
+      std::vector<int> pos(k);
+      for (int p = 0; p < k; ++p) pos[ord[p]] = p;
+      double tot = 0;
+      for (int v : po) {
+        int mp = -1;
+        for (int c = 0; c < k; ++c)
+          if (dep[v] & (uint64_t(1) << c)) mp = std::max(mp, pos[c]);
+        tot += ncost[v] * cm.dpow[mp + 1];
+      }
+      return tot;
+    };
+    double cur = prefix_cost(order);
+    for (bool improved = true; improved;) {
+      improved = false;
+      for (int p = 0; p + 1 < k; ++p) {
+        std::swap(order[p], order[p + 1]);
+        double c = prefix_cost(order);
+        if (c < cur * (1 - 1e-12)) {
+          cur = c;
+          improved = true;
+        } else {
+          std::swap(order[p], order[p + 1]);
+        }
+      }
+    }
+  }
+  sliced.clear();
+  for (int p = 0; p < k; ++p) sliced.push_back(raw_of[chosen[order[p]]]);
+
+  // ---- emit the SSA path over raw ids: absorption steps, then the tree in post-order
+  path = ab.pre_path;
+  int64_t next_id = nt + (int64_t)ab.pre_path.size() / 2;
+  std::vector<int64_t> ssa(best_tree.nodes.size(), -1);
+  for (int i = 0; i < n_leaves; ++i) ssa[i] = ab.comp_ssa[i];
+  std::vector<int> po;
+  if (n_leaves > 1) postorder(best_tree, po);
+  for (int v : po) {
+    path.push_back(ssa[best_tree.nodes[v].left]);
+    path.push_back(ssa[best_tree.nodes[v].right]);
+    ssa[v] = next_id++;
+  }
+}
+
+}  // namespace jt

@@ -1,0 +1,71 @@
+"""Multi-GPU driver: slices are independent ("embarrassingly
+(data-) parallel ... collect the results through a single reduction"), so rank g of G
+contracts the contiguous block of the canonical slice order whose outermost slice digits
+equal g (the prefix cache stays effective inside a block), and the per-rank complex128
+partial sums are combined by ONE all-reduce (NCCL over NVLink on GPUs, gloo in CPU tests).
+"""
+
+import numpy as np
+
+
+def shard_range(n_sl: int, rank: int, world: int):
+    """Contiguous block of [0, n_sl) for `rank`; blocks are disjoint, cover [0, n_sl), and
+    differ in size by at most one slice.  For n_sl = d^k and world = d^j the blocks are
+    exactly the sets of slices whose j outermost digits equal `rank`."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    b = rank * n_sl // world
+    e = (rank + 1) * n_sl // world
+    return b, e
+
+
+def allreduce_amplitude(acc, group=None):
+    """One SUM all-reduce of the 2-double accumulator (16 bytes per amplitude)."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    return acc
+
+
+def run_amplitude(plan, dtype="c64", exec_=None, slices=None):
+    """Amplitude <x|U|0> = sum over all slices, sharded over the process group.
+
+    Each rank contracts its block on its own GPU (current CUDA device) into a device
+    complex128 accumulator, then one all-reduce; returns (amplitude, per-rank info)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import jet
+
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    n_sl = plan.cost()["n_sl"]
+    b, e = slices if slices is not None else shard_range(n_sl, rank, world)
+    ex = exec_ if exec_ is not None else jet.Exec(plan, dtype)
+    acc = torch.zeros(2, dtype=torch.float64, device=ex.device)
+    if e > b:
+        ex.contract(b, e, acc)
+    allreduce_amplitude(acc)
+    a = acc.cpu().numpy()
+    return complex(a[0], a[1]), {"rank": rank, "world": world, "range": (b, e)}
+
+
+def host_shard_sum(values_per_rank):
+    """Reference combination used by the CPU tests: canonical per-rank sums, then the sum of
+    rank partials in rank order (what a ring all-reduce computes up to rounding order)."""
+    parts = []
+    for vals in values_per_rank:
+        acc = 0j
+        for v in vals:
+            acc += v
+        parts.append(acc)
+    tot = 0j
+    for p in parts:
+        tot += p
+    return tot, parts
+
+
+def as_complex(acc_np):
+    a = np.asarray(acc_np, dtype=np.float64)
+    return complex(a[0], a[1])

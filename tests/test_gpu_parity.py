@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star, reading A13): relative amplitude error 1e-4 for
+complex64 and 1e-10 for complex128, rel = |a_gpu - a_ora| / |a_ora|; every s_sigma is
+compared with the same rule.  K1 permutes are compared bit-exactly."""
+
+import math
+
+import numpy as np
+import pytest
+
+from circuits import Circuit, generate_gbs, grid_rqc, random_bitstring, workload
+from circuits.sycamore import random_circuit, sycamore_qubits
+from oracle import contract, statevector
+from oracle.network import build_network
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": 1e-4, "c128": 1e-10}
+
+
+@pytest.fixture(scope="module")
+def jet():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2107_09793_b200 import jet as j
+
+    torch.cuda.set_device(0)
+    return j
+
+
+def run(jet, plan, dtype, reuse=True, ranges=None):
+    import torch
+
+    ex = jet.Exec(plan, dtype)
+    n_sl = plan.cost()["n_sl"]
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    vals = []
+    for b, e in (ranges or [(0, n_sl)]):
+        vals.append(ex.contract(b, e, acc, slice_values=True, reuse=reuse))
+    torch.cuda.synchronize()
+    return complex(acc[0].item(), acc[1].item()), np.concatenate(vals), ex
+
+
+def rel(a, b):
+    return abs(a - b) / abs(b)
+
+
+# ----------------------------------------------------------------------------- K1 permute
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [0, 1, 3, 7, 12, 16, 21])
+def test_permute_bit_exact(jet, dtype, n):
+    import torch
+
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    rng = np.random.default_rng(n)
+    src = torch.randn(1 << n, dtype=tdt, device="cuda")
+    perms = [list(range(n)), list(reversed(range(n))), list(rng.permutation(n))]
+    if n >= 4:
+        perms.append(list(range(1, n)) + [0])
+    idx = np.arange(1 << n)
+    s = src.cpu().numpy()
+    for perm in perms:
+        dst = jet.permute(src, perm)
+        didx = np.zeros_like(idx)
+        for b, p in enumerate(perm):
+            didx |= ((idx >> b) & 1) << int(p)
+        want = np.empty_like(s)
+        want[didx] = s
+        assert np.array_equal(dst.cpu().numpy(), want)
+
+
+# ----------------------------------------------------------------------------- C1 (3x3, m=8)
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [0, 2, 4])
+def test_c1_parity_vs_oracle_and_statevector(jet, dtype, k):
+    circ, _ = workload("C1")
+    psi = statevector.final_state(circ)
+    for seed in range(6):
+        bits = random_bitstring(9, 2, 100 + seed)
+        net = jet.Network.from_circuit(circ, bits)
+        plan = jet.Plan.greedy(net, seed=seed, trials=16, n_sliced=k)
+        onet = build_network(circ, bits)
+        ref_vals = contract.slice_values(onet, plan.ssa_path, plan.sliced_labels)
+        ref = sum(ref_vals)
+        assert abs(ref - psi[tuple(bits)]) < 1e-12
+        amp, vals, _ = run(jet, plan, dtype)
+        assert rel(amp, ref) < TOL[dtype]
+        for v, r in zip(vals, ref_vals):
+            assert abs(v - r) <= TOL[dtype] * max(abs(r), 1e-3 * abs(ref))
+
+
+def test_reuse_on_off_bitwise_and_ranges(jet):
+    """P10: prefix-cache reuse on vs off gives bitwise-identical s_sigma; splitting the slice
+    range across calls (the cache persists) also gives identical values."""
+    circ, bits = workload("C1")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=3, trials=16, n_sliced=5)
+    n = plan.cost()["n_sl"]
+    for dtype in ("c64", "c128"):
+        _, v_on, ex_on = run(jet, plan, dtype, reuse=True)
+        _, v_off, ex_off = run(jet, plan, dtype, reuse=False)
+        _, v_rng, _ = run(jet, plan, dtype, ranges=[(0, 7), (7, 19), (19, n)])
+        assert np.array_equal(v_on, v_off)
+        assert np.array_equal(v_on, v_rng)
+        # executed FLOP equals the cost model (P12): prefix cache vs E-flsl
+        c = plan.cost()
+        assert ex_on.stats()["flop_executed"] == c["prefix"]
+        assert ex_off.stats()["flop_executed"] == c["e_flsl"]
+
+
+def test_contract_host_and_amplitude_api(jet):
+    circ, bits = workload("C1")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=8, n_sliced=2)
+    ref = contract.amplitude(build_network(circ, bits), plan.ssa_path, plan.sliced_labels)
+    ex = jet.Exec(plan, "c128")
+    assert rel(ex.contract_host(0, 4), ref) < 1e-10
+    assert rel(jet.amplitude(plan, "c128"), ref) < 1e-10
+    assert rel(jet.amplitude(plan, "c64"), ref) < 1e-4
+
+
+def test_errors(jet):
+    import torch
+
+    circ, bits = workload("C1")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=8, n_sliced=2)
+    import ctypes
+    from paper_2107_09793_b200.jet import _check, _lib, c_vp
+
+    small = torch.empty(256, dtype=torch.uint8, device="cuda")
+    h = c_vp()
+    with pytest.raises(jet.JetError) as e:
+        _check(_lib.jt_exec_create(plan._h, 0, 0, c_vp(small.data_ptr()), 256, None, ctypes.byref(h)))
+    assert e.value.code == 4
+    ex = jet.Exec(plan, "c64")
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    with pytest.raises(jet.JetError) as e:
+        ex.contract(0, 5, acc)
+    assert e.value.code == 2
+    q = Circuit(2, 3)
+    q.add((0, 1), np.eye(9))
+    qnet = jet.Network.from_circuit(q, [0, 0])
+    qplan = jet.Plan.greedy(qnet)
+    with pytest.raises(jet.JetError) as e:
+        jet.Exec(qplan, "c64")
+    assert e.value.code == 2
+
+
+# ----------------------------------------------------------------------------- GBS (qudits, d=4)
+@pytest.mark.parametrize("dim,width", [(2, 2), (3, 2)])
+def test_gbs_parity_and_closed_forms(jet, dim, width):
+    r, d = 0.5, 4
+    circ = generate_gbs(dim, width, 1, r, d, seed=9)
+    M = circ.n_wires
+    cases = [[0] * M, random_bitstring(M, d, 1), random_bitstring(M, d, 2)]
+    x = [0] * M
+    x[0] = x[M - 1] = 1
+    cases.append(x)
+    for k, bits in enumerate(cases):
+        net = jet.Network.from_circuit(circ, bits)
+        plan = jet.Plan.greedy(net, seed=k, trials=16, n_sliced=min(k, 2))
+        ref = contract.amplitude(build_network(circ, bits), plan.ssa_path, plan.sliced_labels)
+        amp, _, _ = run(jet, plan, "c128")
+        if abs(ref) < 1e-14:
+            assert abs(amp) < 1e-14
+        else:
+            assert rel(amp, ref) < 1e-10
+        if bits == [0] * M:
+            assert abs(amp - math.cosh(r) ** (-M / 2)) < 1e-12            # P8 vacuum
+
+
+# ----------------------------------------------------------------------------- C2 (Sycamore-53 m=10)
+@pytest.fixture(scope="module")
+def c2_plan(jet):
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=256, n_sliced=6)
+    return circ, bits, net, plan
+
+
+def test_c2_full_parity(jet, c2_plan):
+    circ, bits, net, plan = c2_plan
+    onet = build_network(circ, bits)
+    ref_vals = contract.slice_values(onet, plan.ssa_path, plan.sliced_labels)
+    ref = sum(ref_vals)
+    assert abs(ref) ** 2 * 2 ** 53 > 0.01                                    # reading A13
+    amp, vals, ex = run(jet, plan, "c64")
+    assert rel(amp, ref) < 1e-4
+    for v, r in zip(vals, ref_vals):
+        assert abs(v - r) <= 1e-4 * abs(r)
+    assert ex.stats()["flop_executed"] == plan.cost()["prefix"]
+
+
+def test_c2_fsim_identity_closed_form(jet):
+    """P7: fSim(0,0) = I makes the 53-qubit circuit a product of 1-qubit chains, so
+    <x|U|0> = prod_q <x_q|V_q|0>; same network structure and cost as C2."""
+    qs = sycamore_qubits(53)
+    circ = random_circuit(qs, 10, seed=1, theta=0.0, phi=0.0)
+    bits = random_bitstring(53, 2, 1)
+    want = 1 + 0j
+    for q in range(53):
+        v = np.array([1, 0], dtype=np.complex128)
+        for g in circ.gates:
+            if g.wires == (q,):
+                v = g.u @ v
+        want *= v[bits[q]]
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6)
+    for dtype in ("c64", "c128"):
+        amp, _, _ = run(jet, plan, dtype)
+        assert rel(amp, want) < TOL[dtype]
