@@ -59,6 +59,9 @@ typedef struct {
   int32_t reconf_sweeps;  /* subtree-reconfiguration sweeps; <0 -> default 2 */
   int32_t reconf_leaves;  /* frontier size of the subset DP, <=10; <=0 -> 8 */
   double time_budget_s;   /* soft wall-clock budget for the greedy trials; <=0 -> none */
+  double bytes_weight;    /* roofline objective: node cost = max(d^union, w (|A|+|B|+|C|)) with
+                             w = peak FLOP/s * esize / (8 * HBM B/s); <=0 -> pure FLOP (d^union) */
+  int32_t candidates;     /* greedy trees carried through reconfiguration + slicing; <=0 -> 8 */
 } jt_planner_opts;
 
 /* Cost counters (PAPER.md l.140-146 Eq. sliced_flops, l.205-212 Eq. task_based;
@@ -134,6 +137,9 @@ void jt_plan_destroy(jt_plan* plan);
 /* Device workspace bytes for this plan and dtype (leaves + intermediates with lifetime
    reuse + prefix cache + split-K scratch + slice values). */
 jt_status jt_exec_workspace_bytes(const jt_plan* plan, jt_dtype dtype, int64_t* bytes);
+/* Host only: write the compiled per-node launch plan (tiles, grid, split-K, bytes, FLOP,
+   prefix-cache level) and the workspace layout as JSON (for analysis and DESIGN.md). */
+jt_status jt_exec_describe(const jt_plan* plan, jt_dtype dtype, const char* path);
 /* Caller owns d_ws (>= workspace bytes, 256-B aligned) and the stream (cudaStream_t or
    NULL for the legacy stream).  Uploads the leaves (H2D on the stream).  Error 4 if
    ws_bytes is too small; error 2 if d is not a power of two. */
@@ -165,6 +171,13 @@ void jt_exec_destroy(jt_exec* ex);
 
 /* 1-GPU convenience, synchronous: allocates its own workspace. out = (re, im). */
 jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, double out[2]);
+
+/* TEST ONLY (never called by jt_exec_*): execute the compiled K2 descriptors, workspace
+   layout and prefix-cache schedule for slices [b,e) on the host with the kernels' index
+   arithmetic, writing s_sigma to h_vals (2*(e-b) doubles).  Lets CPU tests check the plan
+   compiler and the scheduler against the oracle without a GPU; tiny plans only. */
+jt_status jt_debug_emulate_host(const jt_plan* plan, jt_dtype dtype, int64_t b, int64_t e, double* h_vals,
+                                int32_t reuse);
 
 /* ---- K1 index permutation ("two (partial) tensor transposes") ------- */
 /* dst[pi(i)] = src[i] for a tensor of 2^n_bits elements of the dtype, where the address

@@ -12,6 +12,8 @@ void network_close(jt_network* net, const int32_t* x);
 void network_export(const jt_network* net, const char* path);
 void plan_export(const jt_plan* plan, const char* path);
 int64_t workspace_bytes(const jt_plan& plan, jt_dtype dt);
+void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path);
+void debug_emulate_host(const jt_plan& plan, jt_dtype dt, int64_t b, int64_t e, double* h_vals, bool reuse);
 jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, int64_t ws_bytes, void* stream);
 void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_vals, bool reuse);
 void exec_contract_host(jt_exec* ex, int64_t b, int64_t e, double* h_acc);
@@ -167,6 +169,12 @@ jt_status jt_exec_workspace_bytes(const jt_plan* plan, jt_dtype dtype, int64_t* 
     *bytes = workspace_bytes(*plan, dtype);
   });
 }
+jt_status jt_exec_describe(const jt_plan* plan, jt_dtype dtype, const char* path) {
+  return guarded([&] {
+    NEED(plan && path, "jt_exec_describe");
+    describe_exec(*plan, dtype, path);
+  });
+}
 jt_status jt_exec_create(const jt_plan* plan, jt_dtype dtype, int32_t device, void* d_ws, int64_t ws_bytes,
                          void* cuda_stream, jt_exec** out) {
   return guarded([&] {
@@ -223,6 +231,14 @@ jt_status jt_exec_invalidate(jt_exec* ex) {
   });
 }
 void jt_exec_destroy(jt_exec* ex) { exec_destroy(ex); }
+
+jt_status jt_debug_emulate_host(const jt_plan* plan, jt_dtype dtype, int64_t b, int64_t e, double* h_vals,
+                                int32_t reuse) {
+  return guarded([&] {
+    NEED(plan && (h_vals || b == e), "jt_debug_emulate_host");
+    debug_emulate_host(*plan, dtype, b, e, h_vals, reuse != 0);
+  });
+}
 
 jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, double out[2]) {
   return guarded([&] {

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -395,6 +396,120 @@ Layout compile(const jt_plan& plan, int esize) {
   return L;
 }
 
+
+// ---------------------------------------------------------------- debug: host emulation
+// Test-only (jt_debug_emulate_host): executes the compiled K2 descriptors, the workspace
+// layout and the prefix-cache schedule on host memory with the kernel's exact index
+// arithmetic, so descriptor/layout/scheduling bugs are caught by CPU tests.  Never used by
+// jt_exec_* (there is no CPU execution path in the product).
+template <typename R>
+void emulate_gett(const GettArgs& p, char* ws, const ExecNode& en, const std::vector<std::pair<int64_t, int64_t>>& ab_off) {
+  using C2 = typename V2<R>::t;
+  (void)en;
+  const C2* A = reinterpret_cast<const C2*>(ws + ab_off[0].first) + ab_off[0].second;
+  const C2* B = reinterpret_cast<const C2*>(ws + ab_off[1].first) + ab_off[1].second;
+  C2* C = reinterpret_cast<C2*>(ws + ab_off[2].first);
+  C2* P = reinterpret_cast<C2*>(ws + ab_off[3].first);
+  int64_t tgA[2][64], tgB[2][64];
+  int32_t tsA[2][64], tsB[2][64];
+  for (int i = 0; i < 64; ++i)
+    for (int h = 0; h < 2; ++h) {
+      int64_t g = 0, gb = 0;
+      int32_t s = 0, sb = 0;
+      for (int b = 0; b < 6; ++b)
+        if ((i >> b) & 1) {
+          const int bi = 6 * h + b;
+          if (bi < p.nA) { g += p.gA[bi]; s += p.sA[bi]; }
+          if (bi < p.nB) { gb += p.gB[bi]; sb += p.sB[bi]; }
+        }
+      tgA[h][i] = g; tsA[h][i] = s; tgB[h][i] = gb; tsB[h][i] = sb;
+    }
+  std::vector<C2> sA(size_t(1) << p.nA), sB(size_t(1) << p.nB), acc(size_t(1) << (p.tm + p.tn));
+  for (int64_t tile = 0; tile < p.n_tiles; ++tile)
+    for (int split = 0; split < p.splits; ++split) {
+      int64_t baseA = 0, baseB = 0;
+      for (int j = 0; j < p.n_outer; ++j)
+        if ((tile >> j) & 1) { baseA += p.o_sA[j]; baseB += p.o_sB[j]; }
+      const int64_t it0 = (int64_t)split * p.k_iters / p.splits, it1 = (int64_t)(split + 1) * p.k_iters / p.splits;
+      for (auto& x : acc) { x.x = 0; x.y = 0; }
+      for (int64_t it = it0; it < it1; ++it) {
+        int64_t oa = baseA, ob = baseB;
+        for (int j = 0; j < p.n_ok; ++j)
+          if ((it >> j) & 1) { oa += p.ok_sA[j]; ob += p.ok_sB[j]; }
+        for (int e = 0; e < (1 << p.nA); ++e) sA[tsA[0][e & 63] + tsA[1][e >> 6]] = A[oa + tgA[0][e & 63] + tgA[1][e >> 6]];
+        for (int e = 0; e < (1 << p.nB); ++e) sB[tsB[0][e & 63] + tsB[1][e >> 6]] = B[ob + tgB[0][e & 63] + tgB[1][e >> 6]];
+        for (int k = 0; k < (1 << p.tk); ++k)
+          for (int m = 0; m < (1 << p.tm); ++m)
+            for (int n = 0; n < (1 << p.tn); ++n) {
+              const C2 a = sA[(k << p.tm) + m], b = sB[(k << p.tn) + n];
+              C2& c = acc[(m << p.tn) + n];
+              c.x += a.x * b.x - a.y * b.y;
+              c.y += a.x * b.y + a.y * b.x;
+            }
+      }
+      C2* out = p.splits == 1 ? C : P;
+      const int64_t base = ((int64_t)(p.splits == 1 ? 0 : split) * p.n_tiles + tile) << (p.tm + p.tn);
+      for (size_t i = 0; i < acc.size(); ++i) out[base + i] = acc[i];
+    }
+  if (p.splits > 1) {
+    const int64_t n = p.n_tiles << (p.tm + p.tn);
+    for (int64_t i = 0; i < n; ++i) {
+      C2 s = P[i];
+      for (int k = 1; k < p.splits; ++k) { s.x += P[k * n + i].x; s.y += P[k * n + i].y; }
+      C[i] = s;
+    }
+  }
+}
+
+template <typename R>
+void emulate_host(const jt_plan& plan, int esize, int64_t b, int64_t e, double* h_vals, bool reuse) {
+  using C2 = typename V2<R>::t;
+  Layout L = compile(plan, esize);
+  std::vector<char> ws(L.total, 0);
+  const int64_t nt = (int64_t)plan.net.tensors.size();
+  for (int64_t t = 0; t < nt; ++t) {
+    const auto& data = plan.net.tensors[t].data;
+    C2* dst = reinterpret_cast<C2*>(ws.data() + L.leaf_off[t]);
+    for (size_t i = 0; i < data.size(); ++i) { dst[i].x = (R)data[i].real(); dst[i].y = (R)data[i].imag(); }
+  }
+  const int k = (int)plan.sliced.size(), d = plan.net.d;
+  std::vector<int> dig(k), prev(k);
+  int64_t last = -1;
+  for (int64_t s = b; s < e; ++s) {
+    int64_t x = s;
+    for (int q = k - 1; q >= 0; --q) { dig[q] = (int)(x % d); x /= d; }
+    int j = -1;
+    if (reuse && last >= 0) {
+      j = k;
+      for (int q = 0; q < k; ++q)
+        if (dig[q] != prev[q]) { j = q; break; }
+    }
+    for (const ExecNode& en : L.order) {
+      if (en.maxpos < j) continue;
+      int64_t offA = 0, offB = 0;
+      for (auto& sl : en.sliceA) offA += (int64_t)dig[sl.first] * sl.second;
+      for (auto& sl : en.sliceB) offB += (int64_t)dig[sl.first] * sl.second;
+      std::vector<std::pair<int64_t, int64_t>> offs = {{L.node_off[en.opA], offA}, {L.node_off[en.opB], offB},
+                                                       {en.out_off, 0}, {en.part_off, 0}};
+      emulate_gett<R>(en.args, ws.data(), en, offs);
+    }
+    const C2 r = *reinterpret_cast<const C2*>(ws.data() + L.order.back().out_off);
+    h_vals[2 * (s - b)] = (double)r.x;
+    h_vals[2 * (s - b) + 1] = (double)r.y;
+    last = s;
+    prev = dig;
+  }
+}
+
+}  // namespace
+
+void debug_emulate_host(const jt_plan& plan, jt_dtype dt, int64_t b, int64_t e, double* h_vals, bool reuse) {
+  if (b < 0 || e > plan.n_sl || b > e) fail(JT_EUSAGE, "emulate: bad range");
+  if (dt == JT_C64) emulate_host<float>(plan, 8, b, e, h_vals, reuse);
+  else emulate_host<double>(plan, 16, b, e, h_vals, reuse);
+}
+
+namespace {
 }  // namespace
 
 }  // namespace jt
@@ -426,6 +541,25 @@ struct jt_exec {
 };
 
 namespace jt {
+
+void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
+  Layout L = compile(plan, dt == JT_C64 ? 8 : 16);
+  FILE* f = std::fopen(path, "w");
+  if (!f) fail(JT_EUSAGE, std::string("cannot open ") + path);
+  std::fprintf(f, "{\"total_bytes\": %lld, \"leaf_bytes\": %lld, \"inter_bytes\": %lld, \"scratch_bytes\": %lld, \"nodes\": [",
+               (long long)L.total, (long long)L.leaf_bytes, (long long)L.inter_bytes, (long long)L.scratch_bytes);
+  for (size_t i = 0; i < L.order.size(); ++i) {
+    const ExecNode& en = L.order[i];
+    const GettArgs& g = en.args;
+    std::fprintf(f, "%s{\"v\": %lld, \"maxpos\": %d, \"flop\": %.17g, \"bytes\": %.17g, \"n_out\": %lld, "
+                 "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
+                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu}",
+                 i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
+                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem);
+  }
+  std::fprintf(f, "]}\n");
+  std::fclose(f);
+}
 
 int64_t workspace_bytes(const jt_plan& plan, jt_dtype dt) {
   return compile(plan, dt == JT_C64 ? 8 : 16).total;

@@ -62,20 +62,20 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
   __shared__ int64_t tgA[2][64], tgB[2][64];
   __shared__ int32_t tsA[2][64], tsB[2][64];
   const int tid = threadIdx.x;
-  if (tid < 64) {
+  for (int i = tid; i < 64; i += blockDim.x) {
     // lo tables: tile bits 0..5; hi tables: tile bits 6..11 (of the stride-sorted order)
     for (int h = 0; h < 2; ++h) {
       int64_t g = 0, gb = 0;
       int32_t s = 0, sb = 0;
       for (int b = 0; b < 6; ++b) {
-        if ((tid >> b) & 1) {
+        if ((i >> b) & 1) {
           const int bi = 6 * h + b;
           if (bi < p.nA) { g += p.gA[bi]; s += p.sA[bi]; }
           if (bi < p.nB) { gb += p.gB[bi]; sb += p.sB[bi]; }
         }
       }
-      tgA[h][tid] = g; tsA[h][tid] = s;
-      tgB[h][tid] = gb; tsB[h][tid] = sb;
+      tgA[h][i] = g; tsA[h][i] = s;
+      tgB[h][i] = gb; tsB[h][i] = sb;
     }
   }
   __syncthreads();
@@ -202,16 +202,16 @@ __global__ void __launch_bounds__(256) permute_kernel(const __grid_constant__ Pe
   __shared__ int64_t tin[2][64], tout[2][64];
   __shared__ int32_t tso[2][64];
   const int tid = threadIdx.x;
-  if (tid < 64) {
+  for (int i = tid; i < 64; i += blockDim.x) {
     for (int h = 0; h < 2; ++h) {
       int64_t gi = 0, go = 0;
       int32_t so = 0;
       for (int b = 0; b < 6; ++b)
-        if ((tid >> b) & 1) {
+        if ((i >> b) & 1) {
           const int bi = 6 * h + b;
           if (bi < p.nt) { gi += p.in_g[bi]; go += p.out_g[bi]; so += p.out_s[bi]; }
         }
-      tin[h][tid] = gi; tout[h][tid] = go; tso[h][tid] = so;
+      tin[h][i] = gi; tout[h][i] = go; tso[h][i] = so;
     }
   }
   __syncthreads();

@@ -92,8 +92,11 @@ struct CostModel {
   double log2d = 1.0;
   std::vector<double> dpow;  // d^n
   int cap = std::numeric_limits<int>::max();  // max output width in labels
-  double node_cost(int n_union, int n_out) const {
+  double R = 0;  // roofline weight: FLOP/8 per element moved (0 = pure FLOP objective)
+  // Roofline time model in FLOP/8 units: max(d^union, R (|A|+|B|+|C|)).
+  double node_cost(int n_union, int n_a, int n_b, int n_out) const {
     double c = dpow[n_union];
+    if (R > 0) c = std::max(c, R * (dpow[n_a] + dpow[n_b] + dpow[n_out]));
     if (n_out > cap) c *= 1e6;  // soft width cap (in labels)
     return c;
   }
@@ -107,7 +110,7 @@ double tree_cost(const Tree& T, const CostModel& cm, const uint64_t* mask, int* 
     if (n.left < 0) continue;
     int u = pc_union_not(T.L(n.left), T.L(n.right), mask, T.W);
     int o = pc_and_not(T.L((int)i), mask, T.W);
-    tot += cm.node_cost(u, o);
+    tot += cm.node_cost(u, pc_and_not(T.L(n.left), mask, T.W), pc_and_not(T.L(n.right), mask, T.W), o);
     mw = std::max(mw, o);
   }
   for (int i = 0; i < T.n_leaves; ++i) mw = std::max(mw, pc_and_not(T.L(i), mask, T.W));
@@ -248,7 +251,7 @@ GreedyResult greedy_once(const BitPool& leaves, int n_leaves, const CostModel& c
       un += __builtin_popcountll(A[i] | B[i]);
     }
     int so = pc(C, W);
-    cost += cm.node_cost(un, so);
+    cost += cm.node_cost(un, size[a], size[b], so);
     alive[a] = alive[b] = 0;
     alive.push_back(1);
     size.push_back(so);
@@ -294,7 +297,8 @@ bool reconf_node(Tree& T, int v, int F, const CostModel& cm, const uint64_t* mas
   const int W = T.W;
   auto ncost = [&](int u) {
     const TNode& n = T.nodes[u];
-    return cm.node_cost(pc_union_not(T.L(n.left), T.L(n.right), mask, W), pc_and_not(T.L(u), mask, W));
+    return cm.node_cost(pc_union_not(T.L(n.left), T.L(n.right), mask, W), pc_and_not(T.L(n.left), mask, W),
+                        pc_and_not(T.L(n.right), mask, W), pc_and_not(T.L(u), mask, W));
   };
   std::vector<int> frontier{v}, removed;
   while ((int)frontier.size() < F) {
@@ -343,8 +347,10 @@ bool reconf_node(Tree& T, int v, int F, const CostModel& cm, const uint64_t* mas
         int S2 = S ^ S1;
         double c1 = best[S1], c2 = best[S2];
         if (c1 + c2 < best[S]) {
-          int un = pc_union_not(lab.data() + (size_t)S1 * W, lab.data() + (size_t)S2 * W, mask, W);
-          double c = c1 + c2 + cm.node_cost(un, out);
+          const uint64_t* L1 = lab.data() + (size_t)S1 * W;
+          const uint64_t* L2 = lab.data() + (size_t)S2 * W;
+          int un = pc_union_not(L1, L2, mask, W);
+          double c = c1 + c2 + cm.node_cost(un, pc_and_not(L1, mask, W), pc_and_not(L2, mask, W), out);
           if (c < best[S]) {
             best[S] = c;
             split[S] = S1;
@@ -395,6 +401,63 @@ void reconf_sweeps(Tree& T, int sweeps, int F, const CostModel& cm, const uint64
     bool any = false;
     for (int v : order) any |= reconf_node(T, v, F, cm, mask);
     if (!any) break;
+  }
+}
+
+// Greedy slicing: repeatedly slice the label, taken from the current largest
+// intermediates, that minimises (max width, cost) while over the width cap, else cost; each
+// pick is followed by one reconfiguration sweep of the sliced tree.
+void slice_tree(Tree& T, const CostModel& cm, int kmax, int capw, int sweeps, int F, int NL,
+                std::vector<uint64_t>& mask, std::vector<int>& chosen) {
+  const int W = T.W;
+  if (kmax == 0 || T.n_leaves <= 1) return;
+  for (int iter = 0; iter < 62; ++iter) {
+    int mw;
+    tree_cost(T, cm, mask.data(), &mw);
+    if (kmax >= 0 && (int)chosen.size() >= kmax) break;
+    if (kmax < 0 && (capw < 0 || mw <= capw)) break;
+    std::vector<char> cand(NL, 0);
+    for (size_t v = 0; v < T.nodes.size(); ++v) {
+      if (pc_and_not(T.L((int)v), mask.data(), W) >= mw - 1) {
+        const uint64_t* A = T.L((int)v);
+        for (int w = 0; w < W; ++w) {
+          uint64_t x = A[w] & ~mask[w];
+          while (x) {
+            int bit = __builtin_ctzll(x);
+            x &= x - 1;
+            cand[w * 64 + bit] = 1;
+          }
+        }
+      }
+    }
+    int bl = -1;
+    double bc = 0;
+    int bw = 0;
+    const bool width_first = (capw < 0) || (mw > capw);
+    for (int l = 0; l < NL; ++l) {
+      if (!cand[l]) continue;
+      mask[l / 64] |= uint64_t(1) << (l % 64);
+      int nw;
+      double c = tree_cost(T, cm, mask.data(), &nw);
+      mask[l / 64] &= ~(uint64_t(1) << (l % 64));
+      bool better;
+      if (bl < 0) better = true;
+      else if (width_first) better = (nw < bw) || (nw == bw && c < bc);
+      else better = (c < bc) || (c == bc && nw < bw);
+      if (better) {
+        bl = l;
+        bc = c;
+        bw = nw;
+      }
+    }
+    if (bl < 0) break;
+    mask[bl / 64] |= uint64_t(1) << (bl % 64);
+    chosen.push_back(bl);
+    if (sweeps > 0) {
+      CostModel cmc = cm;
+      if (capw > 0) cmc.cap = capw;
+      reconf_sweeps(T, 1, F, cmc, mask.data());
+    }
   }
 }
 
@@ -487,6 +550,7 @@ void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<in
   }
   CostModel cm;
   cm.log2d = std::log2((double)net.d);
+  cm.R = o.bytes_weight > 0 ? o.bytes_weight : 0.0;
   cm.dpow.resize(NL + 2);
   for (int i = 0; i <= NL + 1; ++i) cm.dpow[i] = std::pow((double)net.d, (double)i);
 
@@ -498,6 +562,9 @@ void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<in
   std::vector<uint64_t> nomask(leaves.W, 0);
 
   Tree best_tree;
+  std::vector<uint64_t> mask(leaves.W, 0);
+  std::vector<int> chosen;
+  const int capw = o.width_cap > 0 ? (int)std::floor(o.width_cap / cm.log2d + 1e-9) : -1;
   if (n_leaves == 1) {
     best_tree = tree_from_pairs(leaves, 1, {});
   } else {
@@ -528,13 +595,16 @@ void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<in
       for (int t = 0; t < nthreads; ++t) th.emplace_back(worker);
       for (auto& t : th) t.join();
     }
-    // reconfigure the best few greedy trees (parallel), keep the best
+    // the best few greedy trees (parallel): reconfigure, slice, reconfigure the sliced tree;
+    // keep the candidate with the lowest sliced cost N_sl * sum_v cost(v)
     std::vector<int> idx;
     for (int i = 0; i < trials; ++i)
       if (std::isfinite(tcost[i])) idx.push_back(i);
     std::sort(idx.begin(), idx.end(), [&](int a, int b) { return tcost[a] < tcost[b] || (tcost[a] == tcost[b] && a < b); });
-    int nre = std::min<int>((int)idx.size(), std::max(4, nthreads));
+    int nre = std::min<int>((int)idx.size(), std::max(o.candidates > 0 ? o.candidates : 8, 1));
     std::vector<Tree> trees(nre);
+    std::vector<std::vector<int>> chosen_c(nre);
+    std::vector<std::vector<uint64_t>> mask_c(nre);
     std::vector<double> rcost(nre);
     std::atomic<int> nx{0};
     auto rworker = [&]() {
@@ -543,7 +613,9 @@ void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<in
         if (i >= nre) break;
         trees[i] = tree_from_pairs(leaves, n_leaves, tpairs[idx[i]]);
         reconf_sweeps(trees[i], sweeps, F, cm, nomask.data());
-        rcost[i] = tree_cost(trees[i], cm, nomask.data(), nullptr);
+        mask_c[i].assign(leaves.W, 0);
+        slice_tree(trees[i], cm, o.n_sliced, capw, sweeps, F, NL, mask_c[i], chosen_c[i]);
+        rcost[i] = tree_cost(trees[i], cm, mask_c[i].data(), nullptr) * cm.dpow[chosen_c[i].size()];
       }
     };
     {
@@ -555,64 +627,8 @@ void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<in
     for (int i = 1; i < nre; ++i)
       if (rcost[i] < rcost[bi]) bi = i;
     best_tree = std::move(trees[bi]);
-  }
-
-  // ---- slicing (labels in compact ids)
-  std::vector<uint64_t> mask(leaves.W, 0);
-  std::vector<int> chosen;
-  const int kmax = o.n_sliced;  // -1: until width cap
-  const int capw = o.width_cap > 0 ? (int)std::floor(o.width_cap / cm.log2d + 1e-9) : -1;
-  if (kmax != 0 && n_leaves > 1) {
-    for (int iter = 0; iter < 62; ++iter) {
-      int mw;
-      double cur = tree_cost(best_tree, cm, mask.data(), &mw);
-      (void)cur;
-      if (kmax >= 0 && (int)chosen.size() >= kmax) break;
-      if (kmax < 0 && (capw < 0 || mw <= capw)) break;
-      // candidates: labels on intermediates within 1 of the max width
-      std::vector<char> cand(NL, 0);
-      for (size_t v = 0; v < best_tree.nodes.size(); ++v) {
-        if (pc_and_not(best_tree.L((int)v), mask.data(), leaves.W) >= mw - 1) {
-          const uint64_t* A = best_tree.L((int)v);
-          for (int w = 0; w < leaves.W; ++w) {
-            uint64_t x = A[w] & ~mask[w];
-            while (x) {
-              int bit = __builtin_ctzll(x);
-              x &= x - 1;
-              cand[w * 64 + bit] = 1;
-            }
-          }
-        }
-      }
-      int bl = -1;
-      double bc = 0;
-      int bw = 0;
-      const bool width_first = (capw < 0) || (mw > capw);
-      for (int l = 0; l < NL; ++l) {
-        if (!cand[l]) continue;
-        mask[l / 64] |= uint64_t(1) << (l % 64);
-        int nw;
-        double c = tree_cost(best_tree, cm, mask.data(), &nw);
-        mask[l / 64] &= ~(uint64_t(1) << (l % 64));
-        bool better;
-        if (bl < 0) better = true;
-        else if (width_first) better = (nw < bw) || (nw == bw && c < bc);
-        else better = (c < bc) || (c == bc && nw < bw);
-        if (better) {
-          bl = l;
-          bc = c;
-          bw = nw;
-        }
-      }
-      if (bl < 0) break;
-      mask[bl / 64] |= uint64_t(1) << (bl % 64);
-      chosen.push_back(bl);
-      if (sweeps > 0) {
-        CostModel cmc = cm;
-        if (capw > 0) cmc.cap = capw;
-        reconf_sweeps(best_tree, 1, F, cmc, mask.data());
-      }
-    }
+    mask = mask_c[bi];
+    chosen = chosen_c[bi];
   }
 
   // ---- slice loop order: heaviest dependent FLOP outermost, then adjacent-swap search
@@ -630,7 +646,10 @@ void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<in
     for (int v : po) {
       const TNode& n = best_tree.nodes[v];
       dep[v] = dep[n.left] | dep[n.right];
-      ncost[v] = cm.dpow[pc_union_not(best_tree.L(n.left), best_tree.L(n.right), mask.data(), leaves.W)];
+      ncost[v] = cm.node_cost(pc_union_not(best_tree.L(n.left), best_tree.L(n.right), mask.data(), leaves.W),
+                              pc_and_not(best_tree.L(n.left), mask.data(), leaves.W),
+                              pc_and_not(best_tree.L(n.right), mask.data(), leaves.W),
+                              pc_and_not(best_tree.L(v), mask.data(), leaves.W));
     }
     std::vector<double> wt(k, 0);
     for (int v : po)

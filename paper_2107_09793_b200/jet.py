@@ -31,7 +31,7 @@ P_dbl = ctypes.POINTER(c_dbl)
 class PlannerOpts(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("trials", c_i32), ("threads", c_i32), ("n_sliced", c_i32),
                 ("width_cap", c_i32), ("reconf_sweeps", c_i32), ("reconf_leaves", c_i32),
-                ("time_budget_s", c_dbl)]
+                ("time_budget_s", c_dbl), ("bytes_weight", c_dbl), ("candidates", c_i32)]
 
 
 class Cost(ctypes.Structure):
@@ -77,6 +77,7 @@ _sig("jt_plan_prefix_flop", c_i32, [c_vp, c_i64, c_i64, P_dbl])
 _sig("jt_plan_export", c_i32, [c_vp, ctypes.c_char_p])
 _sig("jt_plan_destroy", None, [c_vp])
 _sig("jt_exec_workspace_bytes", c_i32, [c_vp, c_i32, P_i64])
+_sig("jt_exec_describe", c_i32, [c_vp, c_i32, ctypes.c_char_p])
 _sig("jt_exec_create", c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64, c_vp, ctypes.POINTER(c_vp)])
 _sig("jt_exec_contract", c_i32, [c_vp, c_i64, c_i64, c_vp, P_dbl])
 _sig("jt_exec_contract_noreuse", c_i32, [c_vp, c_i64, c_i64, c_vp, P_dbl])
@@ -87,16 +88,17 @@ _sig("jt_exec_set_profiling", c_i32, [c_vp, c_i32])
 _sig("jt_exec_stats_reset", c_i32, [c_vp])
 _sig("jt_exec_invalidate", c_i32, [c_vp])
 _sig("jt_exec_destroy", None, [c_vp])
+_sig("jt_debug_emulate_host", c_i32, [c_vp, c_i32, c_i64, c_i64, P_dbl, c_i32])
 _sig("jt_amplitude", c_i32, [c_vp, c_i32, c_i32, P_dbl])
 _sig("jt_permute", c_i32, [c_i32, c_vp, c_vp, c_i32, P_i32, c_vp])
 
 EXPORTED = ["jt_last_error", "jt_version", "jt_network_create", "jt_network_add_gate", "jt_network_close",
             "jt_network_info", "jt_network_export", "jt_network_destroy", "jt_plan_create", "jt_plan_greedy",
             "jt_plan_sizes", "jt_plan_get", "jt_plan_cost", "jt_plan_prefix_flop", "jt_plan_export",
-            "jt_plan_destroy", "jt_exec_workspace_bytes", "jt_exec_create", "jt_exec_contract",
+            "jt_plan_destroy", "jt_exec_workspace_bytes", "jt_exec_describe", "jt_exec_create", "jt_exec_contract",
             "jt_exec_contract_noreuse", "jt_exec_contract_host", "jt_exec_stats_get",
             "jt_exec_upload_leaves", "jt_exec_set_profiling", "jt_exec_stats_reset",
-            "jt_exec_invalidate", "jt_exec_destroy", "jt_amplitude", "jt_permute"]
+            "jt_exec_invalidate", "jt_exec_destroy", "jt_amplitude", "jt_permute", "jt_debug_emulate_host"]
 
 
 class JetError(RuntimeError):
@@ -183,8 +185,9 @@ class Plan:
 
     @classmethod
     def greedy(cls, net, seed=1, trials=64, threads=0, n_sliced=0, width_cap=0, reconf_sweeps=-1,
-               reconf_leaves=0, time_budget_s=0.0):
-        o = PlannerOpts(seed, trials, threads, n_sliced, width_cap, reconf_sweeps, reconf_leaves, time_budget_s)
+               reconf_leaves=0, time_budget_s=0.0, bytes_weight=0.0, candidates=0):
+        o = PlannerOpts(seed, trials, threads, n_sliced, width_cap, reconf_sweeps, reconf_leaves, time_budget_s,
+                        bytes_weight, candidates)
         h = c_vp()
         _check(_lib.jt_plan_greedy(net._h, ctypes.byref(o), ctypes.byref(h)))
         return cls(h, net)
@@ -227,6 +230,14 @@ class Plan:
         b = c_i64()
         _check(_lib.jt_exec_workspace_bytes(self._h, _DT[dtype], ctypes.byref(b)))
         return b.value
+
+    def describe_exec(self, dtype="c64"):
+        import json
+        import tempfile
+
+        with tempfile.NamedTemporaryFile(suffix=".json") as f:
+            _check(_lib.jt_exec_describe(self._h, _DT[dtype], f.name.encode()))
+            return json.load(open(f.name))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -293,6 +304,13 @@ class Exec:
         if getattr(self, "_h", None):
             _lib.jt_exec_destroy(self._h)
             self._h = None
+
+
+def debug_emulate_host(plan, begin, end, dtype="c128", reuse=True):
+    """TEST ONLY: the compiled launch descriptors executed on the host (see jetb200.h)."""
+    vals = np.zeros(2 * max(end - begin, 1), dtype=np.float64)
+    _check(_lib.jt_debug_emulate_host(plan._h, _DT[dtype], begin, end, vals.ctypes.data_as(P_dbl), 1 if reuse else 0))
+    return vals[: 2 * (end - begin)].view(np.complex128)
 
 
 def amplitude(plan, dtype="c64", device=0):

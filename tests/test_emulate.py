@@ -1,0 +1,62 @@
+"""CPU check of the plan compiler and the prefix-cache scheduler: the compiled K2 launch
+descriptors (bit tiles, strides, split-K, workspace offsets) executed on the host with the
+kernels' index arithmetic (jt_debug_emulate_host, test-only) must reproduce the oracle's
+s_sigma.  The GPU parity tests then only have to cover the device code itself."""
+
+import numpy as np
+import pytest
+
+from circuits import generate_gbs, random_bitstring, workload
+from oracle import contract
+from oracle.network import build_network
+
+
+@pytest.fixture(scope="module")
+def jet():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2107_09793_b200 import jet as j
+
+    return j
+
+
+@pytest.mark.parametrize("k", [0, 1, 3, 5])
+def test_emulated_descriptors_match_oracle_c1(jet, k):
+    circ, _ = workload("C1")
+    for seed in range(3):
+        bits = random_bitstring(9, 2, 40 + seed)
+        net = jet.Network.from_circuit(circ, bits)
+        plan = jet.Plan.greedy(net, seed=seed, trials=8, n_sliced=k, bytes_weight=10.0 * (seed % 2))
+        ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
+        n = len(ref)
+        v128 = jet.debug_emulate_host(plan, 0, n, "c128")
+        assert np.max(np.abs(v128 - ref)) <= 1e-12 * np.max(np.abs(ref))
+        v64 = jet.debug_emulate_host(plan, 0, n, "c64")
+        assert np.max(np.abs(v64 - ref)) <= 1e-5 * np.max(np.abs(ref))
+        # reuse on/off and split ranges give bitwise-identical values (P10 on the host)
+        off = jet.debug_emulate_host(plan, 0, n, "c64", reuse=False)
+        assert np.array_equal(v64, off)
+
+
+def test_emulated_descriptors_match_oracle_gbs(jet):
+    circ = generate_gbs(2, 2, 1, 0.5, 4, seed=2)
+    for seed in range(3):
+        bits = random_bitstring(4, 4, seed)
+        net = jet.Network.from_circuit(circ, bits)
+        plan = jet.Plan.greedy(net, seed=seed, trials=8, n_sliced=seed)
+        ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
+        v = jet.debug_emulate_host(plan, 0, len(ref), "c128")
+        assert np.max(np.abs(v - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1e-300)
+
+
+def test_describe_exec_layout(jet):
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=32, n_sliced=6)
+    d = plan.describe_exec("c64")
+    assert d["total_bytes"] == plan.workspace_bytes("c64")
+    for n in d["nodes"]:
+        assert n["tm"] + n["tk"] <= 12 and n["tk"] + n["tn"] <= 12 and n["tm"] + n["tn"] <= 12
+        assert n["block"] % 32 == 0 and n["block"] <= 256
+        assert n["n_out"] == 2 ** (n["tm"] + n["tn"] + n["n_outer"])
