@@ -69,3 +69,41 @@ def host_shard_sum(values_per_rank):
 def as_complex(acc_np):
     a = np.asarray(acc_np, dtype=np.float64)
     return complex(a[0], a[1])
+
+
+# Roofline model of the current kernels (c64 on B200): K2 streams at most the HBM bandwidth
+# and computes complex FP32 on CUDA cores.  Used only to choose among host plans.
+MODEL_HBM_BPS = 6.0e12
+MODEL_FLOPS = {"c64": 60e12, "c128": 30e12}
+
+
+def modeled_time(plan, dtype="c64", bw=MODEL_HBM_BPS, flops=None):
+    """sum over executed nodes (prefix-cache multiplicity over the full slice range) of
+    max(bytes/bw, flop/peak) -- the roofline time of one amplitude on one GPU."""
+    flops = flops or MODEL_FLOPS[dtype]
+    d = plan.describe_exec(dtype)
+    dq = plan.net.d
+    t = 0.0
+    for n in d["nodes"]:
+        runs = dq ** (n["maxpos"] + 1)
+        t += runs * max(n["bytes"] / bw, n["flop"] / flops)
+    return t, d["total_bytes"]
+
+
+def plan_best(net, n_sliced, dtype="c64", seed=1, trials=4096, weights=(0.0, 3.0, 5.0, 10.0), width_cap=0,
+              ws_limit=150e9):
+    """Run the host planner with several roofline weights and keep the plan with the lowest
+    modeled time whose workspace fits ws_limit bytes.  Deterministic."""
+    from . import jet
+
+    best = None
+    for w in weights:
+        p = jet.Plan.greedy(net, seed=seed, trials=trials, n_sliced=n_sliced, width_cap=width_cap, bytes_weight=w)
+        t, ws = modeled_time(p, dtype)
+        if ws > ws_limit:
+            continue
+        if best is None or t < best[0]:
+            best = (t, w, p)
+    if best is None:
+        raise RuntimeError("no plan fits the workspace limit")
+    return best[2], {"modeled_s": best[0], "bytes_weight": best[1]}
