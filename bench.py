@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--slices-per-step", type=int, default=0)
-    ap.add_argument("--trials", type=int, default=256)
+    ap.add_argument("--trials", type=int, default=4096)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--width-cap", type=int, default=31)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -66,10 +66,12 @@ def make_plan(jet, cfg, args):
 
     circ, bits = workload(cfg["circ"], args.seed)
     net = jet.Network.from_circuit(circ, bits)
+    from paper_2107_09793_b200.runtime import plan_best
+
     k = cfg["k"]
     t0 = time.time()
-    plan = jet.Plan.greedy(net, seed=args.seed, trials=args.trials, n_sliced=k if k is not None else -1,
-                           width_cap=args.width_cap if k is None else 0)
+    plan, info = plan_best(net, k if k is not None else -1, dtype=cfg["dtype"], seed=args.seed,
+                           trials=args.trials, width_cap=args.width_cap if k is None else 0)
     return circ, bits, net, plan, time.time() - t0
 
 

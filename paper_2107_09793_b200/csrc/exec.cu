@@ -42,6 +42,7 @@ struct ExecNode {
   std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
   GettArgs args{};
   int RM = 1, RN = 1, block = 32;
+  int64_t grid_x = 1;  // persistent CTAs along the output tiles (set for the device at exec create)
   size_t smem = 0;
   int64_t out_off = 0;   // byte offset of the output in the workspace
   int64_t part_off = 0;  // byte offset of split-K partials
@@ -147,7 +148,10 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
   while (cnt(inM) < std::min<int>((int)M.size(), 6) && cnt(inM) + cnt(inN) < lim && add_first(inM)) {}
   while (cnt(inM) + cnt(inN) < lim && add_first(inN)) {}
   while (cnt(inM) + cnt(inN) < lim && add_first(inM)) {}
-  while (cnt(inK) < 4 && cnt(inK) + std::max(cnt(inM), cnt(inN)) < lim && add_first(inK)) {}
+  // K: at least 4 bits, and more while one K step moves < 4096 elements (small C tiles,
+  // e.g. big x big -> small reductions, need long K steps to amortise each barrier)
+  while (cnt(inK) + std::max(cnt(inM), cnt(inN)) < lim &&
+         (cnt(inK) < 4 || (1 << (cnt(inM) + cnt(inK))) + (1 << (cnt(inK) + cnt(inN))) < 4096) && add_first(inK)) {}
   // enforce operand tile limits by dropping non-mandatory bits from the high end
   auto drop_last = [](std::vector<char>& in, const std::vector<char>& keep) {
     for (int i = (int)in.size() - 1; i >= 0; --i)
@@ -197,18 +201,25 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
   g.nA = g.tm + g.tk;
   g.nB = g.tk + g.tn;
   if (g.nA > 12 || g.nB > 12) fail(JT_EINTERNAL, "exec: tile too large");
-  // A tile bits (sorted by A stride): smem index = m + (k << tm)
+  // operand tiles in the operand's own bit order (stride ascending): tile bit j has global
+  // stride g[j] and shared-memory stride 2^j; record where each M/K/N bit landed
   {
-    std::vector<std::pair<int64_t, std::pair<int64_t, int32_t>>> ta;
-    for (int i = 0; i < g.tm; ++i) ta.push_back({sa[tM[i]], {sa[tM[i]], 1 << i}});
-    for (int i = 0; i < g.tk; ++i) ta.push_back({sa[tK[i]], {sa[tK[i]], 1 << (g.tm + i)}});
+    std::vector<std::pair<int64_t, std::pair<int, int>>> ta;  // (stride, (role 0=M 1=K, index))
+    for (int i = 0; i < g.tm; ++i) ta.push_back({sa[tM[i]], {0, i}});
+    for (int i = 0; i < g.tk; ++i) ta.push_back({sa[tK[i]], {1, i}});
     std::sort(ta.begin(), ta.end());
-    for (size_t i = 0; i < ta.size(); ++i) { g.gA[i] = ta[i].second.first; g.sA[i] = ta[i].second.second; }
-    std::vector<std::pair<int64_t, std::pair<int64_t, int32_t>>> tb;
-    for (int i = 0; i < g.tn; ++i) tb.push_back({sb[tN[i]], {sb[tN[i]], 1 << i}});
-    for (int i = 0; i < g.tk; ++i) tb.push_back({sb[tK[i]], {sb[tK[i]], 1 << (g.tn + i)}});
+    for (size_t j = 0; j < ta.size(); ++j) {
+      g.gA[j] = ta[j].first;
+      (ta[j].second.first == 0 ? g.pM : g.pKA)[ta[j].second.second] = (int8_t)j;
+    }
+    std::vector<std::pair<int64_t, std::pair<int, int>>> tb;
+    for (int i = 0; i < g.tn; ++i) tb.push_back({sb[tN[i]], {0, i}});
+    for (int i = 0; i < g.tk; ++i) tb.push_back({sb[tK[i]], {1, i}});
     std::sort(tb.begin(), tb.end());
-    for (size_t i = 0; i < tb.size(); ++i) { g.gB[i] = tb[i].second.first; g.sB[i] = tb[i].second.second; }
+    for (size_t j = 0; j < tb.size(); ++j) {
+      g.gB[j] = tb[j].first;
+      (tb[j].second.first == 0 ? g.pN : g.pKB)[tb[j].second.second] = (int8_t)j;
+    }
   }
   // outer bits: N (B-stride order) then M (A-stride order) -> blockIdx.x bits
   std::vector<int64_t> outer;
@@ -246,9 +257,20 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
     while (splits > 1 && splits * cbytes > cap) splits /= 2;
   }
   g.splits = (int32_t)splits;
-  const int64_t ab = (int64_t(1) << g.nA) + (int64_t(1) << g.nB);
-  const int64_t red = (int64_t)g.KG * (int64_t(1) << (g.tm + g.tn));
-  en.smem = (size_t)(std::max(ab, red) * esize);
+  // 16-B element-pair copies (c64) when tile bit 0 is unit-stride and every other stride is even
+  auto vec_ok = [&](const int64_t* gt, int n, const int64_t* o, const int64_t* ok) {
+    if (esize != 8 || n < 1 || gt[0] != 1) return 0;
+    for (int j = 1; j < n; ++j) if (gt[j] & 1) return 0;
+    for (int j = 0; j < g.n_outer; ++j) if (o[j] & 1) return 0;
+    for (int j = 0; j < g.n_ok; ++j) if (ok[j] & 1) return 0;
+    return 1;
+  };
+  g.vecA = vec_ok(g.gA, g.nA, g.o_sA, g.ok_sA);
+  g.vecB = vec_ok(g.gB, g.nB, g.o_sB, g.ok_sB);
+  g.dbuf = 1;
+  const int64_t stage = (int64_t(1) << g.nA) + (int64_t(1) << g.nB);
+  const int64_t red = g.KG > 1 ? (int64_t)(g.KG - 1) * (int64_t(1) << (g.tm + g.tn)) : 0;
+  en.smem = (size_t)((2 * stage + red) * esize + 2 * 4 * (int64_t(1) << g.tk));
   en.n_out = g.n_tiles << (g.tm + g.tn);
   // output view: [tile N bits][tile M bits][outer bits]
   View vc;
@@ -410,20 +432,16 @@ void emulate_gett(const GettArgs& p, char* ws, const ExecNode& en, const std::ve
   const C2* B = reinterpret_cast<const C2*>(ws + ab_off[1].first) + ab_off[1].second;
   C2* C = reinterpret_cast<C2*>(ws + ab_off[2].first);
   C2* P = reinterpret_cast<C2*>(ws + ab_off[3].first);
-  int64_t tgA[2][64], tgB[2][64];
-  int32_t tsA[2][64], tsB[2][64];
-  for (int i = 0; i < 64; ++i)
-    for (int h = 0; h < 2; ++h) {
-      int64_t g = 0, gb = 0;
-      int32_t s = 0, sb = 0;
-      for (int b = 0; b < 6; ++b)
-        if ((i >> b) & 1) {
-          const int bi = 6 * h + b;
-          if (bi < p.nA) { g += p.gA[bi]; s += p.sA[bi]; }
-          if (bi < p.nB) { gb += p.gB[bi]; sb += p.sB[bi]; }
-        }
-      tgA[h][i] = g; tsA[h][i] = s; tgB[h][i] = gb; tsB[h][i] = sb;
-    }
+  auto gofs = [](const int64_t* g, int n, int e) {
+    int64_t o = 0;
+    for (int j = 0; j < n; ++j) if ((e >> j) & 1) o += g[j];
+    return o;
+  };
+  auto dep = [](int v, const int8_t* pos, int n) {
+    int r = 0;
+    for (int i = 0; i < n; ++i) r |= ((v >> i) & 1) << pos[i];
+    return r;
+  };
   std::vector<C2> sA(size_t(1) << p.nA), sB(size_t(1) << p.nB), acc(size_t(1) << (p.tm + p.tn));
   for (int64_t tile = 0; tile < p.n_tiles; ++tile)
     for (int split = 0; split < p.splits; ++split) {
@@ -436,12 +454,13 @@ void emulate_gett(const GettArgs& p, char* ws, const ExecNode& en, const std::ve
         int64_t oa = baseA, ob = baseB;
         for (int j = 0; j < p.n_ok; ++j)
           if ((it >> j) & 1) { oa += p.ok_sA[j]; ob += p.ok_sB[j]; }
-        for (int e = 0; e < (1 << p.nA); ++e) sA[tsA[0][e & 63] + tsA[1][e >> 6]] = A[oa + tgA[0][e & 63] + tgA[1][e >> 6]];
-        for (int e = 0; e < (1 << p.nB); ++e) sB[tsB[0][e & 63] + tsB[1][e >> 6]] = B[ob + tgB[0][e & 63] + tgB[1][e >> 6]];
+        for (int e = 0; e < (1 << p.nA); ++e) sA[e] = A[oa + gofs(p.gA, p.nA, e)];
+        for (int e = 0; e < (1 << p.nB); ++e) sB[e] = B[ob + gofs(p.gB, p.nB, e)];
         for (int k = 0; k < (1 << p.tk); ++k)
           for (int m = 0; m < (1 << p.tm); ++m)
             for (int n = 0; n < (1 << p.tn); ++n) {
-              const C2 a = sA[(k << p.tm) + m], b = sB[(k << p.tn) + n];
+              const C2 a = sA[dep(m, p.pM, p.tm) | dep(k, p.pKA, p.tk)];
+              const C2 b = sB[dep(n, p.pN, p.tn) | dep(k, p.pKB, p.tk)];
               C2& c = acc[(m << p.tn) + n];
               c.x += a.x * b.x - a.y * b.y;
               c.y += a.x * b.y + a.y * b.x;
@@ -553,9 +572,9 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
     const GettArgs& g = en.args;
     std::fprintf(f, "%s{\"v\": %lld, \"maxpos\": %d, \"flop\": %.17g, \"bytes\": %.17g, \"n_out\": %lld, "
                  "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
-                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu}",
+                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d}",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
-                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem);
+                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf);
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
@@ -583,6 +602,17 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     fail(JT_ERESOURCE, "exec: workspace too small (" + std::to_string(ws_bytes) + " < " + std::to_string(L.total) + ")");
   JT_CUDA(cudaSetDevice(device));
   set_smem_attrs();
+  int n_sm = 148;
+  JT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+  for (ExecNode& en : L.order) {
+    int nb = 1;
+    const void* fn = dt == JT_C64 ? reinterpret_cast<const void*>(pick_gett<float>(en.RM, en.RN))
+                                  : reinterpret_cast<const void*>(pick_gett<double>(en.RM, en.RN));
+    JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, en.block, en.smem));
+    if (nb < 1) fail(JT_EINTERNAL, "exec: a contraction tile does not fit on an SM");
+    const int64_t resident = (int64_t)nb * n_sm;
+    en.grid_x = std::min<int64_t>(en.args.n_tiles, std::max<int64_t>(1, resident / en.args.splits));
+  }
   auto* ex = new jt_exec();
   ex->L = std::move(L);
   ex->dtype = dt;
@@ -633,7 +663,7 @@ void launch_node(jt_exec* ex, ExecNode& en, const std::vector<int>& dig) {
   g.B = reinterpret_cast<const C2*>(ex->ws + L.node_off[en.opB]) + offB;
   g.C = ex->ws + en.out_off;
   g.P = ex->ws + en.part_off;
-  dim3 grid((unsigned)g.n_tiles, (unsigned)g.splits);
+  dim3 grid((unsigned)en.grid_x, (unsigned)g.splits);
   GettFn fn = pick_gett<R>(en.RM, en.RN);
   if (ex->profiling) {
     if (ex->ev_used == ex->ev.size()) {

@@ -41,10 +41,14 @@ struct GettArgs {
   int32_t n_outer, n_ok, splits;
   int32_t tm, tn, tk, nA, nB;
   int32_t TX, TY, KG;
+  int32_t vecA, vecB;  // 1: tile bit 0 has global stride 1 -> 16-B copies of element pairs (c64)
+  int32_t dbuf;        // unused (kept for the descriptor dump); the kernel always double-buffers
   int64_t o_sA[kMaxOuter], o_sB[kMaxOuter];    // outer M/N bit j: strides in A and B
   int64_t ok_sA[kMaxOuter], ok_sB[kMaxOuter];  // outer K bit j
-  int64_t gA[kMaxTile], gB[kMaxTile];          // tile bit (sorted by operand stride): global stride
-  int32_t sA[kMaxTile], sB[kMaxTile];          //   ... and shared-memory stride
+  int64_t gA[kMaxTile], gB[kMaxTile];          // tile bit j of A (B), sorted by stride: global stride;
+                                               // its shared-memory stride is 2^j (operand order)
+  int8_t pM[kMaxTile], pKA[kMaxTile];          // tile-M bit i / tile-K bit i -> bit position in A's tile
+  int8_t pKB[kMaxTile], pN[kMaxTile];          // tile-K bit i / tile-N bit i -> bit position in B's tile
 };
 
 template <typename C2>
@@ -55,108 +59,200 @@ __device__ __forceinline__ void cmac(C2& acc, const C2 a, const C2 b) {
   acc.y = fma(a.y, b.x, acc.y);
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// deposit the bits of v at the given bit positions: sum_i bit_i(v) << pos[i]
+__device__ __forceinline__ int deposit(int v, const int8_t* pos, int n) {
+  int r = 0;
+  for (int i = 0; i < n; ++i) r |= ((v >> i) & 1) << pos[i];
+  return r;
+}
+
+// Copy one operand tile (2^n elements, tile bit j at global stride g[j], shared stride 2^j)
+// into shared memory with cp.async; element pairs move as 16 B when g[0] == 1.
+template <typename C2>
+__device__ __forceinline__ void load_tile(C2* dst, const C2* src, int n, bool vec, const int64_t (*tg)[64],
+                                          int tid, int nthr) {
+  const int sz = 1 << n;
+  if (sizeof(C2) == 16) {
+    for (int e = tid; e < sz; e += nthr) cp_async16(dst + e, src + tg[0][e & 63] + tg[1][e >> 6]);
+  } else if (vec) {
+    for (int e = 2 * tid; e < sz; e += 2 * nthr) cp_async16(dst + e, src + tg[0][e & 63] + tg[1][e >> 6]);
+  } else {
+    for (int e = tid; e < sz; e += nthr) cp_async8(dst + e, src + tg[0][e & 63] + tg[1][e >> 6]);
+  }
+}
+
+// Persistent over output tiles: CTA x walks tiles x, x + gridDim.x, ...; within a tile it walks
+// its split's K steps.  The (tile, K step) items form one flat sequence with a two-stage
+// cp.async pipeline, so the next item's operand tiles stream in while this one computes.
 template <typename R, int RM, int RN>
 __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettArgs p) {
   using C2 = typename V2<R>::t;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int64_t tgA[2][64], tgB[2][64];
-  __shared__ int32_t tsA[2][64], tsB[2][64];
   const int tid = threadIdx.x;
-  for (int i = tid; i < 64; i += blockDim.x) {
-    // lo tables: tile bits 0..5; hi tables: tile bits 6..11 (of the stride-sorted order)
+  const int nthr = blockDim.x;
+  for (int i = tid; i < 64; i += nthr) {
+    // global-offset tables: lo = tile bits 0..5, hi = tile bits 6..11 (stride order)
     for (int h = 0; h < 2; ++h) {
       int64_t g = 0, gb = 0;
-      int32_t s = 0, sb = 0;
       for (int b = 0; b < 6; ++b) {
         if ((i >> b) & 1) {
           const int bi = 6 * h + b;
-          if (bi < p.nA) { g += p.gA[bi]; s += p.sA[bi]; }
-          if (bi < p.nB) { gb += p.gB[bi]; sb += p.sB[bi]; }
+          if (bi < p.nA) g += p.gA[bi];
+          if (bi < p.nB) gb += p.gB[bi];
         }
       }
-      tgA[h][i] = g; tsA[h][i] = s;
-      tgB[h][i] = gb; tsB[h][i] = sb;
+      tgA[h][i] = g;
+      tgB[h][i] = gb;
     }
   }
+  const int szA = 1 << p.nA, szB = 1 << p.nB, TK = 1 << p.tk;
+  const int CT = 1 << (p.tm + p.tn);
+  C2* sA0 = reinterpret_cast<C2*>(smem_raw);
+  const int stage = szA + szB;  // elements per pipeline stage
+  C2* red = sA0 + 2 * stage;    // k-group partials (KG > 1)
+  int* posKA = reinterpret_cast<int*>(red + (p.KG > 1 ? (p.KG - 1) * CT : 0));
+  int* posKB = posKA + TK;
+  for (int kk = tid; kk < TK; kk += nthr) {
+    posKA[kk] = deposit(kk, p.pKA, p.tk);
+    posKB[kk] = deposit(kk, p.pKB, p.tk);
+  }
   __syncthreads();
-  C2* sAm = reinterpret_cast<C2*>(smem_raw);
-  C2* sBm = sAm + (1 << p.nA);
-  const int64_t tile = blockIdx.x;
   const int split = blockIdx.y;
-  int64_t baseA = 0, baseB = 0;
-  for (int j = 0; j < p.n_outer; ++j)
-    if ((tile >> j) & 1) { baseA += p.o_sA[j]; baseB += p.o_sB[j]; }
   const int64_t it0 = (int64_t)split * p.k_iters / p.splits;
   const int64_t it1 = (int64_t)(split + 1) * p.k_iters / p.splits;
+  const int64_t nk = it1 - it0;
+  const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_tiles * nk;
   const int TXY = p.TX * p.TY;
   const int kg = tid / TXY;
   const int txy = tid - kg * TXY;
   const int tx = txy % p.TX, ty = txy / p.TX;
   const bool active = kg < p.KG;
+  // this thread's rows m = ty + r*TY and columns n = pairs (2tx, 2tx+1) + (c/2)*2TX (RN >= 2)
+  auto col = [&](int c) { return RN >= 2 ? (2 * tx + (c & 1) + (c >> 1) * 2 * p.TX) : tx; };
+  int offM[RM], offN[RN];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) offM[r] = deposit(ty + r * p.TY, p.pM, p.tm);
+#pragma unroll
+  for (int c = 0; c < RN; ++c) offN[c] = deposit(col(c), p.pN, p.tn);
+  const C2* __restrict__ A = reinterpret_cast<const C2*>(p.A);
+  const C2* __restrict__ B = reinterpret_cast<const C2*>(p.B);
+  auto offsets = [&](int64_t w, int64_t& tile, int64_t& oa, int64_t& ob) {
+    tile = blockIdx.x + (w / nk) * gridDim.x;
+    const int64_t it = it0 + w % nk;
+    oa = 0;
+    ob = 0;
+    for (int j = 0; j < p.n_outer; ++j)
+      if ((tile >> j) & 1) { oa += p.o_sA[j]; ob += p.o_sB[j]; }
+    for (int j = 0; j < p.n_ok; ++j)
+      if ((it >> j) & 1) { oa += p.ok_sA[j]; ob += p.ok_sB[j]; }
+  };
   C2 acc[RM][RN];
 #pragma unroll
   for (int r = 0; r < RM; ++r)
 #pragma unroll
     for (int c = 0; c < RN; ++c) { acc[r][c].x = 0; acc[r][c].y = 0; }
-  const C2* __restrict__ A = reinterpret_cast<const C2*>(p.A);
-  const C2* __restrict__ B = reinterpret_cast<const C2*>(p.B);
-  const int szA = 1 << p.nA, szB = 1 << p.nB, TK = 1 << p.tk;
-  for (int64_t it = it0; it < it1; ++it) {
-    int64_t oa = baseA, ob = baseB;
-    for (int j = 0; j < p.n_ok; ++j)
-      if ((it >> j) & 1) { oa += p.ok_sA[j]; ob += p.ok_sB[j]; }
-    if (it != it0) __syncthreads();
-    for (int e = tid; e < szA; e += blockDim.x)
-      sAm[tsA[0][e & 63] + tsA[1][e >> 6]] = A[oa + tgA[0][e & 63] + tgA[1][e >> 6]];
-    for (int e = tid; e < szB; e += blockDim.x)
-      sBm[tsB[0][e & 63] + tsB[1][e >> 6]] = B[ob + tgB[0][e & 63] + tgB[1][e >> 6]];
+  if (total > 0) {
+    int64_t t, oa, ob;
+    offsets(0, t, oa, ob);
+    load_tile(sA0, A + oa, p.nA, p.vecA, tgA, tid, nthr);
+    load_tile(sA0 + szA, B + ob, p.nB, p.vecB, tgB, tid, nthr);
+    cp_async_commit();
+  }
+  for (int64_t w = 0; w < total; ++w) {
+    const int buf = (int)(w & 1);
+    if (w + 1 < total) {  // prefetch the next item into the other stage
+      int64_t t, oa, ob;
+      offsets(w + 1, t, oa, ob);
+      C2* nxt = sA0 + (buf ^ 1) * stage;
+      load_tile(nxt, A + oa, p.nA, p.vecA, tgA, tid, nthr);
+      load_tile(nxt + szA, B + ob, p.nB, p.vecB, tgB, tid, nthr);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
+    const C2* sA = sA0 + buf * stage;
+    const C2* sB = sA + szA;
     if (active) {
       for (int kk = kg; kk < TK; kk += p.KG) {
+        const int ka = posKA[kk], kb = posKB[kk];
         C2 a[RM], b[RN];
 #pragma unroll
-        for (int r = 0; r < RM; ++r) a[r] = sAm[(kk << p.tm) + ty + r * p.TY];
+        for (int r = 0; r < RM; ++r) a[r] = sA[ka + offM[r]];
 #pragma unroll
-        for (int c = 0; c < RN; ++c) b[c] = sBm[(kk << p.tn) + tx + c * p.TX];
+        for (int c = 0; c < RN; ++c) b[c] = sB[kb + offN[c]];
 #pragma unroll
         for (int r = 0; r < RM; ++r)
 #pragma unroll
           for (int c = 0; c < RN; ++c) cmac(acc[r][c], a[r], b[c]);
       }
     }
-  }
-  const int CT = 1 << (p.tm + p.tn);
-  if (p.KG > 1) {  // deterministic in-CTA reduction over k-groups
-    __syncthreads();
-    C2* red = sAm;
-    if (active && kg > 0) {
-#pragma unroll
-      for (int r = 0; r < RM; ++r)
-#pragma unroll
-        for (int c = 0; c < RN; ++c)
-          red[(kg - 1) * CT + ((ty + r * p.TY) << p.tn) + tx + c * p.TX] = acc[r][c];
+    if (w % nk != nk - 1) {
+      __syncthreads();  // this stage is refilled by the prefetch two items later
+      continue;
     }
-    __syncthreads();
-    if (kg == 0) {
-      for (int g = 1; g < p.KG; ++g) {
+    // ---- epilogue of a tile
+    const int64_t tile = blockIdx.x + (w / nk) * gridDim.x;
+    if (p.KG > 1) {  // deterministic in-CTA reduction over k-groups
+      if (active && kg > 0) {
 #pragma unroll
         for (int r = 0; r < RM; ++r)
 #pragma unroll
-          for (int c = 0; c < RN; ++c) {
-            const C2 v = red[(g - 1) * CT + ((ty + r * p.TY) << p.tn) + tx + c * p.TX];
-            acc[r][c].x += v.x;
-            acc[r][c].y += v.y;
-          }
+          for (int c = 0; c < RN; ++c) red[(kg - 1) * CT + ((ty + r * p.TY) << p.tn) + col(c)] = acc[r][c];
+      }
+      __syncthreads();
+      if (kg == 0) {
+        for (int g = 1; g < p.KG; ++g) {
+#pragma unroll
+          for (int r = 0; r < RM; ++r)
+#pragma unroll
+            for (int c = 0; c < RN; ++c) {
+              const C2 v = red[(g - 1) * CT + ((ty + r * p.TY) << p.tn) + col(c)];
+              acc[r][c].x += v.x;
+              acc[r][c].y += v.y;
+            }
+        }
       }
     }
-  }
-  if (kg == 0 && txy < TXY) {
-    C2* out = reinterpret_cast<C2*>(p.splits == 1 ? p.C : p.P);
-    const int64_t base = ((int64_t)(p.splits == 1 ? 0 : split) * p.n_tiles + tile) << (p.tm + p.tn);
+    if (kg == 0 && txy < TXY) {
+      C2* out = reinterpret_cast<C2*>(p.splits == 1 ? p.C : p.P);
+      const int64_t base = ((int64_t)(p.splits == 1 ? 0 : split) * p.n_tiles + tile) << (p.tm + p.tn);
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        C2* row = out + base + ((int64_t)(ty + r * p.TY) << p.tn);
+        if (RN >= 2 && sizeof(C2) == 8) {
+#pragma unroll
+          for (int c = 0; c < RN; c += 2) {
+            const float4 v = make_float4((float)acc[r][c].x, (float)acc[r][c].y, (float)acc[r][c + 1].x,
+                                         (float)acc[r][c + 1].y);
+            *reinterpret_cast<float4*>(row + col(c)) = v;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < RN; ++c) row[col(c)] = acc[r][c];
+        }
+      }
+    }
 #pragma unroll
     for (int r = 0; r < RM; ++r)
 #pragma unroll
-      for (int c = 0; c < RN; ++c) out[base + ((ty + r * p.TY) << p.tn) + tx + c * p.TX] = acc[r][c];
+      for (int c = 0; c < RN; ++c) { acc[r][c].x = 0; acc[r][c].y = 0; }
+    __syncthreads();
   }
 }
 
