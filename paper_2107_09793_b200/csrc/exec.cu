@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -15,6 +16,7 @@
 
 #include "jt_internal.hpp"
 #include "kernels.cuh"
+#include "kernels_tc.cuh"
 
 #define JT_CUDA(x)                                                                        \
   do {                                                                                    \
@@ -37,6 +39,8 @@ struct View {
 };
 
 struct ExecNode {
+  int kind = 0;  // 0: K2 CUDA-core GETT, 1: K3 tcgen05 3xTF32 (c64)
+  TcArgs tc{};
   int64_t v = -1;
   int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
   std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
@@ -61,6 +65,18 @@ struct Layout {
 };
 
 using GettFn = void (*)(GettArgs);
+using TcFn = void (*)(TcArgs);
+
+TcFn pick_tc(int tk) {
+  switch (tk) {
+    case 2: return gett_tc_kernel<2>;
+    case 3: return gett_tc_kernel<4>;
+    case 4: return gett_tc_kernel<8>;
+    case 5: return gett_tc_kernel<16>;
+    case 6: return gett_tc_kernel<32>;
+  }
+  fail(JT_EINTERNAL, "no tc instance");
+}
 
 template <typename R>
 GettFn pick_gett(int RM, int RN) {
@@ -83,6 +99,10 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
+    const void* tcs[5] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<4>),
+                          reinterpret_cast<const void*>(gett_tc_kernel<8>), reinterpret_cast<const void*>(gett_tc_kernel<16>),
+                          reinterpret_cast<const void*>(gett_tc_kernel<32>)};
+    for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2>),
@@ -95,6 +115,78 @@ int ilog2_exact(int d) {
   while ((1 << b) < d) ++b;
   if ((1 << b) != d) fail(JT_EUSAGE, "exec: the GPU path needs a power-of-two qudit dimension d");
   return b;
+}
+
+// K3 eligibility and descriptor (c64 only): small A fully inside the tile with 3..7 free
+// bits and 2..6 contracted bits, big B with >= 7 free bits (128-row MMA tiles).  Returns
+// false if the contraction does not fit K3.
+bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out) {
+  if (esize != 8) return false;
+  std::map<int64_t, int64_t> sa, sb;
+  for (auto& x : va.bits) sa[x.first] = x.second;
+  for (auto& x : vb.bits) sb[x.first] = x.second;
+  std::vector<std::pair<int64_t, int64_t>> M, N, K;  // (stride, bit)
+  for (auto& x : va.bits) {
+    if (sb.count(x.first)) K.push_back({sb[x.first], x.first});
+    else M.push_back({x.second, x.first});
+  }
+  for (auto& x : vb.bits)
+    if (!sa.count(x.first)) N.push_back({x.second, x.first});
+  const int tm = (int)M.size(), tk = (int)K.size();
+  if (tm < 3 || tm > 7 || tk < 2 || tk > 6 || (int)N.size() < 7) return false;
+  const int Kp = 2 << tk, Np = 2 << tm;
+  const int64_t smem = 2LL * 4 * Kp * (128 + Np);
+  if (smem > 200 * 1024) return false;
+  std::sort(M.begin(), M.end());
+  std::sort(N.begin(), N.end());
+  std::sort(K.begin(), K.end());
+  std::vector<int64_t> tN, oN;
+  for (size_t i = 0; i < N.size(); ++i) (i < 7 ? tN : oN).push_back(N[i].second);
+  if ((int)oN.size() > 31) return false;
+  TcArgs& t = en.tc;
+  std::memset(&t, 0, sizeof(t));
+  t.tm = tm;
+  t.tk = tk;
+  t.nX = 7 + tk;
+  t.Np = Np;
+  t.Kp = Kp;
+  t.sbo = (Kp / 4) * 128;
+  t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  uint32_t cols = 32;
+  while ((int)cols < Np) cols <<= 1;
+  t.tmem_cols = cols;
+  // B tile bits in B-stride order with their byte offsets in the canonical K-major layout
+  std::vector<std::pair<int64_t, int32_t>> tb;
+  for (int i = 0; i < 7; ++i) tb.push_back({sb[tN[i]], i < 3 ? (16 << i) : (t.sbo << (i - 3))});
+  for (int i = 0; i < tk; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : (128 << (i - 1))});
+  std::sort(tb.begin(), tb.end());
+  for (size_t j = 0; j < tb.size(); ++j) {
+    t.gX[j] = tb[j].first;
+    t.sX[j] = tb[j].second;
+  }
+  for (int i = 0; i < tm; ++i) t.aM[i] = sa[M[i].second];
+  for (int i = 0; i < tk; ++i) t.aK[i] = sa[K[i].second];
+  t.n_outer = (int)oN.size();
+  for (int j = 0; j < t.n_outer; ++j) t.o_sB[j] = sb[oN[j]];
+  t.n_tiles = int64_t(1) << t.n_outer;
+  en.kind = 1;
+  en.smem = (size_t)smem;
+  en.block = 256;
+  en.n_out = t.n_tiles << (7 + tm);
+  en.grid_x = t.n_tiles;
+  en.args.splits = 1;
+  en.args.n_tiles = t.n_tiles;
+  out.bits.clear();
+  int64_t st = 1;
+  for (auto b : tN) { out.bits.push_back({b, st}); st <<= 1; }
+  for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
+  for (auto b : oN) { out.bits.push_back({b, st}); st <<= 1; }
+  return true;
+}
+
+bool tc_enabled() {
+  const char* e = std::getenv("JETB200_TC");
+  return !(e && e[0] == '0');
 }
 
 // Tile selection and argument fill for one contraction (K2).  Returns the output view.
@@ -282,6 +374,7 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
 }
 
 Layout compile(const jt_plan& plan, int esize) {
+  const bool use_tc = tc_enabled();
   Layout L;
   L.esize = esize;
   const jt_network& net = plan.net;
@@ -356,7 +449,9 @@ Layout compile(const jt_plan& plan, int esize) {
     en.opB = fl <= fr ? n.right : n.left;
     if (en.opA < nt) en.sliceA = leaf_slices[en.opA];
     if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
-    views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
+    View tv;
+    if (use_tc && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
+    else views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
     en.maxpos = n.maxpos;
     en.flop = n.flop;
     en.bytes = n.bytes8 / 8.0 * esize;
@@ -480,6 +575,42 @@ void emulate_gett(const GettArgs& p, char* ws, const ExecNode& en, const std::ve
   }
 }
 
+void emulate_tc(const TcArgs& p, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
+  const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
+  const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
+  float2* C = reinterpret_cast<float2*>(ws + off[2].first);
+  // invert the B-tile byte offsets back to (row n, k) through the same per-bit tables
+  const int nX = p.nX;
+  for (int64_t t = 0; t < p.n_tiles; ++t) {
+    int64_t base = 0;
+    for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
+    std::vector<float2> Bt((size_t)128 << p.tk);
+    for (int e = 0; e < (1 << nX); ++e) {
+      int64_t g = 0;
+      int32_t byte = 0;
+      for (int j = 0; j < nX; ++j) if ((e >> j) & 1) { g += p.gX[j]; byte += p.sX[j]; }
+      // byte = (n&7)*16 + (n>>3)*sbo + (k>>1)*128 + (k&1)*8
+      const int n = ((byte % 128) / 16) + 8 * (byte / p.sbo);
+      const int rem = byte % p.sbo;
+      const int k = 2 * ((rem / 128)) + ((rem % 16) / 8);
+      Bt[(size_t)k * 128 + n] = B[base + g];
+    }
+    for (int m = 0; m < (1 << p.tm); ++m)
+      for (int n = 0; n < 128; ++n) {
+        double re = 0, im = 0;
+        for (int k = 0; k < (1 << p.tk); ++k) {
+          int64_t ao = 0;
+          for (int i = 0; i < p.tm; ++i) if ((m >> i) & 1) ao += p.aM[i];
+          for (int i = 0; i < p.tk; ++i) if ((k >> i) & 1) ao += p.aK[i];
+          const float2 a = A[ao], b = Bt[(size_t)k * 128 + n];
+          re += (double)a.x * b.x - (double)a.y * b.y;
+          im += (double)a.x * b.y + (double)a.y * b.x;
+        }
+        C[(t << (7 + p.tm)) + ((int64_t)m << 7) + n] = make_float2((float)re, (float)im);
+      }
+  }
+}
+
 template <typename R>
 void emulate_host(const jt_plan& plan, int esize, int64_t b, int64_t e, double* h_vals, bool reuse) {
   using C2 = typename V2<R>::t;
@@ -510,7 +641,8 @@ void emulate_host(const jt_plan& plan, int esize, int64_t b, int64_t e, double* 
       for (auto& sl : en.sliceB) offB += (int64_t)dig[sl.first] * sl.second;
       std::vector<std::pair<int64_t, int64_t>> offs = {{L.node_off[en.opA], offA}, {L.node_off[en.opB], offB},
                                                        {en.out_off, 0}, {en.part_off, 0}};
-      emulate_gett<R>(en.args, ws.data(), en, offs);
+      if (en.kind == 1) emulate_tc(en.tc, ws.data(), offs);
+      else emulate_gett<R>(en.args, ws.data(), en, offs);
     }
     const C2 r = *reinterpret_cast<const C2*>(ws.data() + L.order.back().out_off);
     h_vals[2 * (s - b)] = (double)r.x;
@@ -572,9 +704,10 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
     const GettArgs& g = en.args;
     std::fprintf(f, "%s{\"v\": %lld, \"maxpos\": %d, \"flop\": %.17g, \"bytes\": %.17g, \"n_out\": %lld, "
                  "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
-                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d}",
+                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d}",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
-                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf);
+                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind, en.tc.tm,
+                 en.tc.tk, en.tc.n_outer);
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
@@ -606,6 +739,14 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   JT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
   for (ExecNode& en : L.order) {
     int nb = 1;
+    if (en.kind == 1) {
+      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tk)), 256,
+                                                            en.smem));
+      nb = std::min<int>(nb, 512 / (int)en.tc.tmem_cols);  // TMEM columns per SM
+      if (nb < 1) fail(JT_EINTERNAL, "exec: a K3 tile does not fit on an SM");
+      en.grid_x = std::min<int64_t>(en.tc.n_tiles, (int64_t)nb * n_sm);
+      continue;
+    }
     const void* fn = dt == JT_C64 ? reinterpret_cast<const void*>(pick_gett<float>(en.RM, en.RN))
                                   : reinterpret_cast<const void*>(pick_gett<double>(en.RM, en.RN));
     JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, en.block, en.smem));
@@ -659,6 +800,32 @@ void launch_node(jt_exec* ex, ExecNode& en, const std::vector<int>& dig) {
   int64_t offA = 0, offB = 0;
   for (auto& s : en.sliceA) offA += (int64_t)dig[s.first] * s.second;
   for (auto& s : en.sliceB) offB += (int64_t)dig[s.first] * s.second;
+  if (en.kind == 1) {
+    TcArgs& t = en.tc;
+    t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]) + offA;
+    t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]) + offB;
+    t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
+    if (ex->profiling) {
+      if (ex->ev_used == ex->ev.size()) {
+        cudaEvent_t a, b;
+        JT_CUDA(cudaEventCreate(&a));
+        JT_CUDA(cudaEventCreate(&b));
+        ex->ev.push_back({a, b});
+      }
+      JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].first, ex->stream));
+    }
+    pick_tc(t.tk)<<<(unsigned)en.grid_x, 256, en.smem, ex->stream>>>(t);
+    if (ex->profiling) {
+      JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].second, ex->stream));
+      ex->ev_work.push_back({en.bytes, en.flop});
+      ex->ev_used++;
+    }
+    ex->stats.kernel_launches++;
+    ex->stats.node_launches++;
+    ex->stats.flop_executed += en.flop;
+    ex->stats.bytes_executed += en.bytes;
+    return;
+  }
   g.A = reinterpret_cast<const C2*>(ex->ws + L.node_off[en.opA]) + offA;
   g.B = reinterpret_cast<const C2*>(ex->ws + L.node_off[en.opB]) + offB;
   g.C = ex->ws + en.out_off;

@@ -181,7 +181,9 @@ def test_gbs_parity_and_closed_forms(jet, dim, width):
 def c2_plan(jet):
     circ, bits = workload("C2")
     net = jet.Network.from_circuit(circ, bits)
-    plan = jet.Plan.greedy(net, seed=1, trials=256, n_sliced=6)
+    plan = jet.Plan.greedy(net, seed=1, trials=256, n_sliced=6, bytes_weight=5.0)
+    kinds = [n["kind"] for n in plan.describe_exec("c64")["nodes"]]
+    assert sum(kinds) >= 10, "the C2 plan should exercise the K3 tensor-core kernel"
     return circ, bits, net, plan
 
 
@@ -216,3 +218,15 @@ def test_c2_fsim_identity_closed_form(jet):
     for dtype in ("c64", "c128"):
         amp, _, _ = run(jet, plan, dtype)
         assert rel(amp, want) < TOL[dtype]
+
+
+def test_k3_tensor_cores_vs_cuda_cores(jet, c2_plan, monkeypatch):
+    """K3 (tcgen05 3xTF32) and K2 (CUDA-core FP32) give the same slices within c64 rounding."""
+    circ, bits, net, plan = c2_plan
+    monkeypatch.setenv("JETB200_TC", "0")
+    assert sum(n["kind"] for n in plan.describe_exec("c64")["nodes"]) == 0
+    amp0, v0, _ = run(jet, plan, "c64", ranges=[(0, 8)])
+    monkeypatch.setenv("JETB200_TC", "1")
+    amp1, v1, _ = run(jet, plan, "c64", ranges=[(0, 8)])
+    assert np.max(np.abs(v1 - v0) / np.abs(v0)) < 2e-5
+    assert rel(amp1, amp0) < 2e-5
