@@ -57,6 +57,20 @@ def test_describe_exec_layout(jet):
     d = plan.describe_exec("c64")
     assert d["total_bytes"] == plan.workspace_bytes("c64")
     for n in d["nodes"]:
-        assert n["tm"] + n["tk"] <= 12 and n["tk"] + n["tn"] <= 12 and n["tm"] + n["tn"] <= 12
         assert n["block"] % 32 == 0 and n["block"] <= 256
-        assert n["n_out"] == 2 ** (n["tm"] + n["tn"] + n["n_outer"])
+        if n["kind"] == 1:   # K3: 128-row MMA tiles, all of A in the tile
+            assert n["n_out"] == 2 ** (7 + n["tc_tm"] + n["tc_outer"])
+            assert 3 <= n["tc_tm"] <= 7 and 2 <= n["tc_tk"] <= 6 and n["smem"] <= 200 * 1024
+        else:
+            assert n["tm"] + n["tk"] <= 12 and n["tk"] + n["tn"] <= 12 and n["tm"] + n["tn"] <= 12
+            assert n["n_out"] == 2 ** (n["tm"] + n["tn"] + n["n_outer"])
+
+
+def test_emulated_k3_matches_oracle_c2_slices(jet):
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6, bytes_weight=5.0)
+    assert sum(n["kind"] for n in plan.describe_exec("c64")["nodes"]) > 0
+    ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[5]))
+    v = jet.debug_emulate_host(plan, 5, 6, "c64")
+    assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4
