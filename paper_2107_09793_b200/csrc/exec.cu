@@ -133,7 +133,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (auto& x : vb.bits)
     if (!sa.count(x.first)) N.push_back({x.second, x.first});
   const int tm = (int)M.size(), tk = (int)K.size();
-  if (tm < 3 || tm > 7 || tk < 2 || tk > 6 || (int)N.size() < 7) return false;
+  if (tm < 3 || tm > 7 || tk < 2 || tk > 5 || (int)N.size() < 7) return false;  // 7 + tk <= 12 table bits
   const int Kp = 2 << tk, Np = 2 << tm;
   const int64_t smem = 2LL * 4 * Kp * (128 + Np);
   if (smem > 200 * 1024) return false;

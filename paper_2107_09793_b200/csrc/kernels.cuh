@@ -78,6 +78,17 @@ __device__ __forceinline__ int deposit(int v, const int8_t* pos, int n) {
   return r;
 }
 
+// Shared-memory XOR swizzle of an operand tile index: folds bits 4-12 (c64) / 3-11 (c128)
+// onto the 16-B slot bits of a 128-B row so that warp reads along any tile bit spread over
+// the banks.  Linear over GF(2): swz(a | b) = swz(a) ^ swz(b) for disjoint a, b, so a row
+// offset and a column offset can be swizzled separately and combined with XOR.  Bit 0 is
+// untouched for c64, keeping 16-B element pairs contiguous.
+template <typename C2>
+__device__ __forceinline__ int swz(int i) {
+  if (sizeof(C2) == 8) return i ^ ((((i >> 4) ^ (i >> 7) ^ (i >> 10)) & 7) << 1);
+  return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7);
+}
+
 // Copy one operand tile (2^n elements, tile bit j at global stride g[j], shared stride 2^j)
 // into shared memory with cp.async; element pairs move as 16 B when g[0] == 1.
 template <typename C2>
@@ -85,11 +96,11 @@ __device__ __forceinline__ void load_tile(C2* dst, const C2* src, int n, bool ve
                                           int tid, int nthr) {
   const int sz = 1 << n;
   if (sizeof(C2) == 16) {
-    for (int e = tid; e < sz; e += nthr) cp_async16(dst + e, src + tg[0][e & 63] + tg[1][e >> 6]);
+    for (int e = tid; e < sz; e += nthr) cp_async16(dst + swz<C2>(e), src + tg[0][e & 63] + tg[1][e >> 6]);
   } else if (vec) {
-    for (int e = 2 * tid; e < sz; e += 2 * nthr) cp_async16(dst + e, src + tg[0][e & 63] + tg[1][e >> 6]);
+    for (int e = 2 * tid; e < sz; e += 2 * nthr) cp_async16(dst + swz<C2>(e), src + tg[0][e & 63] + tg[1][e >> 6]);
   } else {
-    for (int e = tid; e < sz; e += nthr) cp_async8(dst + e, src + tg[0][e & 63] + tg[1][e >> 6]);
+    for (int e = tid; e < sz; e += nthr) cp_async8(dst + swz<C2>(e), src + tg[0][e & 63] + tg[1][e >> 6]);
   }
 }
 
@@ -126,8 +137,8 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
   int* posKA = reinterpret_cast<int*>(red + (p.KG > 1 ? (p.KG - 1) * CT : 0));
   int* posKB = posKA + TK;
   for (int kk = tid; kk < TK; kk += nthr) {
-    posKA[kk] = deposit(kk, p.pKA, p.tk);
-    posKB[kk] = deposit(kk, p.pKB, p.tk);
+    posKA[kk] = swz<C2>(deposit(kk, p.pKA, p.tk));
+    posKB[kk] = swz<C2>(deposit(kk, p.pKB, p.tk));
   }
   __syncthreads();
   const int split = blockIdx.y;
@@ -145,9 +156,9 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
   auto col = [&](int c) { return RN >= 2 ? (2 * tx + (c & 1) + (c >> 1) * 2 * p.TX) : tx; };
   int offM[RM], offN[RN];
 #pragma unroll
-  for (int r = 0; r < RM; ++r) offM[r] = deposit(ty + r * p.TY, p.pM, p.tm);
+  for (int r = 0; r < RM; ++r) offM[r] = swz<C2>(deposit(ty + r * p.TY, p.pM, p.tm));
 #pragma unroll
-  for (int c = 0; c < RN; ++c) offN[c] = deposit(col(c), p.pN, p.tn);
+  for (int c = 0; c < RN; ++c) offN[c] = swz<C2>(deposit(col(c), p.pN, p.tn));
   const C2* __restrict__ A = reinterpret_cast<const C2*>(p.A);
   const C2* __restrict__ B = reinterpret_cast<const C2*>(p.B);
   auto offsets = [&](int64_t w, int64_t& tile, int64_t& oa, int64_t& ob) {
@@ -193,9 +204,9 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
         const int ka = posKA[kk], kb = posKB[kk];
         C2 a[RM], b[RN];
 #pragma unroll
-        for (int r = 0; r < RM; ++r) a[r] = sA[ka + offM[r]];
+        for (int r = 0; r < RM; ++r) a[r] = sA[ka ^ offM[r]];
 #pragma unroll
-        for (int c = 0; c < RN; ++c) b[c] = sB[kb + offN[c]];
+        for (int c = 0; c < RN; ++c) b[c] = sB[kb ^ offN[c]];
 #pragma unroll
         for (int r = 0; r < RM; ++r)
 #pragma unroll

@@ -162,7 +162,7 @@ class Network:
         _check(_lib.jt_network_export(self._h, path.encode()))
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.jt_network_destroy(self._h)
             self._h = None
 
@@ -240,7 +240,7 @@ class Plan:
             return json.load(open(f.name))
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.jt_plan_destroy(self._h)
             self._h = None
 
@@ -301,7 +301,7 @@ class Exec:
         _check(_lib.jt_exec_invalidate(self._h))
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.jt_exec_destroy(self._h)
             self._h = None
 

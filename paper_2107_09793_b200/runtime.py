@@ -74,7 +74,8 @@ def as_complex(acc_np):
 # Roofline model of the current kernels (c64 on B200): K2 streams at most the HBM bandwidth
 # and computes complex FP32 on CUDA cores.  Used only to choose among host plans.
 MODEL_HBM_BPS = 6.0e12
-MODEL_FLOPS = {"c64": 60e12, "c128": 30e12}
+MODEL_FLOPS = {"c64": 40e12, "c128": 30e12}   # K2 (CUDA cores), measured order of magnitude
+MODEL_FLOPS_TC = 250e12                         # K3 (tcgen05 3xTF32, algorithmic complex FLOP/s)
 
 
 def modeled_time(plan, dtype="c64", bw=MODEL_HBM_BPS, flops=None):
@@ -86,11 +87,12 @@ def modeled_time(plan, dtype="c64", bw=MODEL_HBM_BPS, flops=None):
     t = 0.0
     for n in d["nodes"]:
         runs = dq ** (n["maxpos"] + 1)
-        t += runs * max(n["bytes"] / bw, n["flop"] / flops)
+        f = MODEL_FLOPS_TC if n.get("kind", 0) == 1 else flops
+        t += runs * (max(n["bytes"] / bw, n["flop"] / f) + 3e-6)   # + launch gap
     return t, d["total_bytes"]
 
 
-def plan_best(net, n_sliced, dtype="c64", seed=1, trials=4096, weights=(0.0, 3.0, 5.0, 10.0), width_cap=0,
+def plan_best(net, n_sliced, dtype="c64", seed=1, trials=4096, weights=(0.0, 3.0, 5.0, 10.0, 20.0, 40.0), width_cap=0,
               ws_limit=150e9):
     """Run the host planner with several roofline weights and keep the plan with the lowest
     modeled time whose workspace fits ws_limit bytes.  Deterministic."""

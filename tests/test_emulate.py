@@ -60,7 +60,7 @@ def test_describe_exec_layout(jet):
         assert n["block"] % 32 == 0 and n["block"] <= 256
         if n["kind"] == 1:   # K3: 128-row MMA tiles, all of A in the tile
             assert n["n_out"] == 2 ** (7 + n["tc_tm"] + n["tc_outer"])
-            assert 3 <= n["tc_tm"] <= 7 and 2 <= n["tc_tk"] <= 6 and n["smem"] <= 200 * 1024
+            assert 3 <= n["tc_tm"] <= 7 and 2 <= n["tc_tk"] <= 5 and n["smem"] <= 200 * 1024
         else:
             assert n["tm"] + n["tk"] <= 12 and n["tk"] + n["tn"] <= 12 and n["tm"] + n["tn"] <= 12
             assert n["n_out"] == 2 ** (n["tm"] + n["tn"] + n["n_outer"])
