@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -61,7 +62,7 @@ struct Layout {
   std::vector<int64_t> leaf_off;      // byte offset of every leaf (full, unsliced data)
   std::vector<int64_t> node_off;      // byte offset of every node output (leaves: leaf_off)
   int64_t leaf_bytes = 0, inter_bytes = 0, scratch_bytes = 0;
-  int64_t inter_base = 0, scratch_base = 0, vals_base = 0, acc_base = 0, total = 0;
+  int64_t inter_base = 0, scratch_base = 0, vals_base = 0, acc_base = 0, state_base = 0, total = 0;
 };
 
 using GettFn = void (*)(GettArgs);
@@ -449,6 +450,7 @@ Layout compile(const jt_plan& plan, int esize) {
     en.opB = fl <= fr ? n.right : n.left;
     if (en.opA < nt) en.sliceA = leaf_slices[en.opA];
     if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
+    if (en.sliceA.size() > 4 || en.sliceB.size() > 4) fail(JT_EUSAGE, "exec: more than 4 sliced labels on one leaf");
     View tv;
     if (use_tc && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
     else views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
@@ -509,7 +511,8 @@ Layout compile(const jt_plan& plan, int esize) {
   L.scratch_bytes = scratch;
   L.vals_base = align_up(L.scratch_base + L.scratch_bytes);
   L.acc_base = align_up(L.vals_base + plan.n_sl * 16);
-  L.total = align_up(L.acc_base + 16);
+  L.state_base = align_up(L.acc_base + 16);
+  L.total = align_up(L.state_base + (int64_t)sizeof(SliceState));
   return L;
 }
 
@@ -682,7 +685,20 @@ struct jt_exec {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // event pool for K2 timing
   size_t ev_used = 0;
   std::vector<std::pair<double, double>> ev_work;        // (bytes, flop) of each timed launch
+  bool use_graphs = true;
+  std::vector<cudaGraphExec_t> graphs;   // per prefix-cache level j+1 (j = -1..k)
+  std::vector<jt_exec_stats> graph_stats;
+  double* graph_acc = nullptr;           // accumulator baked into the graphs
+  jt_exec_stats* cur_stats = nullptr;
+  void drop_graphs() {
+    for (auto g : graphs)
+      if (g) cudaGraphExecDestroy(g);
+    graphs.clear();
+    graph_stats.clear();
+    graph_acc = nullptr;
+  }
   ~jt_exec() {
+    drop_graphs();
     for (auto& e : ev) {
       cudaEventDestroy(e.first);
       cudaEventDestroy(e.second);
@@ -756,6 +772,23 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   }
   auto* ex = new jt_exec();
   ex->L = std::move(L);
+  ex->cur_stats = &ex->stats;
+  {
+    const char* e = std::getenv("JETB200_GRAPHS");
+    ex->use_graphs = !(e && e[0] == '0') && stream != nullptr;  // no capture on the legacy stream
+  }
+  const int32_t* dptr = reinterpret_cast<const int32_t*>(static_cast<char*>(d_ws) + ex->L.state_base +
+                                                         offsetof(SliceState, digits));
+  for (ExecNode& en : ex->L.order) {
+    SliceView sv{};
+    sv.digits = dptr;
+    sv.nA = (int)en.sliceA.size();
+    sv.nB = (int)en.sliceB.size();
+    for (int i = 0; i < sv.nA; ++i) { sv.posA[i] = en.sliceA[i].first; sv.strA[i] = en.sliceA[i].second; }
+    for (int i = 0; i < sv.nB; ++i) { sv.posB[i] = en.sliceB[i].first; sv.strB[i] = en.sliceB[i].second; }
+    en.args.sv = sv;
+    en.tc.sv = sv;
+  }
   ex->dtype = dt;
   ex->device = device;
   ex->ws = static_cast<char*>(d_ws);
@@ -792,82 +825,97 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   return ex;
 }
 
+void ev_begin(jt_exec* ex) {
+  if (!ex->profiling) return;
+  if (ex->ev_used == ex->ev.size()) {
+    cudaEvent_t a, b;
+    JT_CUDA(cudaEventCreate(&a));
+    JT_CUDA(cudaEventCreate(&b));
+    ex->ev.push_back({a, b});
+  }
+  JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].first, ex->stream));
+}
+void ev_end(jt_exec* ex, const ExecNode& en) {
+  if (!ex->profiling) return;
+  JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].second, ex->stream));
+  ex->ev_work.push_back({en.bytes, en.flop});
+  ex->ev_used++;
+}
+
 template <typename R>
-void launch_node(jt_exec* ex, ExecNode& en, const std::vector<int>& dig) {
+void launch_node(jt_exec* ex, ExecNode& en) {
   using C2 = typename V2<R>::t;
   const Layout& L = ex->L;
-  GettArgs& g = en.args;
-  int64_t offA = 0, offB = 0;
-  for (auto& s : en.sliceA) offA += (int64_t)dig[s.first] * s.second;
-  for (auto& s : en.sliceB) offB += (int64_t)dig[s.first] * s.second;
+  jt_exec_stats& st = *ex->cur_stats;
   if (en.kind == 1) {
     TcArgs& t = en.tc;
-    t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]) + offA;
-    t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]) + offB;
+    t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]);
+    t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
-    if (ex->profiling) {
-      if (ex->ev_used == ex->ev.size()) {
-        cudaEvent_t a, b;
-        JT_CUDA(cudaEventCreate(&a));
-        JT_CUDA(cudaEventCreate(&b));
-        ex->ev.push_back({a, b});
-      }
-      JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].first, ex->stream));
-    }
+    ev_begin(ex);
     pick_tc(t.tk)<<<(unsigned)en.grid_x, 256, en.smem, ex->stream>>>(t);
-    if (ex->profiling) {
-      JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].second, ex->stream));
-      ex->ev_work.push_back({en.bytes, en.flop});
-      ex->ev_used++;
+    ev_end(ex, en);
+    st.kernel_launches++;
+  } else {
+    GettArgs& g = en.args;
+    g.A = ex->ws + L.node_off[en.opA];
+    g.B = ex->ws + L.node_off[en.opB];
+    g.C = ex->ws + en.out_off;
+    g.P = ex->ws + en.part_off;
+    dim3 grid((unsigned)en.grid_x, (unsigned)g.splits);
+    GettFn fn = pick_gett<R>(en.RM, en.RN);
+    ev_begin(ex);
+    fn<<<grid, en.block, en.smem, ex->stream>>>(g);
+    ev_end(ex, en);
+    st.kernel_launches++;
+    if (g.splits > 1) {
+      int64_t n = en.n_out;
+      int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+      reduce_splits_kernel<R><<<blocks, 256, 0, ex->stream>>>(reinterpret_cast<const C2*>(g.P),
+                                                               reinterpret_cast<C2*>(g.C), n, g.splits);
+      st.kernel_launches++;
     }
-    ex->stats.kernel_launches++;
-    ex->stats.node_launches++;
-    ex->stats.flop_executed += en.flop;
-    ex->stats.bytes_executed += en.bytes;
-    return;
   }
-  g.A = reinterpret_cast<const C2*>(ex->ws + L.node_off[en.opA]) + offA;
-  g.B = reinterpret_cast<const C2*>(ex->ws + L.node_off[en.opB]) + offB;
-  g.C = ex->ws + en.out_off;
-  g.P = ex->ws + en.part_off;
-  dim3 grid((unsigned)en.grid_x, (unsigned)g.splits);
-  GettFn fn = pick_gett<R>(en.RM, en.RN);
-  if (ex->profiling) {
-    if (ex->ev_used == ex->ev.size()) {
-      cudaEvent_t a, b;
-      JT_CUDA(cudaEventCreate(&a));
-      JT_CUDA(cudaEventCreate(&b));
-      ex->ev.push_back({a, b});
-    }
-    JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].first, ex->stream));
-  }
-  fn<<<grid, en.block, en.smem, ex->stream>>>(g);
-  if (ex->profiling) {
-    JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].second, ex->stream));
-    ex->ev_work.push_back({en.bytes, en.flop});
-    ex->ev_used++;
-  }
-  ex->stats.kernel_launches++;
-  if (g.splits > 1) {
-    int64_t n = en.n_out;
-    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    reduce_splits_kernel<R><<<blocks, 256, 0, ex->stream>>>(reinterpret_cast<const C2*>(g.P),
-                                                             reinterpret_cast<C2*>(g.C), n, g.splits);
-    ex->stats.kernel_launches++;
-  }
-  ex->stats.node_launches++;
-  ex->stats.flop_executed += en.flop;
-  ex->stats.bytes_executed += en.bytes;
+  st.node_launches++;
+  st.flop_executed += en.flop;
+  st.bytes_executed += en.bytes;
+}
+
+// One slice at prefix-cache level j: advance the device slice state, every node with
+// maxpos(S(v)) >= j, then the accumulate.
+template <typename R>
+void slice_sequence(jt_exec* ex, int j, double* d_acc) {
+  using C2 = typename V2<R>::t;
+  SliceState* state = reinterpret_cast<SliceState*>(ex->ws + ex->L.state_base);
+  advance_slice_kernel<<<1, 32, 0, ex->stream>>>(state, ex->k, ex->d);
+  ex->cur_stats->kernel_launches++;
+  for (ExecNode& en : ex->L.order)
+    if (en.maxpos >= j) launch_node<R>(ex, en);
+  const ExecNode& root = ex->L.order.back();
+  accumulate_kernel<R><<<1, 32, 0, ex->stream>>>(reinterpret_cast<const C2*>(ex->ws + root.out_off), d_acc,
+                                                 reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), state);
+  ex->cur_stats->kernel_launches++;
+  ex->cur_stats->slices_done++;
 }
 
 template <typename R>
 void contract_range(jt_exec* ex, int64_t b, int64_t e, double* d_acc, bool reuse) {
-  using C2 = typename V2<R>::t;
   std::vector<int> dig(ex->k), prev(ex->k);
   auto digits = [&](int64_t s, std::vector<int>& out) {
     for (int p = ex->k - 1; p >= 0; --p) { out[p] = (int)(s % ex->d); s /= ex->d; }
   };
   if (ex->last >= 0) digits(ex->last, prev);
+  const bool graphs = ex->use_graphs && !ex->profiling;
+  if (graphs && ex->graph_acc != d_acc) {
+    ex->drop_graphs();
+    ex->graphs.assign(ex->k + 2, nullptr);
+    ex->graph_stats.assign(ex->k + 2, jt_exec_stats{});
+    ex->graph_acc = d_acc;
+  }
+  if (e > b) {
+    set_slice_kernel<<<1, 32, 0, ex->stream>>>(reinterpret_cast<SliceState*>(ex->ws + ex->L.state_base), b - 1);
+    ex->stats.kernel_launches++;
+  }
   for (int64_t s = b; s < e; ++s) {
     digits(s, dig);
     int j;
@@ -878,16 +926,32 @@ void contract_range(jt_exec* ex, int64_t b, int64_t e, double* d_acc, bool reuse
       for (int p = 0; p < ex->k; ++p)
         if (dig[p] != prev[p]) { j = p; break; }
     }
-    for (ExecNode& en : ex->L.order)
-      if (en.maxpos >= j) launch_node<R>(ex, en, dig);
-    const ExecNode& root = ex->L.order.back();
-    accumulate_kernel<R><<<1, 32, 0, ex->stream>>>(reinterpret_cast<const C2*>(ex->ws + root.out_off), d_acc,
-                                                   reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), s);
-    ex->stats.kernel_launches++;
-    ex->stats.slices_done++;
+    if (!graphs) {
+      ex->cur_stats = &ex->stats;
+      slice_sequence<R>(ex, j, d_acc);
+    } else {
+      cudaGraphExec_t& ge = ex->graphs[j + 1];
+      if (!ge) {  // capture this level once
+        cudaGraph_t g;
+        ex->cur_stats = &ex->graph_stats[j + 1];
+        JT_CUDA(cudaStreamBeginCapture(ex->stream, cudaStreamCaptureModeThreadLocal));
+        slice_sequence<R>(ex, j, d_acc);
+        JT_CUDA(cudaStreamEndCapture(ex->stream, &g));
+        JT_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        JT_CUDA(cudaGraphDestroy(g));
+      }
+      JT_CUDA(cudaGraphLaunch(ge, ex->stream));
+      const jt_exec_stats& gs = ex->graph_stats[j + 1];
+      ex->stats.kernel_launches += gs.kernel_launches;
+      ex->stats.node_launches += gs.node_launches;
+      ex->stats.flop_executed += gs.flop_executed;
+      ex->stats.bytes_executed += gs.bytes_executed;
+      ex->stats.slices_done += gs.slices_done;
+    }
     ex->last = s;
     prev = dig;
   }
+  ex->cur_stats = &ex->stats;
   JT_CUDA(cudaGetLastError());
 }
 
@@ -927,6 +991,7 @@ void exec_contract_host(jt_exec* ex, int64_t b, int64_t e, double* h_acc) {
 }
 
 void exec_invalidate(jt_exec* ex) { ex->last = -1; }
+void exec_set_graphs(jt_exec* ex, bool on) { ex->use_graphs = on; }
 void exec_set_profiling(jt_exec* ex, bool on) { ex->profiling = on; }
 void exec_stats(const jt_exec* ex, jt_exec_stats* out) { *out = ex->stats; }
 void exec_stats_reset(jt_exec* ex) { ex->stats = jt_exec_stats{}; }

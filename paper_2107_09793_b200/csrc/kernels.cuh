@@ -27,6 +27,23 @@ namespace jt {
 constexpr int kMaxOuter = 48;
 constexpr int kMaxTile = 14;
 
+// K5 slice views, resolved on the device: a leaf operand carrying sliced labels is read at
+// base + sum_i digit[pos_i] * stride_i, with the digits of the current slice in device
+// memory (written by advance_slice_kernel), so a captured CUDA graph serves every slice.
+struct SliceView {
+  const int32_t* digits;
+  int32_t nA, nB;
+  int32_t posA[4], posB[4];
+  int64_t strA[4], strB[4];
+};
+
+__device__ __forceinline__ int64_t slice_off(const SliceView& v, bool a) {
+  int64_t o = 0;
+  const int n = a ? v.nA : v.nB;
+  for (int i = 0; i < n; ++i) o += (int64_t)v.digits[a ? v.posA[i] : v.posB[i]] * (a ? v.strA[i] : v.strB[i]);
+  return o;
+}
+
 template <typename R> struct V2;
 template <> struct V2<float> { using t = float2; };
 template <> struct V2<double> { using t = double2; };
@@ -49,6 +66,7 @@ struct GettArgs {
                                                // its shared-memory stride is 2^j (operand order)
   int8_t pM[kMaxTile], pKA[kMaxTile];          // tile-M bit i / tile-K bit i -> bit position in A's tile
   int8_t pKB[kMaxTile], pN[kMaxTile];          // tile-K bit i / tile-N bit i -> bit position in B's tile
+  SliceView sv;
 };
 
 template <typename C2>
@@ -159,8 +177,8 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
   for (int r = 0; r < RM; ++r) offM[r] = swz<C2>(deposit(ty + r * p.TY, p.pM, p.tm));
 #pragma unroll
   for (int c = 0; c < RN; ++c) offN[c] = swz<C2>(deposit(col(c), p.pN, p.tn));
-  const C2* __restrict__ A = reinterpret_cast<const C2*>(p.A);
-  const C2* __restrict__ B = reinterpret_cast<const C2*>(p.B);
+  const C2* __restrict__ A = reinterpret_cast<const C2*>(p.A) + slice_off(p.sv, true);
+  const C2* __restrict__ B = reinterpret_cast<const C2*>(p.B) + slice_off(p.sv, false);
   auto offsets = [&](int64_t w, int64_t& tile, int64_t& oa, int64_t& ob) {
     tile = blockIdx.x + (w / nk) * gridDim.x;
     const int64_t it = it0 + w % nk;
@@ -281,14 +299,36 @@ __global__ void reduce_splits_kernel(const typename V2<R>::t* __restrict__ P, ty
   }
 }
 
+// Device slice state: the current slice index and its digits (loop order, pos 0 outermost).
+struct SliceState {
+  int64_t s;
+  int32_t digits[64];
+};
+
+__global__ void set_slice_kernel(SliceState* st, int64_t s) {
+  if (threadIdx.x == 0) st->s = s;
+}
+
+// s += 1 and its mixed-radix digits (every sliced label has dimension d)
+__global__ void advance_slice_kernel(SliceState* st, int k, int d) {
+  if (threadIdx.x == 0) {
+    int64_t s = st->s + 1;
+    st->s = s;
+    for (int p = k - 1; p >= 0; --p) {
+      st->digits[p] = (int32_t)(s % d);
+      s /= d;
+    }
+  }
+}
+
 template <typename R>
 __global__ void accumulate_kernel(const typename V2<R>::t* __restrict__ root, double* __restrict__ acc,
-                                  double2* __restrict__ slicevals, int64_t idx) {
+                                  double2* __restrict__ slicevals, const SliceState* __restrict__ st) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const double re = (double)root[0].x, im = (double)root[0].y;
     acc[0] += re;
     acc[1] += im;
-    slicevals[idx] = make_double2(re, im);
+    slicevals[st->s] = make_double2(re, im);
   }
 }
 

@@ -42,6 +42,7 @@ struct TcArgs {
   int64_t gX[kTcMaxTile];        // B tile bit j (stride order): global stride
   int32_t sX[kTcMaxTile];        //   ... and byte offset in the X tile (canonical layout)
   int64_t aM[8], aK[8];          // A strides of its M bits / K bits
+  SliceView sv;
 };
 
 namespace tc {
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(256, 1) gett_tc_kernel(const __grid_constant__
       int64_t off = 0;
       for (int i = 0; i < p.tm; ++i) if ((m >> i) & 1) off += p.aM[i];
       for (int i = 0; i < p.tk; ++i) if ((k >> i) & 1) off += p.aK[i];
-      const float2 a = p.A[off];
+      const float2 a = p.A[off + slice_off(p.sv, true)];
       const float vals[2][2] = {{a.x, -a.y}, {a.y, a.x}};  // [s][t]
       for (int s = 0; s < 2; ++s)
         for (int t = 0; t < 2; ++t) {
@@ -178,8 +179,9 @@ __global__ void __launch_bounds__(256, 1) gett_tc_kernel(const __grid_constant__
     for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) o += p.o_sB[j];
     return o;
   };
+  const int64_t boff = slice_off(p.sv, false);
   auto prefetch = [&](int64_t t) {
-    const float2* src = p.B + tile_base(t);
+    const float2* src = p.B + boff + tile_base(t);
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int e = tid + i * 256;

@@ -230,3 +230,27 @@ def test_k3_tensor_cores_vs_cuda_cores(jet, c2_plan, monkeypatch):
     amp1, v1, _ = run(jet, plan, "c64", ranges=[(0, 8)])
     assert np.max(np.abs(v1 - v0) / np.abs(v0)) < 2e-5
     assert rel(amp1, amp0) < 2e-5
+
+
+def test_cuda_graph_replay_bitwise(jet, monkeypatch):
+    """Per-level CUDA graphs (device-side slice digits) give the same s_sigma bit for bit as
+    direct launches, across split ranges, and count the same executed FLOP."""
+    import torch
+
+    circ, bits = workload("C1")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=4, trials=16, n_sliced=5)
+    n = plan.cost()["n_sl"]
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("JETB200_GRAPHS", mode)
+        stream = torch.cuda.Stream()
+        ex = jet.Exec(plan, "c64", stream=stream)
+        acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        vals = np.concatenate([ex.contract(0, 11, acc, slice_values=True),
+                               ex.contract(11, n, acc, slice_values=True)])
+        torch.cuda.synchronize()
+        out[mode] = (vals, ex.stats()["flop_executed"])
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert out["0"][1] == out["1"][1] == plan.cost()["prefix"]
