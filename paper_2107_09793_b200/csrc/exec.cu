@@ -42,6 +42,7 @@ struct View {
 struct ExecNode {
   int kind = 0;  // 0: K2 CUDA-core GETT, 1: K3 tcgen05 3xTF32 (c64)
   TcArgs tc{};
+  std::vector<int64_t> tcB_n, tcB_k;  // K3: B strides of the 7 row bits and the K bits (emulator)
   int64_t v = -1;
   int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
   std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
@@ -68,13 +69,12 @@ struct Layout {
 using GettFn = void (*)(GettArgs);
 using TcFn = void (*)(TcArgs);
 
-TcFn pick_tc(int tk) {
-  switch (tk) {
-    case 2: return gett_tc_kernel<2>;
-    case 3: return gett_tc_kernel<4>;
-    case 4: return gett_tc_kernel<8>;
-    case 5: return gett_tc_kernel<16>;
-    case 6: return gett_tc_kernel<32>;
+TcFn pick_tc(int tkc) {
+  switch (tkc) {
+    case 2: return gett_tc_kernel<4>;
+    case 3: return gett_tc_kernel<8>;
+    case 4: return gett_tc_kernel<16>;
+    case 5: return gett_tc_kernel<32>;
   }
   fail(JT_EINTERNAL, "no tc instance");
 }
@@ -100,10 +100,9 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-    const void* tcs[5] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<4>),
-                          reinterpret_cast<const void*>(gett_tc_kernel<8>), reinterpret_cast<const void*>(gett_tc_kernel<16>),
-                          reinterpret_cast<const void*>(gett_tc_kernel<32>)};
-    for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    const void* tcs[4] = {reinterpret_cast<const void*>(gett_tc_kernel<4>), reinterpret_cast<const void*>(gett_tc_kernel<8>),
+                          reinterpret_cast<const void*>(gett_tc_kernel<16>), reinterpret_cast<const void*>(gett_tc_kernel<32>)};
+    for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2>),
@@ -133,11 +132,15 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   }
   for (auto& x : vb.bits)
     if (!sa.count(x.first)) N.push_back({x.second, x.first});
-  const int tm = (int)M.size(), tk = (int)K.size();
-  if (tm < 3 || tm > 7 || tk < 2 || tk > 5 || (int)N.size() < 7) return false;  // 7 + tk <= 12 table bits
-  const int Kp = 2 << tk, Np = 2 << tm;
-  const int64_t smem = 2LL * 4 * Kp * (128 + Np);
-  if (smem > 200 * 1024) return false;
+  const int tm = (int)M.size(), kt = (int)K.size();
+  if (tm < 3 || tm > 7 || kt < 2 || kt > 8 || (int)N.size() < 7) return false;
+  const int swz = kt >= 4 ? 1 : 0;        // SWIZZLE_128B needs 32 TF32 (16 complex) per row
+  const int tkc = swz ? 4 : kt;
+  const int n_kc = 1 << (kt - tkc);
+  const int Kpc = 2 << tkc, Np = 2 << tm;
+  const int xbuf = 128 * Kpc * 4, yplane = Np * Kpc * 4;
+  const int64_t smem = 4LL * xbuf + 2LL * n_kc * yplane + 1024;
+  if (smem > 220 * 1024) return false;
   std::sort(M.begin(), M.end());
   std::sort(N.begin(), N.end());
   std::sort(K.begin(), K.end());
@@ -147,32 +150,46 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   TcArgs& t = en.tc;
   std::memset(&t, 0, sizeof(t));
   t.tm = tm;
-  t.tk = tk;
-  t.nX = 7 + tk;
+  t.K = kt;
+  t.tkc = tkc;
+  t.n_kc = n_kc;
+  t.swz = swz;
+  t.nX = 7 + tkc;
   t.Np = Np;
-  t.Kp = Kp;
-  t.sbo = (Kp / 4) * 128;
+  t.Kpc = Kpc;
+  t.sbo_x = t.sbo_y = swz ? 1024 : (Kpc / 4) * 128;
+  t.xbuf = xbuf;
+  t.yplane = yplane;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t cols = 32;
-  while ((int)cols < Np) cols <<= 1;
+  while ((int)cols < 2 * Np) cols <<= 1;
   t.tmem_cols = cols;
-  // B tile bits in B-stride order with their byte offsets in the canonical K-major layout
+  // chunk-tile bits in B-stride order; byte offsets XOR-combine (SWIZZLE_128B folds row bits
+  // 0-2 onto the 16-B chunk index)
   std::vector<std::pair<int64_t, int32_t>> tb;
-  for (int i = 0; i < 7; ++i) tb.push_back({sb[tN[i]], i < 3 ? (16 << i) : (t.sbo << (i - 3))});
-  for (int i = 0; i < tk; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : (128 << (i - 1))});
+  for (int i = 0; i < 7; ++i) {
+    int32_t off = swz ? (i < 3 ? (144 << i) : (1024 << (i - 3))) : (i < 3 ? (16 << i) : (t.sbo_x << (i - 3)));
+    tb.push_back({sb[tN[i]], off});
+  }
+  for (int i = 0; i < tkc; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : ((swz ? 16 : 128) << (i - 1))});
   std::sort(tb.begin(), tb.end());
   for (size_t j = 0; j < tb.size(); ++j) {
     t.gX[j] = tb[j].first;
     t.sX[j] = tb[j].second;
   }
+  for (int j = 0; j < kt - tkc; ++j) t.o_kB[j] = sb[K[tkc + j].second];
   for (int i = 0; i < tm; ++i) t.aM[i] = sa[M[i].second];
-  for (int i = 0; i < tk; ++i) t.aK[i] = sa[K[i].second];
+  for (int i = 0; i < kt; ++i) t.aK[i] = sa[K[i].second];
   t.n_outer = (int)oN.size();
   for (int j = 0; j < t.n_outer; ++j) t.o_sB[j] = sb[oN[j]];
   t.n_tiles = int64_t(1) << t.n_outer;
+  en.tcB_n.clear();
+  en.tcB_k.clear();
+  for (int i = 0; i < 7; ++i) en.tcB_n.push_back(sb[tN[i]]);
+  for (int i = 0; i < kt; ++i) en.tcB_k.push_back(sb[K[i].second]);
   en.kind = 1;
   en.smem = (size_t)smem;
-  en.block = 256;
+  en.block = 288;
   en.n_out = t.n_tiles << (7 + tm);
   en.grid_x = t.n_tiles;
   en.args.splits = 1;
@@ -578,39 +595,37 @@ void emulate_gett(const GettArgs& p, char* ws, const ExecNode& en, const std::ve
   }
 }
 
-void emulate_tc(const TcArgs& p, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
+void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
   const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
   const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
   float2* C = reinterpret_cast<float2*>(ws + off[2].first);
-  // invert the B-tile byte offsets back to (row n, k) through the same per-bit tables
-  const int nX = p.nX;
+  const int nm = 1 << p.tm, nk = 1 << p.K;
+  std::vector<float2> a((size_t)nm * nk);
+  for (int m = 0; m < nm; ++m)
+    for (int k = 0; k < nk; ++k) {
+      int64_t ao = 0;
+      for (int i = 0; i < p.tm; ++i) if ((m >> i) & 1) ao += p.aM[i];
+      for (int i = 0; i < p.K; ++i) if ((k >> i) & 1) ao += p.aK[i];
+      a[(size_t)m * nk + k] = A[ao];
+    }
   for (int64_t t = 0; t < p.n_tiles; ++t) {
     int64_t base = 0;
     for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
-    std::vector<float2> Bt((size_t)128 << p.tk);
-    for (int e = 0; e < (1 << nX); ++e) {
-      int64_t g = 0;
-      int32_t byte = 0;
-      for (int j = 0; j < nX; ++j) if ((e >> j) & 1) { g += p.gX[j]; byte += p.sX[j]; }
-      // byte = (n&7)*16 + (n>>3)*sbo + (k>>1)*128 + (k&1)*8
-      const int n = ((byte % 128) / 16) + 8 * (byte / p.sbo);
-      const int rem = byte % p.sbo;
-      const int k = 2 * ((rem / 128)) + ((rem % 16) / 8);
-      Bt[(size_t)k * 128 + n] = B[base + g];
-    }
-    for (int m = 0; m < (1 << p.tm); ++m)
-      for (int n = 0; n < 128; ++n) {
+    for (int n = 0; n < 128; ++n) {
+      int64_t bn = base;
+      for (int i = 0; i < 7; ++i) if ((n >> i) & 1) bn += en.tcB_n[i];
+      for (int m = 0; m < nm; ++m) {
         double re = 0, im = 0;
-        for (int k = 0; k < (1 << p.tk); ++k) {
-          int64_t ao = 0;
-          for (int i = 0; i < p.tm; ++i) if ((m >> i) & 1) ao += p.aM[i];
-          for (int i = 0; i < p.tk; ++i) if ((k >> i) & 1) ao += p.aK[i];
-          const float2 a = A[ao], b = Bt[(size_t)k * 128 + n];
-          re += (double)a.x * b.x - (double)a.y * b.y;
-          im += (double)a.x * b.y + (double)a.y * b.x;
+        for (int k = 0; k < nk; ++k) {
+          int64_t bo = bn;
+          for (int i = 0; i < p.K; ++i) if ((k >> i) & 1) bo += en.tcB_k[i];
+          const float2 x = a[(size_t)m * nk + k], y = B[bo];
+          re += (double)x.x * y.x - (double)x.y * y.y;
+          im += (double)x.x * y.y + (double)x.y * y.x;
         }
         C[(t << (7 + p.tm)) + ((int64_t)m << 7) + n] = make_float2((float)re, (float)im);
       }
+    }
   }
 }
 
@@ -644,7 +659,7 @@ void emulate_host(const jt_plan& plan, int esize, int64_t b, int64_t e, double* 
       for (auto& sl : en.sliceB) offB += (int64_t)dig[sl.first] * sl.second;
       std::vector<std::pair<int64_t, int64_t>> offs = {{L.node_off[en.opA], offA}, {L.node_off[en.opB], offB},
                                                        {en.out_off, 0}, {en.part_off, 0}};
-      if (en.kind == 1) emulate_tc(en.tc, ws.data(), offs);
+      if (en.kind == 1) emulate_tc(en.tc, en, ws.data(), offs);
       else emulate_gett<R>(en.args, ws.data(), en, offs);
     }
     const C2 r = *reinterpret_cast<const C2*>(ws.data() + L.order.back().out_off);
@@ -723,7 +738,7 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
                  "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d}",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
                  g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind, en.tc.tm,
-                 en.tc.tk, en.tc.n_outer);
+                 en.tc.K, en.tc.n_outer);
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
@@ -756,7 +771,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   for (ExecNode& en : L.order) {
     int nb = 1;
     if (en.kind == 1) {
-      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tk)), 256,
+      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc)), 288,
                                                             en.smem));
       nb = std::min<int>(nb, 512 / (int)en.tc.tmem_cols);  // TMEM columns per SM
       if (nb < 1) fail(JT_EINTERNAL, "exec: a K3 tile does not fit on an SM");
@@ -853,7 +868,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
-    pick_tc(t.tk)<<<(unsigned)en.grid_x, 256, en.smem, ex->stream>>>(t);
+    pick_tc(t.tkc)<<<(unsigned)en.grid_x, 288, en.smem, ex->stream>>>(t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else {

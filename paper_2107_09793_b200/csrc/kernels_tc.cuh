@@ -26,22 +26,24 @@
 
 namespace jt {
 
-constexpr int kTcMaxTile = 13;  // 7 row bits + up to 6 K bits
+constexpr int kTcMaxTile = 12;  // 7 row bits + up to 5 K bits per chunk
 
 struct TcArgs {
   const float2* A;  // small operand (all bits in the tile)
   const float2* B;  // big operand
   float2* C;        // output, layout [7 row (n) bits][tm bits][outer bits]
   int64_t n_tiles;
-  int32_t n_outer, tm, tk, nX;   // nX = 7 + tk tile bits of B
-  int32_t Np, Kp;                // MMA N (2*2^tm padded to >= 16), K' (2*2^tk padded to >= 8)
-  int32_t sbo;                   // bytes between 8-row core-matrix groups (X and Y)
-  uint32_t idesc;                // instruction descriptor (kind::tf32, M=128, N=Np, F32 accum)
-  uint32_t tmem_cols;
-  int64_t o_sB[kMaxOuter];       // outer (row) bit j of B: stride
-  int64_t gX[kTcMaxTile];        // B tile bit j (stride order): global stride
-  int32_t sX[kTcMaxTile];        //   ... and byte offset in the X tile (canonical layout)
-  int64_t aM[8], aK[8];          // A strides of its M bits / K bits
+  int32_t n_outer, tm, K, tkc, n_kc, nX, swz;  // K contracted bits, tkc per chunk, n_kc = 2^(K-tkc)
+  int32_t Np, Kpc;                             // MMA N (2*2^tm); TF32 per row per chunk (2*2^tkc)
+  int32_t sbo_x, sbo_y;                        // bytes between 8-row core-matrix groups
+  int32_t xbuf, yplane;                        // bytes of one X buffer / one Y chunk plane (hi or lo)
+  uint32_t idesc;                              // kind::tf32, M=128, N=Np, F32 accumulate, K-major
+  uint32_t tmem_cols;                          // 2 accumulators of Np columns
+  int64_t o_sB[kMaxOuter];                     // outer (row) bit j of B: stride
+  int64_t o_kB[4];                             // chunk-index bit j of B: stride
+  int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
+  int32_t sX[kTcMaxTile];                      //   ... and its byte offset in the X buffer (XOR-combined)
+  int64_t aM[8], aK[8];                        // A strides of its M bits / K bits
   SliceView sv;
 };
 
@@ -49,15 +51,19 @@ namespace tc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-__device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo, uint32_t sbo) {
-  // start address [0,14), LBO [16,30), SBO [32,46) in 16-B units; version 1 at [46,48);
-  // base offset 0; layout SWIZZLE_NONE (0) at [61,64)
+// UMMA shared-memory descriptor: start address [0,14), LBO [16,30), SBO [32,46) in 16-B
+// units, version 1 at [46,48), layout type at [61,64) (0 = none, 2 = SWIZZLE_128B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
-  d |= (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
   return d;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -105,23 +111,31 @@ __device__ __forceinline__ float tf32_hi(float x) {
 
 }  // namespace tc
 
-// PER = elements of the B tile each thread carries between the prefetch and the smem store
-// (2^(7+tk) / 256 = 2^(tk-1)).
+// Byte offset of A-operand element (row r, tf32 column kk) inside one X buffer / Y plane.
+__device__ __forceinline__ int tc_off(int r, int kk, int sbo, int swz) {
+  if (swz) return (r & 7) * 128 + (r >> 3) * 1024 + ((((kk >> 2) ^ (r & 7)) & 7) << 4) + (kk & 3) * 4;
+  return (r & 7) * 16 + (r >> 3) * sbo + (kk >> 2) * 128 + (kk & 3) * 4;
+}
+
+// Warp-specialised K3.  Warps 0-3: epilogue (TMEM lane quarter w -> 256-B coalesced stores);
+// warps 4-7: producers (B chunk tile -> registers -> hi/lo split -> shared stage); warp 8:
+// MMA issuer (one elected thread).  Two X stages and two TMEM accumulators, so the loads of
+// item i+1, the MMAs of item i and the epilogue of the previous tile overlap.  Y (the expanded
+// small operand) is built once and stays resident for every K chunk.
+// PER = B-tile elements per producer thread = 2^(7+tkc) / 128.
 template <int PER>
-__global__ void __launch_bounds__(256, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
+__global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
-  __shared__ uint64_t mbar;
+  __shared__ __align__(8) uint64_t full[2], empty[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // smem carve: Xhi | Xlo | Yhi | Ylo, each operand tile = rows * Kp * 4 bytes
-  const int xbytes = 128 * p.Kp * 4;
-  const int ybytes = p.Np * p.Kp * 4;
-  unsigned char* Xhi = smem_raw;
-  unsigned char* Xlo = Xhi + xbytes;
-  unsigned char* Yhi = Xlo + xbytes;
-  unsigned char* Ylo = Yhi + ybytes;
+  // 1024-B aligned carve: X stage s = [hi | lo], then Y planes [hi c=0..n_kc-1 | lo ...]
+  unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* X = base;
+  unsigned char* Yhi = X + 4 * p.xbuf;
+  unsigned char* Ylo = Yhi + p.n_kc * p.yplane;
   for (int i = tid; i < 64; i += blockDim.x) {
     for (int h = 0; h < 2; ++h) {
       int64_t g = 0;
@@ -129,15 +143,12 @@ __global__ void __launch_bounds__(256, 1) gett_tc_kernel(const __grid_constant__
       for (int b = 0; b < 6; ++b)
         if ((i >> b) & 1) {
           const int bi = 6 * h + b;
-          if (bi < p.nX) { g += p.gX[bi]; s += p.sX[bi]; }
+          if (bi < p.nX) { g += p.gX[bi]; s ^= p.sX[bi]; }
         }
       tg[h][i] = g;
       ts[h][i] = s;
     }
   }
-  // zero the operand tiles (padding rows/columns of K' and N' must be finite zeros)
-  for (int i = tid; i < (2 * xbytes + 2 * ybytes) / 16; i += blockDim.x)
-    reinterpret_cast<float4*>(smem_raw)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_base_sh)),
                  "r"(p.tmem_cols)
@@ -145,27 +156,29 @@ __global__ void __launch_bounds__(256, 1) gett_tc_kernel(const __grid_constant__
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    tc::mbar_init(&mbar, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full[i], 128);
+      tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = tmem_base_sh;
-  // ---- Y = expanded small operand (hi/lo), built once: row = 2m+s, col = 2k+t
+  // ---- Y = expanded small operand (hi/lo) for every K chunk: row = 2m+s, col = 2k+t
   {
-    const int nm = 1 << p.tm, nk = 1 << p.tk;
+    const int nm = 1 << p.tm, nk = 1 << p.K, nkc = 1 << p.tkc;
+    const int64_t aoff = slice_off(p.sv, true);
     for (int idx = tid; idx < nm * nk; idx += blockDim.x) {
       const int m = idx % nm, k = idx / nm;
-      int64_t off = 0;
+      int64_t off = aoff;
       for (int i = 0; i < p.tm; ++i) if ((m >> i) & 1) off += p.aM[i];
-      for (int i = 0; i < p.tk; ++i) if ((k >> i) & 1) off += p.aK[i];
-      const float2 a = p.A[off + slice_off(p.sv, true)];
+      for (int i = 0; i < p.K; ++i) if ((k >> i) & 1) off += p.aK[i];
+      const float2 a = p.A[off];
       const float vals[2][2] = {{a.x, -a.y}, {a.y, a.x}};  // [s][t]
+      const int c = k / nkc, kl = k % nkc;
       for (int s = 0; s < 2; ++s)
         for (int t = 0; t < 2; ++t) {
-          const int row = 2 * m + s, kk = 2 * k + t;
-          const int byte = (row & 7) * 16 + (row >> 3) * p.sbo + (kk >> 2) * 128 + (kk & 3) * 4;
+          const int byte = c * p.yplane + tc_off(2 * m + s, 2 * kl + t, p.sbo_y, p.swz);
           const float x = vals[s][t];
           const float hi = tc::tf32_hi(x);
           *reinterpret_cast<float*>(Yhi + byte) = hi;
@@ -173,80 +186,109 @@ __global__ void __launch_bounds__(256, 1) gett_tc_kernel(const __grid_constant__
         }
     }
   }
-  float2 reg[PER];
-  auto tile_base = [&](int64_t t) {
-    int64_t o = 0;
-    for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) o += p.o_sB[j];
-    return o;
-  };
-  const int64_t boff = slice_off(p.sv, false);
-  auto prefetch = [&](int64_t t) {
-    const float2* src = p.B + boff + tile_base(t);
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int e = tid + i * 256;
-      reg[i] = src[tg[0][e & 63] + tg[1][e >> 6]];
-    }
-  };
-  auto stash = [&]() {
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int e = tid + i * 256;
-      const int byte = ts[0][e & 63] + ts[1][e >> 6];
-      const float hx = tc::tf32_hi(reg[i].x), hy = tc::tf32_hi(reg[i].y);
-      *reinterpret_cast<float2*>(Xhi + byte) = make_float2(hx, hy);
-      *reinterpret_cast<float2*>(Xlo + byte) = make_float2(reg[i].x - hx, reg[i].y - hy);
-    }
-  };
-  int64_t t = blockIdx.x;
-  if (t < p.n_tiles) {
-    prefetch(t);
-  }
-  uint32_t phase = 0;
-  for (; t < p.n_tiles; t += gridDim.x) {
-    stash();
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const int64_t tn = t + gridDim.x;
-    if (tn < p.n_tiles) prefetch(tn);  // in flight during the MMAs and the epilogue
-    if (tid == 0) {
-      const int ksteps = p.Kp / 8;
-      for (int ks = 0; ks < ksteps; ++ks) {
-        const uint64_t xh = tc::sdesc(Xhi + ks * 256, 128, p.sbo), xl = tc::sdesc(Xlo + ks * 256, 128, p.sbo);
-        const uint64_t yh = tc::sdesc(Yhi + ks * 256, 128, p.sbo), yl = tc::sdesc(Ylo + ks * 256, 128, p.sbo);
-        tc::mma_tf32(tmem, xh, yh, p.idesc, ks > 0 ? 1u : 0u);
-        tc::mma_tf32(tmem, xh, yl, p.idesc, 1u);
-        tc::mma_tf32(tmem, xl, yh, p.idesc, 1u);
-      }
-      tc::mma_commit(&mbar);
-    }
-    tc::mbar_wait(&mbar, phase);
-    phase ^= 1;
-    tc::fence_after();
-    // ---- epilogue: warp w reads TMEM lanes 32*(w%4)...; warps w and w+4 split the columns
-    const int quarter = warp & 3, half = warp >> 2;
-    const int row = quarter * 32 + lane;  // n within the tile
-    // column range of this warp: halves when Np >= 32, else warps 0-3 take all 16 columns
-    const int cbeg = p.Np >= 32 ? half * (p.Np / 2) : (half ? p.Np : 0);
-    const int cend = p.Np >= 32 ? (half + 1) * (p.Np / 2) : (half ? p.Np : p.Np);
-    float2* out = p.C + (t << (7 + p.tm));
-    const int nm = 1 << p.tm;
-    for (int c0 = cbeg; c0 < cend; c0 += 16) {
-      float v[16];
-      tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int m = c0 / 2 + j;
-        if (m < nm) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
-      }
-    }
-    tc::fence_before();
-    __syncthreads();  // TMEM and the X tile are free for the next tile
-    tc::fence_after();
-  }
+  tc::fence_proxy_async();
+  tc::fence_before();
   __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t items = my_tiles * p.n_kc;
+  auto tile_of = [&](int64_t it) { return (int64_t)blockIdx.x + (it / p.n_kc) * gridDim.x; };
+  const uint32_t layout = p.swz ? 2u : 0u;
+  const uint32_t lbo = p.swz ? 16u : 128u;
+  const uint32_t kstep = p.swz ? 32u : 256u;  // descriptor advance per 8-TF32 K step
+
+  if (warp >= 4 && warp < 8) {
+    // ===================== producers =====================
+    const int ptid = tid - 128;
+    const int64_t boff = slice_off(p.sv, false);
+    float2 reg[PER];
+    for (int64_t it = 0; it < items; ++it) {
+      const int s = (int)(it & 1);
+      const uint32_t ph = (uint32_t)((it >> 1) & 1);
+      const int64_t t = tile_of(it);
+      const int c = (int)(it % p.n_kc);
+      int64_t src = boff;
+      for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) src += p.o_sB[j];
+      for (int j = 0; j < p.K - p.tkc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int e = ptid + i * 128;
+        reg[i] = p.B[src + tg[0][e & 63] + tg[1][e >> 6]];
+      }
+      tc::mbar_wait(&empty[s], ph ^ 1);  // stage free (first use passes)
+      unsigned char* xhi = X + s * 2 * p.xbuf;
+      unsigned char* xlo = xhi + p.xbuf;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int e = ptid + i * 128;
+        const int byte = ts[0][e & 63] ^ ts[1][e >> 6];
+        const float hx = tc::tf32_hi(reg[i].x), hy = tc::tf32_hi(reg[i].y);
+        *reinterpret_cast<float2*>(xhi + byte) = make_float2(hx, hy);
+        *reinterpret_cast<float2*>(xlo + byte) = make_float2(reg[i].x - hx, reg[i].y - hy);
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&full[s]);
+    }
+  } else if (warp == 8) {
+    // ===================== MMA issuer =====================
+    const bool leader = lane == 0;
+    int64_t tt = 0;
+    for (int64_t it = 0; it < items; ++it) {
+      const int s = (int)(it & 1);
+      const uint32_t ph = (uint32_t)((it >> 1) & 1);
+      const int c = (int)(it % p.n_kc);
+      const int b = (int)(tt & 1);
+      const uint32_t tph = (uint32_t)((tt >> 1) & 1);
+      if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
+      tc::mbar_wait(&full[s], ph);
+      tc::fence_after();
+      if (leader) {
+        const uint32_t d = tmem + (uint32_t)(b * p.Np);
+        const uint32_t xh = tc::smem_u32(X + s * 2 * p.xbuf), xl = xh + p.xbuf;
+        const uint32_t yh = tc::smem_u32(Yhi + c * p.yplane), yl = tc::smem_u32(Ylo + c * p.yplane);
+        const int ksteps = p.Kpc / 8;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const uint32_t o = ks * kstep;
+          const uint64_t dxh = tc::sdesc(xh + o, lbo, p.sbo_x, layout), dxl = tc::sdesc(xl + o, lbo, p.sbo_x, layout);
+          const uint64_t dyh = tc::sdesc(yh + o, lbo, p.sbo_y, layout), dyl = tc::sdesc(yl + o, lbo, p.sbo_y, layout);
+          tc::mma_tf32(d, dxh, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_tf32(d, dxh, dyl, p.idesc, 1u);
+          tc::mma_tf32(d, dxl, dyh, p.idesc, 1u);
+        }
+        tc::mma_commit(&empty[s]);                      // stage s free once these MMAs finish
+        if (c == p.n_kc - 1) tc::mma_commit(&tfull[b]);  // tile accumulated
+      }
+      __syncwarp();
+      if (c == p.n_kc - 1) ++tt;
+    }
+  } else if (warp < 4) {
+    // ===================== epilogue =====================
+    const int row = warp * 32 + lane;
+    const int nm = 1 << p.tm;
+    for (int64_t tt = 0; tt < my_tiles; ++tt) {
+      const int b = (int)(tt & 1);
+      const uint32_t tph = (uint32_t)((tt >> 1) & 1);
+      tc::mbar_wait(&tfull[b], tph);
+      tc::fence_after();
+      const int64_t t = (int64_t)blockIdx.x + tt * gridDim.x;
+      float2* out = p.C + (t << (7 + p.tm));
+      for (int c0 = 0; c0 < p.Np; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.Np + c0), v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int m = c0 / 2 + j;
+          if (m < nm) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&tempty[b]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
 }
