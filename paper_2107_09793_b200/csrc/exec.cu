@@ -103,9 +103,11 @@ void set_smem_attrs() {
     const void* tcs[4] = {reinterpret_cast<const void*>(gett_tc_kernel<4>), reinterpret_cast<const void*>(gett_tc_kernel<8>),
                           reinterpret_cast<const void*>(gett_tc_kernel<16>), reinterpret_cast<const void*>(gett_tc_kernel<32>)};
     for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2>),
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, false>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2>),
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, true>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2, false>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
 }
@@ -1072,8 +1074,11 @@ void permute(jt_dtype dt, const void* src, void* dst, int n, const int32_t* perm
   if (nblk > (int64_t(1) << 31) - 1) fail(JT_EUSAGE, "permute: tensor too large");
   const size_t smem = (size_t)(int64_t(1) << p.nt) * esize;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (esize == 8) permute_kernel<float2><<<(unsigned)nblk, 256, smem, s>>>(p);
-  else permute_kernel<double2><<<(unsigned)nblk, 256, smem, s>>>(p);
+  // element pairs stay together when bit 0 maps to bit 0 (and the tile holds >= 2 elements)
+  const bool pair = esize == 8 && n >= 1 && perm[0] == 0 && p.nt >= 1 && p.in_g[0] == 1 && p.out_g[0] == 1;
+  if (esize == 8 && pair) permute_kernel<float2, true><<<(unsigned)nblk, 256, smem, s>>>(p);
+  else if (esize == 8) permute_kernel<float2, false><<<(unsigned)nblk, 256, smem, s>>>(p);
+  else permute_kernel<double2, false><<<(unsigned)nblk, 256, smem, s>>>(p);
   JT_CUDA(cudaGetLastError());
 }
 

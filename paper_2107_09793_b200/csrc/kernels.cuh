@@ -342,7 +342,9 @@ struct PermArgs {
   int32_t out_s[kMaxTile];  //   ... and smem stride
 };
 
-template <typename E>
+// PAIR (c64 only): address bit 0 stays bit 0, so element pairs move as 16 B on both sides.
+// The shared tile is XOR-swizzled (swz, 8-B units) so the output-order reads spread over banks.
+template <typename E, bool PAIR>
 __global__ void __launch_bounds__(256) permute_kernel(const __grid_constant__ PermArgs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* tileb = reinterpret_cast<E*>(smem_raw);
@@ -369,9 +371,19 @@ __global__ void __launch_bounds__(256) permute_kernel(const __grid_constant__ Pe
   const E* __restrict__ src = reinterpret_cast<const E*>(p.src);
   E* __restrict__ dst = reinterpret_cast<E*>(p.dst);
   const int sz = 1 << p.nt;
-  for (int e = tid; e < sz; e += blockDim.x) tileb[e] = src[bs + tin[0][e & 63] + tin[1][e >> 6]];
-  __syncthreads();
-  for (int f = tid; f < sz; f += blockDim.x) dst[bd + tout[0][f & 63] + tout[1][f >> 6]] = tileb[tso[0][f & 63] + tso[1][f >> 6]];
+  if (PAIR) {
+    for (int e = 2 * tid; e < sz; e += 2 * blockDim.x)
+      *reinterpret_cast<float4*>(tileb + swz<E>(e)) = *reinterpret_cast<const float4*>(src + bs + tin[0][e & 63] + tin[1][e >> 6]);
+    __syncthreads();
+    for (int f = 2 * tid; f < sz; f += 2 * blockDim.x)
+      *reinterpret_cast<float4*>(dst + bd + tout[0][f & 63] + tout[1][f >> 6]) =
+          *reinterpret_cast<const float4*>(tileb + swz<E>(tso[0][f & 63] + tso[1][f >> 6]));
+  } else {
+    for (int e = tid; e < sz; e += blockDim.x) tileb[swz<E>(e)] = src[bs + tin[0][e & 63] + tin[1][e >> 6]];
+    __syncthreads();
+    for (int f = tid; f < sz; f += blockDim.x)
+      dst[bd + tout[0][f & 63] + tout[1][f >> 6]] = tileb[swz<E>(tso[0][f & 63] + tso[1][f >> 6])];
+  }
 }
 
 }  // namespace jt
