@@ -74,7 +74,6 @@ TcFn pick_tc(int tkc) {
     case 2: return gett_tc_kernel<4>;
     case 3: return gett_tc_kernel<8>;
     case 4: return gett_tc_kernel<16>;
-    case 5: return gett_tc_kernel<32>;
   }
   fail(JT_EINTERNAL, "no tc instance");
 }
@@ -100,8 +99,8 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-    const void* tcs[4] = {reinterpret_cast<const void*>(gett_tc_kernel<4>), reinterpret_cast<const void*>(gett_tc_kernel<8>),
-                          reinterpret_cast<const void*>(gett_tc_kernel<16>), reinterpret_cast<const void*>(gett_tc_kernel<32>)};
+    const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<4>), reinterpret_cast<const void*>(gett_tc_kernel<8>),
+                          reinterpret_cast<const void*>(gett_tc_kernel<16>)};
     for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, false>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1047,11 +1046,15 @@ void permute(jt_dtype dt, const void* src, void* dst, int n, const int32_t* perm
   p.src = src;
   p.dst = dst;
   // tile: the lowest input bits and the lowest output bits (as input bits)
+  // tile = the lowest `half` input bits + the lowest `half` output bits, filled with further
+  // low input bits to 2^12 (c64) / 2^11 (c128) elements: 32 KB per CTA keeps enough bytes in
+  // flight per SM
   const int half = esize == 8 ? 5 : 4;
+  const int tile_bits = esize == 8 ? 12 : 11;
   std::vector<char> in_tile(n, 0);
   for (int b = 0; b < std::min(n, half); ++b) in_tile[b] = 1;          // low input bits
   for (int o = 0; o < std::min(n, half); ++o) in_tile[inv[o]] = 1;     // low output bits
-  for (int b = 0; b < n && std::count(in_tile.begin(), in_tile.end(), 1) < std::min(n, 2 * half); ++b)
+  for (int b = 0; b < n && std::count(in_tile.begin(), in_tile.end(), 1) < std::min(n, tile_bits); ++b)
     in_tile[b] = 1;
   std::vector<int> tbits, obits;
   for (int b = 0; b < n; ++b) (in_tile[b] ? tbits : obits).push_back(b);

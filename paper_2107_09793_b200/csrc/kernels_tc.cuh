@@ -200,12 +200,13 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
 
   if (warp >= 4 && warp < 8) {
     // ===================== producers =====================
+    // Three register sets keep up to three items' loads in flight per thread (the HBM
+    // latency x bandwidth product needs ~40 KB in flight per SM); each item is then split
+    // into hi/lo and stored into its X stage once the MMAs have released that stage.
     const int ptid = tid - 128;
     const int64_t boff = slice_off(p.sv, false);
-    float2 reg[PER];
-    for (int64_t it = 0; it < items; ++it) {
-      const int s = (int)(it & 1);
-      const uint32_t ph = (uint32_t)((it >> 1) & 1);
+    float2 r0[PER], r1[PER], r2[PER];
+    auto issue = [&](float2 (&reg)[PER], int64_t it) {
       const int64_t t = tile_of(it);
       const int c = (int)(it % p.n_kc);
       int64_t src = boff;
@@ -216,6 +217,10 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
         const int e = ptid + i * 128;
         reg[i] = p.B[src + tg[0][e & 63] + tg[1][e >> 6]];
       }
+    };
+    auto drain = [&](float2 (&reg)[PER], int64_t it) {
+      const int s = (int)(it & 1);
+      const uint32_t ph = (uint32_t)((it >> 1) & 1);
       tc::mbar_wait(&empty[s], ph ^ 1);  // stage free (first use passes)
       unsigned char* xhi = X + s * 2 * p.xbuf;
       unsigned char* xlo = xhi + p.xbuf;
@@ -229,6 +234,20 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
       }
       tc::fence_proxy_async();
       tc::mbar_arrive(&full[s]);
+    };
+    if (items > 0) issue(r0, 0);
+    if (items > 1) issue(r1, 1);
+    for (int64_t it = 0; it < items; it += 3) {
+      if (it + 2 < items) issue(r2, it + 2);
+      drain(r0, it);
+      if (it + 1 < items) {
+        if (it + 3 < items) issue(r0, it + 3);
+        drain(r1, it + 1);
+      }
+      if (it + 2 < items) {
+        if (it + 4 < items) issue(r1, it + 4);
+        drain(r2, it + 2);
+      }
     }
   } else if (warp == 8) {
     // ===================== MMA issuer =====================
