@@ -140,7 +140,12 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   const int n_kc = 1 << (kt - tkc);
   const int Kpc = 2 << tkc, Np = 2 << tm;
   const int xbuf = 128 * Kpc * 4, yplane = Np * Kpc * 4;
-  const int64_t smem = 4LL * xbuf + 2LL * n_kc * yplane + 1024;
+  int xstages = 3;
+  int64_t smem = 2LL * xstages * xbuf + 2LL * n_kc * yplane + 1024;
+  if (smem > 220 * 1024) {
+    xstages = 2;
+    smem = 2LL * xstages * xbuf + 2LL * n_kc * yplane + 1024;
+  }
   if (smem > 220 * 1024) return false;
   std::sort(M.begin(), M.end());
   std::sort(N.begin(), N.end());
@@ -161,6 +166,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   t.sbo_x = t.sbo_y = swz ? 1024 : (Kpc / 4) * 128;
   t.xbuf = xbuf;
   t.yplane = yplane;
+  t.xstages = xstages;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t cols = 32;
   while ((int)cols < 2 * Np) cols <<= 1;

@@ -39,6 +39,7 @@ struct TcArgs {
   int32_t xbuf, yplane;                        // bytes of one X buffer / one Y chunk plane (hi or lo)
   uint32_t idesc;                              // kind::tf32, M=128, N=Np, F32 accumulate, K-major
   uint32_t tmem_cols;                          // 2 accumulators of Np columns
+  int32_t xstages;                             // X stages (2 or 3): cp.async runs xstages-1 items ahead
   int64_t o_sB[kMaxOuter];                     // outer (row) bit j of B: stride
   int64_t o_kB[4];                             // chunk-index bit j of B: stride
   int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
@@ -128,13 +129,13 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
-  __shared__ __align__(8) uint64_t full[2], empty[2], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[3], empty[3], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // 1024-B aligned carve: X stage s = [hi | lo], then Y planes [hi c=0..n_kc-1 | lo ...]
   unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* X = base;
-  unsigned char* Yhi = X + 4 * p.xbuf;
+  unsigned char* Yhi = X + 2 * p.xstages * p.xbuf;
   unsigned char* Ylo = Yhi + p.n_kc * p.yplane;
   for (int i = tid; i < 64; i += blockDim.x) {
     for (int h = 0; h < 2; ++h) {
@@ -156,9 +157,11 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
       tc::mbar_init(&full[i], 128);
       tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 128);
     }
@@ -200,62 +203,66 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
 
   if (warp >= 4 && warp < 8) {
     // ===================== producers =====================
-    // Three register sets keep up to three items' loads in flight per thread (the HBM
-    // latency x bandwidth product needs ~40 KB in flight per SM); each item is then split
-    // into hi/lo and stored into its X stage once the MMAs have released that stage.
+    // cp.async (no registers, commit groups instead of scoreboards) lands each item's B data
+    // straight into its X stage at the operand-layout position, XSTAGES-1 items ahead; the
+    // thread then splits the elements it copied in place into hi (X_hi) and lo (X_lo).
     const int ptid = tid - 128;
     const int64_t boff = slice_off(p.sv, false);
-    float2 r0[PER], r1[PER], r2[PER];
-    auto issue = [&](float2 (&reg)[PER], int64_t it) {
+    int bytes_of[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = ptid + i * 128;
+      bytes_of[i] = ts[0][e & 63] ^ ts[1][e >> 6];
+    }
+    const int S = p.xstages;
+    auto issue = [&](int64_t it) {
+      const int s = (int)(it % S);
+      const uint32_t ph = (uint32_t)((it / S) & 1);
+      tc::mbar_wait(&empty[s], ph ^ 1);  // stage free (first use passes)
       const int64_t t = tile_of(it);
       const int c = (int)(it % p.n_kc);
       int64_t src = boff;
       for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) src += p.o_sB[j];
       for (int j = 0; j < p.K - p.tkc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
+      unsigned char* xhi = X + s * 2 * p.xbuf;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int e = ptid + i * 128;
-        reg[i] = p.B[src + tg[0][e & 63] + tg[1][e >> 6]];
+        cp_async8(xhi + bytes_of[i], p.B + src + tg[0][e & 63] + tg[1][e >> 6]);
       }
     };
-    auto drain = [&](float2 (&reg)[PER], int64_t it) {
-      const int s = (int)(it & 1);
-      const uint32_t ph = (uint32_t)((it >> 1) & 1);
-      tc::mbar_wait(&empty[s], ph ^ 1);  // stage free (first use passes)
+    const int64_t depth = S - 1;
+    for (int64_t q = 0; q < depth; ++q) {
+      if (q < items) issue(q);
+      cp_async_commit();  // (possibly empty) group per slot keeps the group arithmetic uniform
+    }
+    for (int64_t it = 0; it < items; ++it) {
+      // groups committed so far: depth + it; item it's group is the oldest of the last depth
+      if (S == 3) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      const int s = (int)(it % S);
       unsigned char* xhi = X + s * 2 * p.xbuf;
       unsigned char* xlo = xhi + p.xbuf;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
-        const int e = ptid + i * 128;
-        const int byte = ts[0][e & 63] ^ ts[1][e >> 6];
-        const float hx = tc::tf32_hi(reg[i].x), hy = tc::tf32_hi(reg[i].y);
-        *reinterpret_cast<float2*>(xhi + byte) = make_float2(hx, hy);
-        *reinterpret_cast<float2*>(xlo + byte) = make_float2(reg[i].x - hx, reg[i].y - hy);
+        const float2 v = *reinterpret_cast<const float2*>(xhi + bytes_of[i]);
+        const float hx = tc::tf32_hi(v.x), hy = tc::tf32_hi(v.y);
+        *reinterpret_cast<float2*>(xhi + bytes_of[i]) = make_float2(hx, hy);
+        *reinterpret_cast<float2*>(xlo + bytes_of[i]) = make_float2(v.x - hx, v.y - hy);
       }
       tc::fence_proxy_async();
       tc::mbar_arrive(&full[s]);
-    };
-    if (items > 0) issue(r0, 0);
-    if (items > 1) issue(r1, 1);
-    for (int64_t it = 0; it < items; it += 3) {
-      if (it + 2 < items) issue(r2, it + 2);
-      drain(r0, it);
-      if (it + 1 < items) {
-        if (it + 3 < items) issue(r0, it + 3);
-        drain(r1, it + 1);
-      }
-      if (it + 2 < items) {
-        if (it + 4 < items) issue(r1, it + 4);
-        drain(r2, it + 2);
-      }
+      if (it + depth < items) issue(it + depth);
+      cp_async_commit();
     }
   } else if (warp == 8) {
     // ===================== MMA issuer =====================
     const bool leader = lane == 0;
     int64_t tt = 0;
+    const int S = p.xstages;
     for (int64_t it = 0; it < items; ++it) {
-      const int s = (int)(it & 1);
-      const uint32_t ph = (uint32_t)((it >> 1) & 1);
+      const int s = (int)(it % S);
+      const uint32_t ph = (uint32_t)((it / S) & 1);
       const int c = (int)(it % p.n_kc);
       const int b = (int)(tt & 1);
       const uint32_t tph = (uint32_t)((tt >> 1) & 1);

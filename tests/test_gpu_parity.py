@@ -254,3 +254,62 @@ def test_cuda_graph_replay_bitwise(jet, monkeypatch):
         out[mode] = (vals, ex.stats()["flop_executed"])
     assert np.array_equal(out["0"][0], out["1"][0])
     assert out["0"][1] == out["1"][1] == plan.cost()["prefix"]
+
+
+# ----------------------------------------------------------------------------- C3 (Sycamore-53 m=14)
+@pytest.fixture(scope="module")
+def c3_plan(jet):
+    from paper_2107_09793_b200.runtime import plan_best
+
+    circ, bits = workload("C3")
+    net = jet.Network.from_circuit(circ, bits)
+    plan, _ = plan_best(net, 10, trials=1024)
+    return circ, bits, net, plan
+
+
+def test_c3_full_size_sampled_slices(jet, c3_plan):
+    """BASELINE config C3 at full size, in the bench's launch configuration: the oracle
+    contracts two seeded slices of the same plan one by one and every s_sigma matches."""
+    import torch
+
+    circ, bits, net, plan = c3_plan
+    n_sl = plan.cost()["n_sl"]
+    picks = [0, int(np.random.default_rng(3).integers(1, n_sl))]
+    onet = build_network(circ, bits)
+    ref = contract.slice_values(onet, plan.ssa_path, plan.sliced_labels, indices=picks)
+    stream = torch.cuda.Stream()
+    ex = jet.Exec(plan, "c64", stream=stream)
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    for p_, r in zip(picks, ref):
+        v = ex.contract(p_, p_ + 1, acc, slice_values=True)[0]
+        assert abs(v - r) <= 1e-4 * abs(r), (p_, v, r)
+
+
+def test_c3_fsim_identity_closed_form_full_amplitude(jet):
+    """P7 at C3 scale: with fSim(0, 0) = I the full 1024-slice m=14 amplitude is the product
+    of 53 one-qubit chains."""
+    import torch
+
+    from paper_2107_09793_b200.runtime import plan_best
+
+    qs = sycamore_qubits(53)
+    circ = random_circuit(qs, 14, seed=1, theta=0.0, phi=0.0)
+    bits = random_bitstring(53, 2, 1)
+    want = 1 + 0j
+    for q in range(53):
+        v = np.array([1, 0], dtype=np.complex128)
+        for g in circ.gates:
+            if g.wires == (q,):
+                v = g.u @ v
+        want *= v[bits[q]]
+    net = jet.Network.from_circuit(circ, bits)
+    plan, _ = plan_best(net, 10, trials=256)
+    stream = torch.cuda.Stream()
+    ex = jet.Exec(plan, "c64", stream=stream)
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ex.contract(0, plan.cost()["n_sl"], acc)
+    torch.cuda.synchronize()
+    amp = complex(acc[0].item(), acc[1].item())
+    assert rel(amp, want) < 1e-4
