@@ -62,6 +62,14 @@ typedef struct {
   double bytes_weight;    /* roofline objective: node cost = max(d^union, w (|A|+|B|+|C|)) with
                              w = peak FLOP/s * esize / (8 * HBM B/s); <=0 -> pure FLOP (d^union) */
   int32_t candidates;     /* greedy trees carried through reconfiguration + slicing; <=0 -> 8 */
+  /* kernel-aware roofline objective (used when model_hbm_gbs > 0, overrides bytes_weight):
+     node time = max(FLOP / rate, bytes / HBM) + launch gap, with rate = model_tc_tflops for
+     contractions K3 can run and model_cuda_tflops otherwise */
+  double model_hbm_gbs;
+  double model_cuda_tflops;
+  double model_tc_tflops;
+  double model_launch_us;
+  double model_esize;     /* bytes per element (8 = c64, 16 = c128) */
 } jt_planner_opts;
 
 /* Cost counters (PAPER.md l.140-146 Eq. sliced_flops, l.205-212 Eq. task_based;
@@ -87,12 +95,17 @@ typedef struct {
   int64_t kernel_launches; /* every kernel launched (contractions, reductions, accumulate) */
   double flop_executed;    /* algorithmic FLOP of the executed nodes (compare with jt_cost.prefix) */
   double bytes_executed;   /* algorithmic bytes of the executed nodes, at the exec dtype size */
-  /* filled only while profiling is on (jt_exec_set_profiling): CUDA-event time of every K2
-     contraction launch on the exec stream, and the algorithmic bytes/FLOP of those launches */
+  /* filled only while profiling is on (jt_exec_set_profiling): CUDA-event time of every
+     contraction launch (K2 or K3) on the exec stream, and the algorithmic bytes/FLOP of those
+     launches */
   double k2_time_ms;
   int64_t k2_timed_launches;
   double k2_timed_bytes;
   double k2_timed_flop;
+  double k3_time_ms;          /* ... the subset of those launches that ran on K3 (tcgen05) */
+  int64_t k3_timed_launches;
+  double k3_timed_bytes;
+  double k3_timed_flop;
   int64_t h2d_bytes;       /* host->device bytes copied by jt_exec_create / jt_exec_upload_leaves */
 } jt_exec_stats;
 

@@ -707,6 +707,7 @@ struct jt_exec {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // event pool for K2 timing
   size_t ev_used = 0;
   std::vector<std::pair<double, double>> ev_work;        // (bytes, flop) of each timed launch
+  std::vector<int> ev_kind;                              // 0 = K2, 1 = K3
   bool use_graphs = true;
   std::vector<cudaGraphExec_t> graphs;   // per prefix-cache level j+1 (j = -1..k)
   std::vector<jt_exec_stats> graph_stats;
@@ -861,6 +862,7 @@ void ev_end(jt_exec* ex, const ExecNode& en) {
   if (!ex->profiling) return;
   JT_CUDA(cudaEventRecord(ex->ev[ex->ev_used].second, ex->stream));
   ex->ev_work.push_back({en.bytes, en.flop});
+  ex->ev_kind.push_back(en.kind);
   ex->ev_used++;
 }
 
@@ -983,6 +985,7 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
   JT_CUDA(cudaSetDevice(ex->device));
   ex->ev_used = 0;
   ex->ev_work.clear();
+  ex->ev_kind.clear();
   if (ex->dtype == JT_C64) contract_range<float>(ex, b, e, d_acc, reuse);
   else contract_range<double>(ex, b, e, d_acc, reuse);
   if (ex->profiling && ex->ev_used) {
@@ -994,6 +997,12 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
       ex->stats.k2_timed_launches++;
       ex->stats.k2_timed_bytes += ex->ev_work[i].first;
       ex->stats.k2_timed_flop += ex->ev_work[i].second;
+      if (ex->ev_kind[i] == 1) {
+        ex->stats.k3_time_ms += ms;
+        ex->stats.k3_timed_launches++;
+        ex->stats.k3_timed_bytes += ex->ev_work[i].first;
+        ex->stats.k3_timed_flop += ex->ev_work[i].second;
+      }
     }
   }
   if (h_vals && e > b) {

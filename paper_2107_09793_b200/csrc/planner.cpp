@@ -93,10 +93,28 @@ struct CostModel {
   std::vector<double> dpow;  // d^n
   int cap = std::numeric_limits<int>::max();  // max output width in labels
   double R = 0;  // roofline weight: FLOP/8 per element moved (0 = pure FLOP objective)
-  // Roofline time model in FLOP/8 units: max(d^union, R (|A|+|B|+|C|)).
+  // Kernel-aware roofline model (seconds), used when rf_bw > 0: a contraction that K3 can run
+  // (qubits: small side 3..7 free bits, 2..8 contracted bits, big side >= 7 free bits) costs
+  // max(flop / rf_tc, bytes / rf_bw), any other max(flop / rf_cuda, bytes / rf_bw); plus a
+  // fixed per-launch gap.
+  double rf_bw = 0, rf_cuda = 0, rf_tc = 0, rf_gap = 0, esize = 8;
+  bool qubits = true;
   double node_cost(int n_union, int n_a, int n_b, int n_out) const {
-    double c = dpow[n_union];
-    if (R > 0) c = std::max(c, R * (dpow[n_a] + dpow[n_b] + dpow[n_out]));
+    double c;
+    if (rf_bw > 0) {
+      const double flop = 8.0 * dpow[n_union];
+      const double bytes = esize * (dpow[n_a] + dpow[n_b] + dpow[n_out]);
+      double F = rf_cuda;
+      if (qubits && rf_tc > 0) {
+        const int k = n_a + n_b - n_union, fa = n_a - k, fb = n_b - k;
+        const int small = std::min(fa, fb), big = std::max(fa, fb);
+        if (small >= 3 && small <= 7 && k >= 2 && k <= 8 && big >= 7) F = rf_tc;
+      }
+      c = std::max(flop / F, bytes / rf_bw) + rf_gap;
+    } else {
+      c = dpow[n_union];
+      if (R > 0) c = std::max(c, R * (dpow[n_a] + dpow[n_b] + dpow[n_out]));
+    }
     if (n_out > cap) c *= 1e6;  // soft width cap (in labels)
     return c;
   }
@@ -551,6 +569,14 @@ void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<in
   CostModel cm;
   cm.log2d = std::log2((double)net.d);
   cm.R = o.bytes_weight > 0 ? o.bytes_weight : 0.0;
+  if (o.model_hbm_gbs > 0) {
+    cm.rf_bw = o.model_hbm_gbs * 1e9;
+    cm.rf_cuda = o.model_cuda_tflops > 0 ? o.model_cuda_tflops * 1e12 : 40e12;
+    cm.rf_tc = o.model_tc_tflops > 0 ? o.model_tc_tflops * 1e12 : 0.0;
+    cm.rf_gap = o.model_launch_us * 1e-6;
+    cm.esize = o.model_esize > 0 ? o.model_esize : 8;
+    cm.qubits = net.d == 2;
+  }
   cm.dpow.resize(NL + 2);
   for (int i = 0; i <= NL + 1; ++i) cm.dpow[i] = std::pow((double)net.d, (double)i);
 

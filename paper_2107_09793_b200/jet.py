@@ -31,7 +31,9 @@ P_dbl = ctypes.POINTER(c_dbl)
 class PlannerOpts(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("trials", c_i32), ("threads", c_i32), ("n_sliced", c_i32),
                 ("width_cap", c_i32), ("reconf_sweeps", c_i32), ("reconf_leaves", c_i32),
-                ("time_budget_s", c_dbl), ("bytes_weight", c_dbl), ("candidates", c_i32)]
+                ("time_budget_s", c_dbl), ("bytes_weight", c_dbl), ("candidates", c_i32),
+                ("model_hbm_gbs", c_dbl), ("model_cuda_tflops", c_dbl), ("model_tc_tflops", c_dbl),
+                ("model_launch_us", c_dbl), ("model_esize", c_dbl)]
 
 
 class Cost(ctypes.Structure):
@@ -47,7 +49,8 @@ class ExecStats(ctypes.Structure):
     _fields_ = [("slices_done", c_i64), ("node_launches", c_i64), ("kernel_launches", c_i64),
                 ("flop_executed", c_dbl), ("bytes_executed", c_dbl), ("k2_time_ms", c_dbl),
                 ("k2_timed_launches", c_i64), ("k2_timed_bytes", c_dbl), ("k2_timed_flop", c_dbl),
-                ("h2d_bytes", c_i64)]
+                ("k3_time_ms", c_dbl), ("k3_timed_launches", c_i64), ("k3_timed_bytes", c_dbl),
+                ("k3_timed_flop", c_dbl), ("h2d_bytes", c_i64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -185,9 +188,11 @@ class Plan:
 
     @classmethod
     def greedy(cls, net, seed=1, trials=64, threads=0, n_sliced=0, width_cap=0, reconf_sweeps=-1,
-               reconf_leaves=0, time_budget_s=0.0, bytes_weight=0.0, candidates=0):
+               reconf_leaves=0, time_budget_s=0.0, bytes_weight=0.0, candidates=0, model=None):
+        m = model or {}
         o = PlannerOpts(seed, trials, threads, n_sliced, width_cap, reconf_sweeps, reconf_leaves, time_budget_s,
-                        bytes_weight, candidates)
+                        bytes_weight, candidates, m.get("hbm_gbs", 0.0), m.get("cuda_tflops", 0.0),
+                        m.get("tc_tflops", 0.0), m.get("launch_us", 0.0), m.get("esize", 0.0))
         h = c_vp()
         _check(_lib.jt_plan_greedy(net._h, ctypes.byref(o), ctypes.byref(h)))
         return cls(h, net)
