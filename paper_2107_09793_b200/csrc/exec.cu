@@ -71,9 +71,9 @@ using TcFn = void (*)(TcArgs);
 
 TcFn pick_tc(int tkc) {
   switch (tkc) {
-    case 2: return gett_tc_kernel<4>;
-    case 3: return gett_tc_kernel<8>;
-    case 4: return gett_tc_kernel<16>;
+    case 2: return gett_tc_kernel<2>;
+    case 3: return gett_tc_kernel<4>;
+    case 4: return gett_tc_kernel<8>;
   }
   fail(JT_EINTERNAL, "no tc instance");
 }
@@ -99,8 +99,8 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-    const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<4>), reinterpret_cast<const void*>(gett_tc_kernel<8>),
-                          reinterpret_cast<const void*>(gett_tc_kernel<16>)};
+    const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<4>),
+                          reinterpret_cast<const void*>(gett_tc_kernel<8>)};
     for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, false>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -196,7 +196,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (int i = 0; i < kt; ++i) en.tcB_k.push_back(sb[K[i].second]);
   en.kind = 1;
   en.smem = (size_t)smem;
-  en.block = 288;
+  en.block = 416;
   en.n_out = t.n_tiles << (7 + tm);
   en.grid_x = t.n_tiles;
   en.args.splits = 1;
@@ -779,7 +779,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   for (ExecNode& en : L.order) {
     int nb = 1;
     if (en.kind == 1) {
-      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc)), 288,
+      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc)), 416,
                                                             en.smem));
       nb = std::min<int>(nb, 512 / (int)en.tc.tmem_cols);  // TMEM columns per SM
       if (nb < 1) fail(JT_EINTERNAL, "exec: a K3 tile does not fit on an SM");
@@ -877,7 +877,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
-    pick_tc(t.tkc)<<<(unsigned)en.grid_x, 288, en.smem, ex->stream>>>(t);
+    pick_tc(t.tkc)<<<(unsigned)en.grid_x, 416, en.smem, ex->stream>>>(t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else {

@@ -109,6 +109,10 @@ __device__ __forceinline__ float tf32_hi(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// 3xTF32 split by truncation: hi = x with the low 13 mantissa bits cleared (exactly a TF32
+// value, so the MMA reads it exactly whatever its own rounding), lo = x - hi (exact in fp32);
+// lo is then read at TF32 precision (relative error 2^-11 of lo, ~2^-22 of x).
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 }  // namespace tc
 
@@ -119,13 +123,13 @@ __device__ __forceinline__ int tc_off(int r, int kk, int sbo, int swz) {
 }
 
 // Warp-specialised K3.  Warps 0-3: epilogue (TMEM lane quarter w -> 256-B coalesced stores);
-// warps 4-7: producers (B chunk tile -> registers -> hi/lo split -> shared stage); warp 8:
+// warps 4-11: producers (B chunk tile -> shared stage by cp.async, lo split in place); warp 12:
 // MMA issuer (one elected thread).  Two X stages and two TMEM accumulators, so the loads of
 // item i+1, the MMAs of item i and the epilogue of the previous tile overlap.  Y (the expanded
 // small operand) is built once and stays resident for every K chunk.
-// PER = B-tile elements per producer thread = 2^(7+tkc) / 128.
+// PER = B-tile elements per producer thread = 2^(7+tkc) / 256.
 template <int PER>
-__global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
+__global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
   }
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) {
-      tc::mbar_init(&full[i], 128);
+      tc::mbar_init(&full[i], 256);
       tc::mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
         for (int t = 0; t < 2; ++t) {
           const int byte = c * p.yplane + tc_off(2 * m + s, 2 * kl + t, p.sbo_y, p.swz);
           const float x = vals[s][t];
-          const float hi = tc::tf32_hi(x);
+          const float hi = tc::tf32_trunc(x);
           *reinterpret_cast<float*>(Yhi + byte) = hi;
           *reinterpret_cast<float*>(Ylo + byte) = x - hi;
         }
@@ -201,12 +205,12 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
   const uint32_t lbo = p.swz ? 16u : 128u;
   const uint32_t kstep = p.swz ? 32u : 256u;  // descriptor advance per 8-TF32 K step
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 4 && warp < 12) {
     // ===================== producers =====================
     // cp.async (no registers, commit groups instead of scoreboards) lands each item's B data
     // straight into its X stage at the operand-layout position, XSTAGES-1 items ahead; the
     // thread then splits the elements it copied in place into hi (X_hi) and lo (X_lo).
-    const int ptid = tid - 128;
+    const int ptid = tid - 128;  // 0..255
     const int64_t boff = slice_off(p.sv, false);
     int bytes_of[PER];
 #pragma unroll
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
       unsigned char* xhi = X + s * 2 * p.xbuf;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
-        const int e = ptid + i * 128;
+        const int e = ptid + i * 256;
         cp_async8(xhi + bytes_of[i], p.B + src + tg[0][e & 63] + tg[1][e >> 6]);
       }
     };
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const float2 v = *reinterpret_cast<const float2*>(xhi + bytes_of[i]);
-        const float hx = tc::tf32_hi(v.x), hy = tc::tf32_hi(v.y);
+        const float hx = tc::tf32_trunc(v.x), hy = tc::tf32_trunc(v.y);
         *reinterpret_cast<float2*>(xhi + bytes_of[i]) = make_float2(hx, hy);
         *reinterpret_cast<float2*>(xlo + bytes_of[i]) = make_float2(v.x - hx, v.y - hy);
       }
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(288, 1) gett_tc_kernel(const __grid_constant__
       if (it + depth < items) issue(it + depth);
       cp_async_commit();
     }
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // ===================== MMA issuer =====================
     const bool leader = lane == 0;
     int64_t tt = 0;
