@@ -29,7 +29,8 @@ CONFIGS = {
     # name: circuit key, sliced labels, dtype, slices per step, workload name
     "C2": dict(circ="C2", k=6, dtype="c64", sps=64, workload="sycamore53_m10_2^6slices"),
     "C3": dict(circ="C3", k=10, dtype="c64", sps=16, workload="sycamore53_m14_2^10slices"),
-    "C5": dict(circ="C5", k=None, dtype="c64", sps=4, workload="sycamore53_m20_subset"),
+    "C5": dict(circ="C5", k=None, dtype="c64", sps=1, cap=30, seeds=2, workload="sycamore53_m20_width30_subset"),
+    "C4": dict(circ="C4", k=None, dtype="c128", sps=1, cap=28, seeds=2, workload="gbs444_d4_width28_subset"),
 }
 
 
@@ -47,7 +48,7 @@ def parse():
     ap.add_argument("--slices-per-step", type=int, default=0)
     ap.add_argument("--trials", type=int, default=4096)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--plan-seeds", type=int, default=8, help="planner seeds searched (host only)")
+    ap.add_argument("--plan-seeds", type=int, default=0, help="planner seeds searched (host only; 0 = config default)")
     ap.add_argument("--width-cap", type=int, default=31)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -72,8 +73,9 @@ def make_plan(jet, cfg, args):
     k = cfg["k"]
     t0 = time.time()
     plan, info = plan_best(net, k if k is not None else -1, dtype=cfg["dtype"],
-                           seeds=tuple(range(args.seed, args.seed + args.plan_seeds)), trials=args.trials,
-                           width_cap=args.width_cap if k is None else 0)
+                           seeds=tuple(range(args.seed, args.seed + (args.plan_seeds or cfg.get("seeds", 8)))),
+                           trials=args.trials,
+                           width_cap=cfg.get("cap", args.width_cap) if k is None else 0)
     return circ, bits, net, plan, time.time() - t0
 
 

@@ -161,7 +161,8 @@ jt_status jt_exec_create(const jt_plan* plan, jt_dtype dtype, int32_t device, vo
 /* Contract slices [slice_begin, slice_end) in canonical order with the prefix cache,
    adding sum s_sigma into d_acc (device complex128, 2 doubles) in order -- async on the
    stream.  If h_slice_vals is non-NULL the call synchronises the stream and writes
-   (end-begin) complex128 values s_sigma there.  The cache persists across calls. */
+   (end-begin) complex128 values s_sigma there (at most min(N_sl, 2^20) per call, else
+   error 2).  The cache persists across calls. */
 jt_status jt_exec_contract(jt_exec* ex, int64_t slice_begin, int64_t slice_end, double* d_acc,
                            double* h_slice_vals);
 /* Same with the prefix cache disabled: every node is recomputed for every slice (E-flsl). */

@@ -64,6 +64,7 @@ struct Layout {
   std::vector<int64_t> node_off;      // byte offset of every node output (leaves: leaf_off)
   int64_t leaf_bytes = 0, inter_bytes = 0, scratch_bytes = 0;
   int64_t inter_base = 0, scratch_base = 0, vals_base = 0, acc_base = 0, state_base = 0, total = 0;
+  int64_t vals_cap = 1;  // slice-value ring (per call, indexed from the call's first slice)
 };
 
 using GettFn = void (*)(GettArgs);
@@ -534,7 +535,9 @@ Layout compile(const jt_plan& plan, int esize) {
   }
   L.scratch_bytes = scratch;
   L.vals_base = align_up(L.scratch_base + L.scratch_bytes);
-  L.acc_base = align_up(L.vals_base + plan.n_sl * 16);
+  L.vals_cap = 1;
+  while (L.vals_cap < plan.n_sl && L.vals_cap < (int64_t(1) << 20)) L.vals_cap <<= 1;
+  L.acc_base = align_up(L.vals_base + L.vals_cap * 16);
   L.state_base = align_up(L.acc_base + 16);
   L.total = align_up(L.state_base + (int64_t)sizeof(SliceState));
   return L;
@@ -743,10 +746,10 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
     const GettArgs& g = en.args;
     std::fprintf(f, "%s{\"v\": %lld, \"maxpos\": %d, \"flop\": %.17g, \"bytes\": %.17g, \"n_out\": %lld, "
                  "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
-                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d}",
+                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld}",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
                  g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind, en.tc.tm,
-                 en.tc.K, en.tc.n_outer);
+                 en.tc.K, en.tc.n_outer, (long long)L.node_off[en.v]);
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
@@ -937,7 +940,8 @@ void contract_range(jt_exec* ex, int64_t b, int64_t e, double* d_acc, bool reuse
     ex->graph_acc = d_acc;
   }
   if (e > b) {
-    set_slice_kernel<<<1, 32, 0, ex->stream>>>(reinterpret_cast<SliceState*>(ex->ws + ex->L.state_base), b - 1);
+    set_slice_kernel<<<1, 32, 0, ex->stream>>>(reinterpret_cast<SliceState*>(ex->ws + ex->L.state_base), b - 1, b,
+                                               ex->L.vals_cap - 1);
     ex->stats.kernel_launches++;
   }
   for (int64_t s = b; s < e; ++s) {
@@ -982,6 +986,8 @@ void contract_range(jt_exec* ex, int64_t b, int64_t e, double* d_acc, bool reuse
 void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_vals, bool reuse) {
   if (b < 0 || e > ex->n_sl || b > e) fail(JT_EUSAGE, "exec: slice range out of bounds");
   if (!d_acc) fail(JT_EUSAGE, "exec: null accumulator");
+  if (h_vals && e - b > ex->L.vals_cap)
+    fail(JT_EUSAGE, "exec: at most " + std::to_string(ex->L.vals_cap) + " slice values per call");
   JT_CUDA(cudaSetDevice(ex->device));
   ex->ev_used = 0;
   ex->ev_work.clear();
@@ -1006,8 +1012,7 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
     }
   }
   if (h_vals && e > b) {
-    JT_CUDA(cudaMemcpyAsync(h_vals, ex->ws + ex->L.vals_base + b * 16, (e - b) * 16, cudaMemcpyDeviceToHost,
-                            ex->stream));
+    JT_CUDA(cudaMemcpyAsync(h_vals, ex->ws + ex->L.vals_base, (e - b) * 16, cudaMemcpyDeviceToHost, ex->stream));
     JT_CUDA(cudaStreamSynchronize(ex->stream));
   }
 }

@@ -302,11 +302,17 @@ __global__ void reduce_splits_kernel(const typename V2<R>::t* __restrict__ P, ty
 // Device slice state: the current slice index and its digits (loop order, pos 0 outermost).
 struct SliceState {
   int64_t s;
+  int64_t base;      // first slice of the current jt_exec_contract call
+  int64_t vals_mask; // slice-value ring size - 1 (power of two)
   int32_t digits[64];
 };
 
-__global__ void set_slice_kernel(SliceState* st, int64_t s) {
-  if (threadIdx.x == 0) st->s = s;
+__global__ void set_slice_kernel(SliceState* st, int64_t s, int64_t base, int64_t vals_mask) {
+  if (threadIdx.x == 0) {
+    st->s = s;
+    st->base = base;
+    st->vals_mask = vals_mask;
+  }
 }
 
 // s += 1 and its mixed-radix digits (every sliced label has dimension d)
@@ -328,7 +334,7 @@ __global__ void accumulate_kernel(const typename V2<R>::t* __restrict__ root, do
     const double re = (double)root[0].x, im = (double)root[0].y;
     acc[0] += re;
     acc[1] += im;
-    slicevals[st->s] = make_double2(re, im);
+    slicevals[(st->s - st->base) & st->vals_mask] = make_double2(re, im);
   }
 }
 

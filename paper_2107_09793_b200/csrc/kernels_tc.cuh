@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     int bytes_of[PER];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      const int e = ptid + i * 128;
+      const int e = ptid + i * 256;
       bytes_of[i] = ts[0][e & 63] ^ ts[1][e >> 6];
     }
     const int S = p.xstages;
