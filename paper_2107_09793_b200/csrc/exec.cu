@@ -73,8 +73,8 @@ using TcFn = void (*)(TcArgs);
 TcFn pick_tc(int tkc) {
   switch (tkc) {
     case 2: return gett_tc_kernel<2>;
-    case 3: return gett_tc_kernel<4>;
-    case 4: return gett_tc_kernel<8>;
+    case 3: return gett_tc_kernel<3>;
+    case 4: return gett_tc_kernel<4>;
   }
   fail(JT_EINTERNAL, "no tc instance");
 }
@@ -100,8 +100,8 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-    const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<4>),
-                          reinterpret_cast<const void*>(gett_tc_kernel<8>)};
+    const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<3>),
+                          reinterpret_cast<const void*>(gett_tc_kernel<4>)};
     for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, false>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -140,14 +140,17 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   const int tkc = swz ? 4 : kt;
   const int n_kc = 1 << (kt - tkc);
   const int Kpc = 2 << tkc, Np = 2 << tm;
-  const int xbuf = 128 * Kpc * 4, yplane = Np * Kpc * 4;
-  int xstages = 3;
-  int64_t smem = 2LL * xstages * xbuf + 2LL * n_kc * yplane + 1024;
-  if (smem > 220 * 1024) {
-    xstages = 2;
-    smem = 2LL * xstages * xbuf + 2LL * n_kc * yplane + 1024;
-  }
-  if (smem > 220 * 1024) return false;
+  const int yplane = Np * Kpc * 4;
+  // TMEM: accumulators (2 when they fit beside >= 2 X stages) + X stages of 2*Kpc columns
+  int acc_bufs = (2 * Np + 2 * 2 * Kpc <= 512) ? 2 : 1;
+  int xstages = std::min(4, (512 - acc_bufs * Np) / (2 * Kpc));
+  if (xstages < 2) return false;
+  const int rbytes = 128 * (8 << tkc);
+  const int64_t ybytes = 2LL * n_kc * yplane;
+  const int64_t budget = 220 * 1024 - 1024 - ybytes;
+  const int rstages = (int)std::min<int64_t>(6, budget / rbytes);
+  if (rstages < 2) return false;
+  const int64_t smem = ybytes + (int64_t)rstages * rbytes + 1024;
   std::sort(M.begin(), M.end());
   std::sort(N.begin(), N.end());
   std::sort(K.begin(), K.end());
@@ -165,21 +168,22 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   t.Np = Np;
   t.Kpc = Kpc;
   t.sbo_x = t.sbo_y = swz ? 1024 : (Kpc / 4) * 128;
-  t.xbuf = xbuf;
+  t.xbuf = 0;
   t.yplane = yplane;
   t.xstages = xstages;
+  t.rstages = rstages;
+  t.rbytes = rbytes;
+  t.acc_bufs = acc_bufs;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t cols = 32;
-  while ((int)cols < 2 * Np) cols <<= 1;
+  while ((int)cols < acc_bufs * Np + xstages * 2 * Kpc) cols <<= 1;
   t.tmem_cols = cols;
-  // chunk-tile bits in B-stride order; byte offsets XOR-combine (SWIZZLE_128B folds row bits
-  // 0-2 onto the 16-B chunk index)
+  // chunk-tile bits in B-stride order with their byte offsets in the raw landing stage:
+  // row n, complex k at n*rb + ((k>>1) ^ (n & (chunks-1)))*16 + (k&1)*8 (XOR-combinable)
+  const int rb = 8 << tkc, lg_chunks = tkc - 1;
   std::vector<std::pair<int64_t, int32_t>> tb;
-  for (int i = 0; i < 7; ++i) {
-    int32_t off = swz ? (i < 3 ? (144 << i) : (1024 << (i - 3))) : (i < 3 ? (16 << i) : (t.sbo_x << (i - 3)));
-    tb.push_back({sb[tN[i]], off});
-  }
-  for (int i = 0; i < tkc; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : ((swz ? 16 : 128) << (i - 1))});
+  for (int i = 0; i < 7; ++i) tb.push_back({sb[tN[i]], (rb << i) ^ (i < lg_chunks ? (16 << i) : 0)});
+  for (int i = 0; i < tkc; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : (16 << (i - 1))});
   std::sort(tb.begin(), tb.end());
   for (size_t j = 0; j < tb.size(); ++j) {
     t.gX[j] = tb[j].first;

@@ -39,11 +39,14 @@ struct TcArgs {
   int32_t xbuf, yplane;                        // bytes of one X buffer / one Y chunk plane (hi or lo)
   uint32_t idesc;                              // kind::tf32, M=128, N=Np, F32 accumulate, K-major
   uint32_t tmem_cols;                          // 2 accumulators of Np columns
-  int32_t xstages;                             // X stages (2 or 3): cp.async runs xstages-1 items ahead
+  int32_t xstages;                             // TMEM X stages (hi|lo, 2*Kpc columns each)
+  int32_t rstages;                             // raw shared landing stages (cp.async depth rstages-1)
+  int32_t rbytes;                              // bytes of one raw stage (128 rows x 8*2^tkc)
+  int32_t acc_bufs;                            // TMEM accumulators (2: epilogue overlaps next tile)
   int64_t o_sB[kMaxOuter];                     // outer (row) bit j of B: stride
   int64_t o_kB[4];                             // chunk-index bit j of B: stride
   int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
-  int32_t sX[kTcMaxTile];                      //   ... and its byte offset in the X buffer (XOR-combined)
+  int32_t sX[kTcMaxTile];                      //   ... and its byte offset in the raw stage (XOR-combined)
   int64_t aM[8], aK[8];                        // A strides of its M bits / K bits
   SliceView sv;
 };
@@ -63,6 +66,39 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)layout << 61;
   return d;
 }
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const float (&v)[N]);
+template <>
+__device__ __forceinline__ void tmem_st<4>(uint32_t taddr, const float (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_st<8>(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_st<16>(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -122,25 +158,32 @@ __device__ __forceinline__ int tc_off(int r, int kk, int sbo, int swz) {
   return (r & 7) * 16 + (r >> 3) * sbo + (kk >> 2) * 128 + (kk & 3) * 4;
 }
 
-// Warp-specialised K3.  Warps 0-3: epilogue (TMEM lane quarter w -> 256-B coalesced stores);
-// warps 4-11: producers (B chunk tile -> shared stage by cp.async, lo split in place); warp 12:
-// MMA issuer (one elected thread).  Two X stages and two TMEM accumulators, so the loads of
-// item i+1, the MMAs of item i and the epilogue of the previous tile overlap.  Y (the expanded
-// small operand) is built once and stays resident for every K chunk.
-// PER = B-tile elements per producer thread = 2^(7+tkc) / 256.
-template <int PER>
+// Warp-specialised K3 with the streamed operand in tensor memory.
+//   warps 0-3  epilogue: TMEM accumulator -> registers -> 256-B coalesced global stores
+//   warps 4-11 producers: cp.async gathers each item's B rows into a raw shared stage
+//              (rstages-1 items in flight, no registers held); after a producer barrier each
+//              thread takes one row (its TMEM lane) and half of the K chunk, splits it into
+//              hi/lo TF32 and writes both into a TMEM X stage with tcgen05.st
+//   warp 12    MMA issuer: tcgen05.mma kind::tf32 with A = X from TMEM ([a_tmem], the "TS" form)
+//              and B = Y (expanded small operand, resident in shared memory), 3xTF32
+// Barriers: xfull/xempty per TMEM X stage, tfull/tempty per accumulator.
+// TKC = K bits per chunk (row of the X stage = 2*2^TKC TF32 = hi or lo).
+template <int TKC>
 __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
+  constexpr int PER = (128 << TKC) / 256;  // B elements each producer thread copies per item
+  constexpr int NCOL = 1 << TKC;           // fp32 columns (of hi or lo) each producer thread writes
+  constexpr int KPC = 2 << TKC;            // TF32 columns of one X row (hi or lo)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
-  __shared__ __align__(8) uint64_t full[3], empty[3], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // 1024-B aligned carve: X stage s = [hi | lo], then Y planes [hi c=0..n_kc-1 | lo ...]
+  // 1024-B aligned carve: Y planes [hi c=0..n_kc-1 | lo ...], then the raw stages
   unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  unsigned char* X = base;
-  unsigned char* Yhi = X + 2 * p.xstages * p.xbuf;
+  unsigned char* Yhi = base;
   unsigned char* Ylo = Yhi + p.n_kc * p.yplane;
+  unsigned char* R = Ylo + p.n_kc * p.yplane;
   for (int i = tid; i < 64; i += blockDim.x) {
     for (int h = 0; h < 2; ++h) {
       int64_t g = 0;
@@ -161,9 +204,9 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) {
-      tc::mbar_init(&full[i], 256);
-      tc::mbar_init(&empty[i], 1);
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&xfull[i], 256);
+      tc::mbar_init(&xempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
@@ -198,95 +241,103 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_sh;
+  const uint32_t xcol0 = (uint32_t)(p.acc_bufs * p.Np);  // first TMEM column of the X stages
   const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles * p.n_kc;
   auto tile_of = [&](int64_t it) { return (int64_t)blockIdx.x + (it / p.n_kc) * gridDim.x; };
   const uint32_t layout = p.swz ? 2u : 0u;
   const uint32_t lbo = p.swz ? 16u : 128u;
-  const uint32_t kstep = p.swz ? 32u : 256u;  // descriptor advance per 8-TF32 K step
+  const uint32_t kstep = p.swz ? 32u : 256u;  // Y descriptor advance per 8-TF32 K step
 
   if (warp >= 4 && warp < 12) {
     // ===================== producers =====================
-    // cp.async (no registers, commit groups instead of scoreboards) lands each item's B data
-    // straight into its X stage at the operand-layout position, XSTAGES-1 items ahead; the
-    // thread then splits the elements it copied in place into hi (X_hi) and lo (X_lo).
     const int ptid = tid - 128;  // 0..255
     const int64_t boff = slice_off(p.sv, false);
-    int bytes_of[PER];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int e = ptid + i * 256;
-      bytes_of[i] = ts[0][e & 63] ^ ts[1][e >> 6];
-    }
-    const int S = p.xstages;
-    auto issue = [&](int64_t it) {
-      const int s = (int)(it % S);
-      const uint32_t ph = (uint32_t)((it / S) & 1);
-      tc::mbar_wait(&empty[s], ph ^ 1);  // stage free (first use passes)
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int row = quarter * 32 + lane;  // this thread's TMEM lane (row n of the tile)
+    const int RS = p.rstages, XS = p.xstages;
+    // raw row layout: 16-B chunk c of row n lives at chunk c ^ (n & (chunks-1))
+    const int rb = 8 << TKC;            // raw bytes per row
+    const int chunks = rb >> 4;
+    auto copy = [&](int64_t it) {
       const int64_t t = tile_of(it);
       const int c = (int)(it % p.n_kc);
       int64_t src = boff;
       for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) src += p.o_sB[j];
       for (int j = 0; j < p.K - p.tkc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
-      unsigned char* xhi = X + s * 2 * p.xbuf;
+      unsigned char* raw = R + (int)(it % RS) * p.rbytes;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int e = ptid + i * 256;
-        cp_async8(xhi + bytes_of[i], p.B + src + tg[0][e & 63] + tg[1][e >> 6]);
+        cp_async8(raw + (ts[0][e & 63] ^ ts[1][e >> 6]), p.B + src + tg[0][e & 63] + tg[1][e >> 6]);
       }
     };
-    const int64_t depth = S - 1;
-    for (int64_t q = 0; q < depth; ++q) {
-      if (q < items) issue(q);
-      cp_async_commit();  // (possibly empty) group per slot keeps the group arithmetic uniform
+    for (int q = 0; q < RS - 1; ++q) {
+      if (q < items) copy(q);
+      cp_async_commit();
     }
     for (int64_t it = 0; it < items; ++it) {
-      // groups committed so far: depth + it; item it's group is the oldest of the last depth
-      if (S == 3) cp_async_wait<1>();
-      else cp_async_wait<0>();
-      const int s = (int)(it % S);
-      unsigned char* xhi = X + s * 2 * p.xbuf;
-      unsigned char* xlo = xhi + p.xbuf;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const float2 v = *reinterpret_cast<const float2*>(xhi + bytes_of[i]);
-        const float hx = tc::tf32_trunc(v.x), hy = tc::tf32_trunc(v.y);
-        *reinterpret_cast<float2*>(xhi + bytes_of[i]) = make_float2(hx, hy);
-        *reinterpret_cast<float2*>(xlo + bytes_of[i]) = make_float2(v.x - hx, v.y - hy);
+      // own copies of item it have landed (RS-1+it groups committed, RS-2 may stay pending)
+      switch (RS) {
+        case 2: cp_async_wait<0>(); break;
+        case 3: cp_async_wait<1>(); break;
+        case 4: cp_async_wait<2>(); break;
+        case 5: cp_async_wait<3>(); break;
+        default: cp_async_wait<4>(); break;
       }
-      tc::fence_proxy_async();
-      tc::mbar_arrive(&full[s]);
-      if (it + depth < items) issue(it + depth);
+      tc::bar_sync(1, 256);  // all producers' copies of item it landed; raw stage of it-1 is free
+      if (it + RS - 1 < items) copy(it + RS - 1);
       cp_async_commit();
+      const int xs = (int)(it % XS);
+      tc::mbar_wait(&xempty[xs], (uint32_t)(((it / XS) & 1) ^ 1));  // TMEM X stage free
+      tc::fence_after();
+      const unsigned char* raw = R + (int)(it % RS) * p.rbytes + row * rb;
+      float hi[NCOL], lo[NCOL];
+#pragma unroll
+      for (int j = 0; j < NCOL / 4; ++j) {
+        const int cc = half * (NCOL / 4) + j;  // 16-B chunk of this row = 2 complex
+        const float4 v = *reinterpret_cast<const float4*>(raw + ((cc ^ (row & (chunks - 1))) << 4));
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hi[4 * j + q] = tc::tf32_trunc(x[q]);
+          lo[4 * j + q] = x[q] - hi[4 * j + q];
+        }
+      }
+      const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+      const uint32_t col = xcol0 + (uint32_t)(xs * 2 * KPC + half * NCOL);
+      tc::tmem_st<NCOL>(lane_addr + col, hi);
+      tc::tmem_st<NCOL>(lane_addr + col + KPC, lo);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&xfull[xs]);
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
     const bool leader = lane == 0;
     int64_t tt = 0;
-    const int S = p.xstages;
+    const int XS = p.xstages;
     for (int64_t it = 0; it < items; ++it) {
-      const int s = (int)(it % S);
-      const uint32_t ph = (uint32_t)((it / S) & 1);
+      const int xs = (int)(it % XS);
       const int c = (int)(it % p.n_kc);
-      const int b = (int)(tt & 1);
-      const uint32_t tph = (uint32_t)((tt >> 1) & 1);
+      const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
+      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
       if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
-      tc::mbar_wait(&full[s], ph);
+      tc::mbar_wait(&xfull[xs], (uint32_t)((it / XS) & 1));
       tc::fence_after();
       if (leader) {
         const uint32_t d = tmem + (uint32_t)(b * p.Np);
-        const uint32_t xh = tc::smem_u32(X + s * 2 * p.xbuf), xl = xh + p.xbuf;
+        const uint32_t xh = tmem + xcol0 + (uint32_t)(xs * 2 * KPC), xl = xh + KPC;
         const uint32_t yh = tc::smem_u32(Yhi + c * p.yplane), yl = tc::smem_u32(Ylo + c * p.yplane);
-        const int ksteps = p.Kpc / 8;
-        for (int ks = 0; ks < ksteps; ++ks) {
-          const uint32_t o = ks * kstep;
-          const uint64_t dxh = tc::sdesc(xh + o, lbo, p.sbo_x, layout), dxl = tc::sdesc(xl + o, lbo, p.sbo_x, layout);
-          const uint64_t dyh = tc::sdesc(yh + o, lbo, p.sbo_y, layout), dyl = tc::sdesc(yl + o, lbo, p.sbo_y, layout);
-          tc::mma_tf32(d, dxh, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
-          tc::mma_tf32(d, dxh, dyl, p.idesc, 1u);
-          tc::mma_tf32(d, dxl, dyh, p.idesc, 1u);
+#pragma unroll
+        for (int ks = 0; ks < KPC / 8; ++ks) {
+          const uint64_t dyh = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
+          const uint64_t dyl = tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout);
+          tc::mma_tf32_ts(d, xh + ks * 8, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_tf32_ts(d, xh + ks * 8, dyl, p.idesc, 1u);
+          tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
         }
-        tc::mma_commit(&empty[s]);                      // stage s free once these MMAs finish
+        tc::mma_commit(&xempty[xs]);                     // TMEM X stage free once these finish
         if (c == p.n_kc - 1) tc::mma_commit(&tfull[b]);  // tile accumulated
       }
       __syncwarp();
@@ -297,8 +348,8 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     const int row = warp * 32 + lane;
     const int nm = 1 << p.tm;
     for (int64_t tt = 0; tt < my_tiles; ++tt) {
-      const int b = (int)(tt & 1);
-      const uint32_t tph = (uint32_t)((tt >> 1) & 1);
+      const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
+      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
       tc::mbar_wait(&tfull[b], tph);
       tc::fence_after();
       const int64_t t = (int64_t)blockIdx.x + tt * gridDim.x;
