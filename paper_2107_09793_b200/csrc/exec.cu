@@ -716,6 +716,7 @@ struct jt_exec {
   std::vector<std::pair<double, double>> ev_work;        // (bytes, flop) of each timed launch
   std::vector<int> ev_kind;                              // 0 = K2, 1 = K3
   bool use_graphs = true;
+  bool pdl = true;  // programmatic dependent launch between the kernels of a slice
   std::vector<cudaGraphExec_t> graphs;   // per prefix-cache level j+1 (j = -1..k)
   std::vector<jt_exec_stats> graph_stats;
   double* graph_acc = nullptr;           // accumulator baked into the graphs
@@ -806,6 +807,8 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   {
     const char* e = std::getenv("JETB200_GRAPHS");
     ex->use_graphs = !(e && e[0] == '0') && stream != nullptr;  // no capture on the legacy stream
+    const char* q = std::getenv("JETB200_PDL");
+    ex->pdl = !(q && q[0] == '0');
   }
   const int32_t* dptr = reinterpret_cast<const int32_t*>(static_cast<char*>(d_ws) + ex->L.state_base +
                                                          offsetof(SliceState, digits));
@@ -855,6 +858,23 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   return ex;
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel may start while its
+// predecessor drains and synchronises through griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  JT_CUDA(cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...));
+}
+
 void ev_begin(jt_exec* ex) {
   if (!ex->profiling) return;
   if (ex->ev_used == ex->ev.size()) {
@@ -884,7 +904,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
-    pick_tc(t.tkc)<<<(unsigned)en.grid_x, 416, en.smem, ex->stream>>>(t);
+    launch_pdl(pick_tc(t.tkc), dim3((unsigned)en.grid_x), dim3(416), en.smem, ex->stream, ex->pdl, t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else {
@@ -896,14 +916,14 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     dim3 grid((unsigned)en.grid_x, (unsigned)g.splits);
     GettFn fn = pick_gett<R>(en.RM, en.RN);
     ev_begin(ex);
-    fn<<<grid, en.block, en.smem, ex->stream>>>(g);
+    launch_pdl(fn, grid, dim3(en.block), en.smem, ex->stream, ex->pdl, g);
     ev_end(ex, en);
     st.kernel_launches++;
     if (g.splits > 1) {
       int64_t n = en.n_out;
       int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-      reduce_splits_kernel<R><<<blocks, 256, 0, ex->stream>>>(reinterpret_cast<const C2*>(g.P),
-                                                               reinterpret_cast<C2*>(g.C), n, g.splits);
+      launch_pdl(reduce_splits_kernel<R>, dim3(blocks), dim3(256), 0, ex->stream, ex->pdl,
+                 reinterpret_cast<const C2*>(g.P), reinterpret_cast<C2*>(g.C), n, (int)g.splits);
       st.kernel_launches++;
     }
   }
@@ -918,13 +938,14 @@ template <typename R>
 void slice_sequence(jt_exec* ex, int j, double* d_acc) {
   using C2 = typename V2<R>::t;
   SliceState* state = reinterpret_cast<SliceState*>(ex->ws + ex->L.state_base);
-  advance_slice_kernel<<<1, 32, 0, ex->stream>>>(state, ex->k, ex->d);
+  launch_pdl(advance_slice_kernel, dim3(1), dim3(32), 0, ex->stream, ex->pdl, state, ex->k, ex->d);
   ex->cur_stats->kernel_launches++;
   for (ExecNode& en : ex->L.order)
     if (en.maxpos >= j) launch_node<R>(ex, en);
   const ExecNode& root = ex->L.order.back();
-  accumulate_kernel<R><<<1, 32, 0, ex->stream>>>(reinterpret_cast<const C2*>(ex->ws + root.out_off), d_acc,
-                                                 reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), state);
+  launch_pdl(accumulate_kernel<R>, dim3(1), dim3(32), 0, ex->stream, ex->pdl,
+             reinterpret_cast<const C2*>(ex->ws + root.out_off), d_acc,
+             reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), (const SliceState*)state);
   ex->cur_stats->kernel_launches++;
   ex->cur_stats->slices_done++;
 }

@@ -24,6 +24,13 @@
 
 namespace jt {
 
+// Programmatic dependent launch: every kernel of the slice sequence is launched with
+// programmatic stream serialisation, runs its parameter-only prologue, then waits for the
+// previous kernel's memory (griddepcontrol.wait) before touching the workspace, and lets the
+// next kernel start its own prologue (griddepcontrol.launch_dependents).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr int kMaxOuter = 48;
 constexpr int kMaxTile = 14;
 
@@ -159,6 +166,8 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
     posKB[kk] = swz<C2>(deposit(kk, p.pKB, p.tk));
   }
   __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
   const int split = blockIdx.y;
   const int64_t it0 = (int64_t)split * p.k_iters / p.splits;
   const int64_t it1 = (int64_t)(split + 1) * p.k_iters / p.splits;
@@ -288,6 +297,8 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
 template <typename R>
 __global__ void reduce_splits_kernel(const typename V2<R>::t* __restrict__ P, typename V2<R>::t* __restrict__ C,
                                      int64_t n, int splits) {
+  pdl_wait();
+  pdl_launch_dependents();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     typename V2<R>::t s = P[i];
     for (int k = 1; k < splits; ++k) {
@@ -308,6 +319,8 @@ struct SliceState {
 };
 
 __global__ void set_slice_kernel(SliceState* st, int64_t s, int64_t base, int64_t vals_mask) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (threadIdx.x == 0) {
     st->s = s;
     st->base = base;
@@ -317,6 +330,8 @@ __global__ void set_slice_kernel(SliceState* st, int64_t s, int64_t base, int64_
 
 // s += 1 and its mixed-radix digits (every sliced label has dimension d)
 __global__ void advance_slice_kernel(SliceState* st, int k, int d) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (threadIdx.x == 0) {
     int64_t s = st->s + 1;
     st->s = s;
@@ -330,6 +345,8 @@ __global__ void advance_slice_kernel(SliceState* st, int k, int d) {
 template <typename R>
 __global__ void accumulate_kernel(const typename V2<R>::t* __restrict__ root, double* __restrict__ acc,
                                   double2* __restrict__ slicevals, const SliceState* __restrict__ st) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const double re = (double)root[0].x, im = (double)root[0].y;
     acc[0] += re;

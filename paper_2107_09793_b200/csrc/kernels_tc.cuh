@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // the operands are written by the previous kernels of the sequence
+  pdl_launch_dependents();
   // ---- Y = expanded small operand (hi/lo) for every K chunk: row = 2m+s, col = 2k+t
   {
     const int nm = 1 << p.tm, nk = 1 << p.K, nkc = 1 << p.tkc;
