@@ -261,18 +261,26 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     // raw row layout: 16-B chunk c of row n lives at chunk c ^ (n & (chunks-1))
     const int rb = 8 << TKC;            // raw bytes per row
     const int chunks = rb >> 4;
+    // per-thread gather offsets are the same for every item: keep them in registers
+    int64_t goff[PER];
+    int32_t soff[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = ptid + i * 256;
+      goff[i] = tg[0][e & 63] + tg[1][e >> 6];
+      soff[i] = ts[0][e & 63] ^ ts[1][e >> 6];
+    }
+    const int lg_kc = p.K - p.tkc;  // n_kc = 2^lg_kc
     auto copy = [&](int64_t it) {
-      const int64_t t = tile_of(it);
-      const int c = (int)(it % p.n_kc);
+      const int64_t t = (int64_t)blockIdx.x + (it >> lg_kc) * gridDim.x;
+      const int c = (int)(it & ((1 << lg_kc) - 1));
       int64_t src = boff;
       for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) src += p.o_sB[j];
-      for (int j = 0; j < p.K - p.tkc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
+      for (int j = 0; j < lg_kc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
       unsigned char* raw = R + (int)(it % RS) * p.rbytes;
+      const float2* srcp = p.B + src;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int e = ptid + i * 256;
-        cp_async8(raw + (ts[0][e & 63] ^ ts[1][e >> 6]), p.B + src + tg[0][e & 63] + tg[1][e >> 6]);
-      }
+      for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], srcp + goff[i]);
     };
     for (int q = 0; q < RS - 1; ++q) {
       if (q < items) copy(q);
