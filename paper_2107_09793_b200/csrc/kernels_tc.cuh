@@ -274,8 +274,11 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     auto copy = [&](int64_t it) {
       const int64_t t = (int64_t)blockIdx.x + (it >> lg_kc) * gridDim.x;
       const int c = (int)(it & ((1 << lg_kc) - 1));
-      int64_t src = boff;
-      for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) src += p.o_sB[j];
+      // tile base offset: lane j contributes outer bit j, butterfly-summed over the warp
+      int64_t part = (lane < p.n_outer && ((t >> lane) & 1)) ? p.o_sB[lane] : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      int64_t src = boff + part;
       for (int j = 0; j < lg_kc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
       unsigned char* raw = R + (int)(it % RS) * p.rbytes;
       const float2* srcp = p.B + src;
