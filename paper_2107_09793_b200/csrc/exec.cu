@@ -18,6 +18,7 @@
 #include "jt_internal.hpp"
 #include "kernels.cuh"
 #include "kernels_tc.cuh"
+#include "kernels_tcg.cuh"
 
 #define JT_CUDA(x)                                                                        \
   do {                                                                                    \
@@ -40,8 +41,10 @@ struct View {
 };
 
 struct ExecNode {
-  int kind = 0;  // 0: K2 CUDA-core GETT, 1: K3 tcgen05 3xTF32 (c64)
+  int kind = 0;  // 0: K2 CUDA-core GETT, 1: K3 tcgen05 (resident A), 2: K3g tcgen05 (streamed A)
   TcArgs tc{};
+  TcgArgs tcg{};
+  std::vector<int64_t> tcgA_m, tcgA_k, tcgB_oN, tcgA_oM;  // K3g host strides (emulator)
   std::vector<int64_t> tcB_n, tcB_k;  // K3: B strides of the 7 row bits and the K bits (emulator)
   int64_t v = -1;
   int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
@@ -69,6 +72,16 @@ struct Layout {
 
 using GettFn = void (*)(GettArgs);
 using TcFn = void (*)(TcArgs);
+
+using TcgFn = void (*)(TcgArgs);
+TcgFn pick_tcg(int tmt) {
+  switch (tmt) {
+    case 4: return gett_tcg_kernel<4>;
+    case 5: return gett_tcg_kernel<5>;
+    case 6: return gett_tcg_kernel<6>;
+  }
+  fail(JT_EINTERNAL, "no tcg instance");
+}
 
 TcFn pick_tc(int tkc) {
   switch (tkc) {
@@ -103,6 +116,9 @@ void set_smem_attrs() {
     const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<3>),
                           reinterpret_cast<const void*>(gett_tc_kernel<4>)};
     for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
+    const void* tcgs[3] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
+                           reinterpret_cast<const void*>(gett_tcg_kernel<6>)};
+    for (const void* f : tcgs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, false>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, true>),
@@ -211,6 +227,101 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (auto b : tN) { out.bits.push_back({b, st}); st <<= 1; }
   for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
   for (auto b : oN) { out.bits.push_back({b, st}); st <<= 1; }
+  return true;
+}
+
+// K3g eligibility and descriptor (c64): both operands streamed; output tiles of 128 rows of B's
+// free bits x 2^tmt (16..64) complex columns of A's free bits; K in chunks of 16 complex.
+bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out) {
+  if (esize != 8) return false;
+  std::map<int64_t, int64_t> sa, sb;
+  for (auto& x : va.bits) sa[x.first] = x.second;
+  for (auto& x : vb.bits) sb[x.first] = x.second;
+  std::vector<std::pair<int64_t, int64_t>> M, N, K;
+  for (auto& x : va.bits) {
+    if (sb.count(x.first)) K.push_back({sb[x.first], x.first});
+    else M.push_back({x.second, x.first});
+  }
+  for (auto& x : vb.bits)
+    if (!sa.count(x.first)) N.push_back({x.second, x.first});
+  if ((int)M.size() < 4 || (int)N.size() < 7 || (int)K.size() < 4) return false;
+  const int tmt = std::min<int>((int)M.size(), 6);
+  const int MT = 1 << tmt, NP = 2 * MT;
+  std::sort(M.begin(), M.end());
+  std::sort(N.begin(), N.end());
+  // K chunk: the 2 lowest-A-stride K bits, then the lowest-B-stride ones, to 4 bits
+  std::vector<std::pair<int64_t, int64_t>> KA;
+  for (auto& k : K) KA.push_back({sa[k.second], k.second});
+  std::sort(KA.begin(), KA.end());
+  std::sort(K.begin(), K.end());
+  std::vector<int64_t> kc, ko;
+  for (int i = 0; i < 2; ++i) kc.push_back(KA[i].second);
+  for (auto& k : K)
+    if ((int)kc.size() < 4 && std::find(kc.begin(), kc.end(), k.second) == kc.end()) kc.push_back(k.second);
+  for (auto& k : K)
+    if (std::find(kc.begin(), kc.end(), k.second) == kc.end()) ko.push_back(k.second);
+  std::vector<int64_t> tN, oN, tM, oM;
+  for (size_t i = 0; i < N.size(); ++i) (i < 7 ? tN : oN).push_back(N[i].second);
+  for (size_t i = 0; i < M.size(); ++i) ((int)i < tmt ? tM : oM).push_back(M[i].second);
+  if (oN.size() + oM.size() > 31 || ko.size() > 32 || oN.size() > 32 || oM.size() > 32) return false;
+  const int64_t ybytes = 4LL * NP * 128;
+  const int rb_b = 128 * 128, rb_a = MT * 128;
+  const int rstages = (int)std::min<int64_t>(6, (220 * 1024 - 1024 - ybytes) / (rb_b + rb_a));
+  if (rstages < 2) return false;
+  TcgArgs& t = en.tcg;
+  std::memset(&t, 0, sizeof(t));
+  t.n_oN = (int)oN.size();
+  t.n_oM = (int)oM.size();
+  t.tmt = tmt;
+  t.lg_kc = (int)ko.size();
+  t.nXb = 11;
+  t.nAb = tmt + 4;
+  t.Np = NP;
+  t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  t.acc_bufs = 2;
+  t.tmem_cols = 512;
+  t.rstages = rstages;
+  t.rbytes_b = rb_b;
+  t.rbytes_a = rb_a;
+  for (int j = 0; j < t.n_oN; ++j) t.o_B[j] = sb[oN[j]];
+  for (int j = 0; j < t.n_oM; ++j) t.o_A[j] = sa[oM[j]];
+  for (int j = 0; j < t.lg_kc; ++j) {
+    t.k_B[j] = sb[ko[j]];
+    t.k_A[j] = sa[ko[j]];
+  }
+  auto raw_off_row = [](int i) { return (128 << i) ^ (i < 3 ? (16 << i) : 0); };
+  auto raw_off_k = [](int j) { return j == 0 ? 8 : (16 << (j - 1)); };
+  std::vector<std::pair<int64_t, int32_t>> bb, aa;
+  for (int i = 0; i < 7; ++i) bb.push_back({sb[tN[i]], raw_off_row(i)});
+  for (int j = 0; j < 4; ++j) bb.push_back({sb[kc[j]], raw_off_k(j)});
+  for (int i = 0; i < tmt; ++i) aa.push_back({sa[tM[i]], raw_off_row(i)});
+  for (int j = 0; j < 4; ++j) aa.push_back({sa[kc[j]], raw_off_k(j)});
+  std::sort(bb.begin(), bb.end());
+  std::sort(aa.begin(), aa.end());
+  for (size_t j = 0; j < bb.size(); ++j) { t.gB[j] = bb[j].first; t.sB[j] = bb[j].second; }
+  for (size_t j = 0; j < aa.size(); ++j) { t.gA[j] = aa[j].first; t.sA[j] = aa[j].second; }
+  t.n_tiles = int64_t(1) << (t.n_oN + t.n_oM);
+  // host copies for the emulator
+  en.tcB_n.clear(); en.tcB_k.clear(); en.tcgA_m.clear(); en.tcgA_k.clear(); en.tcgB_oN.clear(); en.tcgA_oM.clear();
+  for (int i = 0; i < 7; ++i) en.tcB_n.push_back(sb[tN[i]]);
+  for (auto b : kc) { en.tcB_k.push_back(sb[b]); en.tcgA_k.push_back(sa[b]); }
+  for (auto b : ko) { en.tcB_k.push_back(sb[b]); en.tcgA_k.push_back(sa[b]); }
+  for (auto b : tM) en.tcgA_m.push_back(sa[b]);
+  for (auto b : oN) en.tcgB_oN.push_back(sb[b]);
+  for (auto b : oM) en.tcgA_oM.push_back(sa[b]);
+  en.kind = 2;
+  en.smem = (size_t)(ybytes + (int64_t)rstages * (rb_b + rb_a) + 1024);
+  en.block = 416;
+  en.n_out = t.n_tiles << (7 + tmt);
+  en.grid_x = t.n_tiles;
+  en.args.splits = 1;
+  en.args.n_tiles = t.n_tiles;
+  out.bits.clear();
+  int64_t st = 1;
+  for (auto b : tN) { out.bits.push_back({b, st}); st <<= 1; }
+  for (auto b : tM) { out.bits.push_back({b, st}); st <<= 1; }
+  for (auto b : oN) { out.bits.push_back({b, st}); st <<= 1; }
+  for (auto b : oM) { out.bits.push_back({b, st}); st <<= 1; }
   return true;
 }
 
@@ -405,6 +516,8 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
 
 Layout compile(const jt_plan& plan, int esize) {
   const bool use_tc = tc_enabled();
+  const char* fg = std::getenv("JETB200_TCG_FORCE");  // tests: route K3-eligible nodes to K3g
+  const bool force_tcg = fg && fg[0] == '1';
   Layout L;
   L.esize = esize;
   const jt_network& net = plan.net;
@@ -481,7 +594,8 @@ Layout compile(const jt_plan& plan, int esize) {
     if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
     if (en.sliceA.size() > 4 || en.sliceB.size() > 4) fail(JT_EUSAGE, "exec: more than 4 sliced labels on one leaf");
     View tv;
-    if (use_tc && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
+    if (use_tc && !force_tcg && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
+    else if (use_tc && plan_tcg(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
     else views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
     en.maxpos = n.maxpos;
     en.flop = n.flop;
@@ -643,6 +757,33 @@ void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector
   }
 }
 
+void emulate_tcg(const TcgArgs& p, const ExecNode& en, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
+  const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
+  const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
+  float2* C = reinterpret_cast<float2*>(ws + off[2].first);
+  const int MT = 1 << p.tmt;
+  const int64_t nk = int64_t(1) << (int)en.tcB_k.size();
+  auto bits = [](int64_t v, const std::vector<int64_t>& st) {
+    int64_t o = 0;
+    for (size_t j = 0; j < st.size(); ++j) if ((v >> j) & 1) o += st[j];
+    return o;
+  };
+  for (int64_t t = 0; t < p.n_tiles; ++t) {
+    const int64_t bo = bits(t, en.tcgB_oN), ao = bits(t >> p.n_oN, en.tcgA_oM);
+    for (int n = 0; n < 128; ++n)
+      for (int m = 0; m < MT; ++m) {
+        double re = 0, im = 0;
+        for (int64_t k = 0; k < nk; ++k) {
+          const float2 a = A[ao + bits(m, en.tcgA_m) + bits(k, en.tcgA_k)];
+          const float2 b = B[bo + bits(n, en.tcB_n) + bits(k, en.tcB_k)];
+          re += (double)a.x * b.x - (double)a.y * b.y;
+          im += (double)a.x * b.y + (double)a.y * b.x;
+        }
+        C[(t << (7 + p.tmt)) + ((int64_t)m << 7) + n] = make_float2((float)re, (float)im);
+      }
+  }
+}
+
 template <typename R>
 void emulate_host(const jt_plan& plan, int esize, int64_t b, int64_t e, double* h_vals, bool reuse) {
   using C2 = typename V2<R>::t;
@@ -673,7 +814,8 @@ void emulate_host(const jt_plan& plan, int esize, int64_t b, int64_t e, double* 
       for (auto& sl : en.sliceB) offB += (int64_t)dig[sl.first] * sl.second;
       std::vector<std::pair<int64_t, int64_t>> offs = {{L.node_off[en.opA], offA}, {L.node_off[en.opB], offB},
                                                        {en.out_off, 0}, {en.part_off, 0}};
-      if (en.kind == 1) emulate_tc(en.tc, en, ws.data(), offs);
+      if (en.kind == 2) emulate_tcg(en.tcg, en, ws.data(), offs);
+      else if (en.kind == 1) emulate_tc(en.tc, en, ws.data(), offs);
       else emulate_gett<R>(en.args, ws.data(), en, offs);
     }
     const C2 r = *reinterpret_cast<const C2*>(ws.data() + L.order.back().out_off);
@@ -753,8 +895,9 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
                  "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
                  "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld}",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
-                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind, en.tc.tm,
-                 en.tc.K, en.tc.n_outer, (long long)L.node_off[en.v]);
+                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind,
+                 en.kind == 2 ? en.tcg.tmt : en.tc.tm, en.kind == 2 ? 4 + en.tcg.lg_kc : en.tc.K,
+                 en.kind == 2 ? en.tcg.n_oN + en.tcg.n_oM : en.tc.n_outer, (long long)L.node_off[en.v]);
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
@@ -786,6 +929,10 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   JT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
   for (ExecNode& en : L.order) {
     int nb = 1;
+    if (en.kind == 2) {
+      en.grid_x = std::min<int64_t>(en.tcg.n_tiles, n_sm);  // one CTA per SM (512 TMEM columns)
+      continue;
+    }
     if (en.kind == 1) {
       JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc)), 416,
                                                             en.smem));
@@ -821,6 +968,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     for (int i = 0; i < sv.nB; ++i) { sv.posB[i] = en.sliceB[i].first; sv.strB[i] = en.sliceB[i].second; }
     en.args.sv = sv;
     en.tc.sv = sv;
+    en.tcg.sv = sv;
   }
   ex->dtype = dt;
   ex->device = device;
@@ -898,7 +1046,16 @@ void launch_node(jt_exec* ex, ExecNode& en) {
   using C2 = typename V2<R>::t;
   const Layout& L = ex->L;
   jt_exec_stats& st = *ex->cur_stats;
-  if (en.kind == 1) {
+  if (en.kind == 2) {
+    TcgArgs& t = en.tcg;
+    t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]);
+    t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
+    t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
+    ev_begin(ex);
+    launch_pdl(pick_tcg(t.tmt), dim3((unsigned)en.grid_x), dim3(416), en.smem, ex->stream, ex->pdl, t);
+    ev_end(ex, en);
+    st.kernel_launches++;
+  } else if (en.kind == 1) {
     TcArgs& t = en.tc;
     t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]);
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
@@ -1028,7 +1185,7 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
       ex->stats.k2_timed_launches++;
       ex->stats.k2_timed_bytes += ex->ev_work[i].first;
       ex->stats.k2_timed_flop += ex->ev_work[i].second;
-      if (ex->ev_kind[i] == 1) {
+      if (ex->ev_kind[i] >= 1) {
         ex->stats.k3_time_ms += ms;
         ex->stats.k3_timed_launches++;
         ex->stats.k3_timed_bytes += ex->ev_work[i].first;

@@ -1,0 +1,279 @@
+// K3g: general complex64 contraction on tcgen05 -- both operands streamed.
+//
+// Same 4M / 3xTF32 formulation as K3 (kernels_tc.cuh), for contractions where the "small"
+// operand does not fit a resident tile: large GEMM-shaped nodes (e.g. Sycamore m=20:
+// M = N = 2^6 tiles, K = 2^12..2^17) that are tensor-bound rather than HBM-bound.
+//   output tile = 128 rows n (7 bits of B) x Mt = 2^tmt complex columns m (bits of A)
+//   K loop over chunks of 16 complex (4 bits); the remaining contracted bits index the chunks
+//   per item (tile, chunk): producers cp.async the B chunk (128 x 16) and the A chunk (Mt x 16)
+//   into raw shared rings, then split B into hi/lo TF32 in TMEM (the MMA's A operand) and expand
+//   A into the Y operand [[Re,-Im],[Im,Re]] hi/lo in shared memory (SWIZZLE_128B, K-major)
+//   MMA warp: 4 K steps x 3 (hi*hi, hi*lo, lo*hi) tcgen05.mma kind::tf32 per item
+//   epilogue warps: TMEM accumulator -> 256-B coalesced stores of the complex output tile
+#pragma once
+
+#include "kernels_tc.cuh"
+
+namespace jt {
+
+struct TcgArgs {
+  const float2* A;
+  const float2* B;
+  float2* C;                // layout [7 n bits][tmt m bits][outer N bits][outer M bits]
+  int64_t n_tiles;          // 2^(n_oN + n_oM)
+  int32_t n_oN, n_oM;       // outer bits of the tile index: N bits first (B strides), then M (A)
+  int32_t tmt, lg_kc;       // M tile bits; K chunk-index bits (n_kc = 2^lg_kc)
+  int32_t nXb, nAb;         // tile bits of a B chunk (7 + 4) and of an A chunk (tmt + 4)
+  int32_t Np;               // MMA N = 2 * 2^tmt
+  uint32_t idesc, tmem_cols;
+  int32_t rstages, rbytes_b, rbytes_a, acc_bufs;
+  int64_t o_B[32], o_A[32]; // outer N bit strides in B / outer M bit strides in A
+  int64_t k_B[32], k_A[32]; // chunk-index bit strides in B / in A
+  int64_t gB[12], gA[12];   // chunk-tile bits (stride order): global strides
+  int32_t sB[12], sA[12];   //   ... and raw byte offsets (XOR-combinable)
+  SliceView sv;
+};
+
+namespace tcg {
+// sum over the set bits j < n of v of stride[j], computed lane-parallel and butterfly-reduced
+__device__ __forceinline__ int64_t bits_sum(int64_t v, int n, const int64_t* stride, int lane) {
+  int64_t part = 0;
+  for (int j = lane; j < n; j += 32)
+    if ((v >> j) & 1) part += stride[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  return part;
+}
+}  // namespace tcg
+
+template <int TMT>
+__global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant__ TcgArgs p) {
+  constexpr int MT = 1 << TMT;       // complex columns of the tile
+  constexpr int NP = 2 * MT;         // MMA N
+  constexpr int PERB = 2048 / 256;   // B chunk elements per producer thread
+  constexpr int PERA = (MT * 16 + 255) / 256;
+  constexpr int PAIRS = (MT * 8 + 255) / 256;  // (m, k-pair) units of the Y expansion per thread
+  constexpr int KPC = 32;            // TF32 columns of one X row (16 complex)
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ int64_t tgb[2][64], tga[2][64];
+  __shared__ int32_t tsb[2][64], tsa[2][64];
+  __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[2], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* Y = base;                            // 2 stages x [hi plane | lo plane], NP x 128 B each
+  unsigned char* RB = Y + 2 * 2 * NP * 128;           // raw B ring
+  unsigned char* RA = RB + p.rstages * p.rbytes_b;    // raw A ring
+  for (int i = tid; i < 64; i += blockDim.x) {
+    for (int h = 0; h < 2; ++h) {
+      int64_t g = 0, ga = 0;
+      int32_t s = 0, sa = 0;
+      for (int b = 0; b < 6; ++b)
+        if ((i >> b) & 1) {
+          const int bi = 6 * h + b;
+          if (bi < p.nXb) { g += p.gB[bi]; s ^= p.sB[bi]; }
+          if (bi < p.nAb) { ga += p.gA[bi]; sa ^= p.sA[bi]; }
+        }
+      tgb[h][i] = g; tsb[h][i] = s;
+      tga[h][i] = ga; tsa[h][i] = sa;
+    }
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_base_sh)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&full[i], 256);
+      tc::mbar_init(&xempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&yempty[i], 1);
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t xcol0 = (uint32_t)(p.acc_bufs * NP);
+  const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t items = my_tiles << p.lg_kc;
+  const int64_t kc_mask = ((int64_t)1 << p.lg_kc) - 1;
+
+  if (warp >= 4 && warp < 12) {
+    // ===================== producers =====================
+    const int ptid = tid - 128;
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int row = quarter * 32 + lane;
+    const int RS = p.rstages;
+    const int64_t boff = slice_off(p.sv, false), aoff = slice_off(p.sv, true);
+    int64_t goffB[PERB], goffA[PERA];
+    int32_t soffB[PERB], soffA[PERA];
+#pragma unroll
+    for (int i = 0; i < PERB; ++i) {
+      const int e = ptid + i * 256;
+      goffB[i] = tgb[0][e & 63] + tgb[1][e >> 6];
+      soffB[i] = tsb[0][e & 63] ^ tsb[1][e >> 6];
+    }
+#pragma unroll
+    for (int i = 0; i < PERA; ++i) {
+      const int e = (ptid + i * 256) & (MT * 16 - 1);
+      goffA[i] = tga[0][e & 63] + tga[1][e >> 6];
+      soffA[i] = tsa[0][e & 63] ^ tsa[1][e >> 6];
+    }
+    auto copy = [&](int64_t it) {
+      const int64_t t = (int64_t)blockIdx.x + (it >> p.lg_kc) * gridDim.x;
+      const int64_t c = it & kc_mask;
+      const int64_t tb = tcg::bits_sum(t, p.n_oN, p.o_B, lane) + tcg::bits_sum(c, p.lg_kc, p.k_B, lane);
+      const int64_t ta = tcg::bits_sum(t >> p.n_oN, p.n_oM, p.o_A, lane) + tcg::bits_sum(c, p.lg_kc, p.k_A, lane);
+      unsigned char* rb = RB + (int)(it % RS) * p.rbytes_b;
+      unsigned char* ra = RA + (int)(it % RS) * p.rbytes_a;
+      const float2* sb = p.B + boff + tb;
+      const float2* sa = p.A + aoff + ta;
+#pragma unroll
+      for (int i = 0; i < PERB; ++i) cp_async8(rb + soffB[i], sb + goffB[i]);
+#pragma unroll
+      for (int i = 0; i < PERA; ++i)
+        if (ptid + i * 256 < MT * 16) cp_async8(ra + soffA[i], sa + goffA[i]);
+    };
+    for (int q = 0; q < RS - 1; ++q) {
+      if (q < items) copy(q);
+      cp_async_commit();
+    }
+    for (int64_t it = 0; it < items; ++it) {
+      switch (RS) {
+        case 2: cp_async_wait<0>(); break;
+        case 3: cp_async_wait<1>(); break;
+        case 4: cp_async_wait<2>(); break;
+        case 5: cp_async_wait<3>(); break;
+        default: cp_async_wait<4>(); break;
+      }
+      tc::bar_sync(1, 256);
+      if (it + RS - 1 < items) copy(it + RS - 1);
+      cp_async_commit();
+      const int xs = (int)(it & 3), ys = (int)(it & 1);
+      tc::mbar_wait(&xempty[xs], (uint32_t)(((it >> 2) & 1) ^ 1));
+      tc::mbar_wait(&yempty[ys], (uint32_t)(((it >> 1) & 1) ^ 1));
+      tc::fence_after();
+      // ---- X: this thread's row, half of the chunk -> hi/lo TF32 in TMEM
+      {
+        const unsigned char* raw = RB + (int)(it % RS) * p.rbytes_b + row * 128;
+        float hi[16], lo[16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int cc = half * 4 + j;
+          const float4 v = *reinterpret_cast<const float4*>(raw + ((cc ^ (row & 7)) << 4));
+          const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            hi[4 * j + q] = tc::tf32_trunc(x[q]);
+            lo[4 * j + q] = x[q] - hi[4 * j + q];
+          }
+        }
+        const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t col = xcol0 + (uint32_t)(xs * 2 * KPC + half * 16);
+        tc::tmem_st<16>(lane_addr + col, hi);
+        tc::tmem_st<16>(lane_addr + col + KPC, lo);
+      }
+      // ---- Y: expand the A chunk into [[Re,-Im],[Im,Re]] hi/lo (SWIZZLE_128B, K-major)
+      {
+        const unsigned char* raw = RA + (int)(it % RS) * p.rbytes_a;
+        unsigned char* yhi = Y + ys * 2 * NP * 128;
+        unsigned char* ylo = yhi + NP * 128;
+#pragma unroll
+        for (int q = 0; q < PAIRS; ++q) {
+          const int u = ptid + q * 256;
+          if (u < MT * 8) {
+            const int m = u >> 3, kp = u & 7;
+            const float4 a = *reinterpret_cast<const float4*>(raw + m * 128 + ((kp ^ (m & 7)) << 4));
+            const float r0[4] = {a.x, -a.y, a.z, -a.w};  // row 2m   (s = 0)
+            const float r1[4] = {a.y, a.x, a.w, a.z};    // row 2m+1 (s = 1)
+            float h0[4], l0[4], h1[4], l1[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+              h0[z] = tc::tf32_trunc(r0[z]);
+              l0[z] = r0[z] - h0[z];
+              h1[z] = tc::tf32_trunc(r1[z]);
+              l1[z] = r1[z] - h1[z];
+            }
+            const int ra0 = 2 * m, ra1 = 2 * m + 1;
+            const int b0 = (ra0 & 7) * 128 + (ra0 >> 3) * 1024 + ((kp ^ (ra0 & 7)) << 4);
+            const int b1 = (ra1 & 7) * 128 + (ra1 >> 3) * 1024 + ((kp ^ (ra1 & 7)) << 4);
+            *reinterpret_cast<float4*>(yhi + b0) = make_float4(h0[0], h0[1], h0[2], h0[3]);
+            *reinterpret_cast<float4*>(ylo + b0) = make_float4(l0[0], l0[1], l0[2], l0[3]);
+            *reinterpret_cast<float4*>(yhi + b1) = make_float4(h1[0], h1[1], h1[2], h1[3]);
+            *reinterpret_cast<float4*>(ylo + b1) = make_float4(l1[0], l1[1], l1[2], l1[3]);
+          }
+        }
+      }
+      tc::fence_proxy_async();
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&full[xs]);
+    }
+  } else if (warp == 12) {
+    // ===================== MMA issuer =====================
+    const bool leader = lane == 0;
+    int64_t tt = 0;
+    for (int64_t it = 0; it < items; ++it) {
+      const int xs = (int)(it & 3), ys = (int)(it & 1);
+      const int64_t c = it & kc_mask;
+      const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
+      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
+      if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);
+      tc::mbar_wait(&full[xs], (uint32_t)((it >> 2) & 1));
+      tc::fence_after();
+      if (leader) {
+        const uint32_t d = tmem + (uint32_t)(b * NP);
+        const uint32_t xh = tmem + xcol0 + (uint32_t)(xs * 2 * KPC), xl = xh + KPC;
+        const uint32_t yh = tc::smem_u32(Y + ys * 2 * NP * 128), yl = yh + NP * 128;
+#pragma unroll
+        for (int ks = 0; ks < KPC / 8; ++ks) {
+          const uint64_t dyh = tc::sdesc(yh + ks * 32, 16, 1024, 2), dyl = tc::sdesc(yl + ks * 32, 16, 1024, 2);
+          tc::mma_tf32_ts(d, xh + ks * 8, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_tf32_ts(d, xh + ks * 8, dyl, p.idesc, 1u);
+          tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
+        }
+        tc::mma_commit(&xempty[xs]);
+        tc::mma_commit(&yempty[ys]);
+        if (c == kc_mask) tc::mma_commit(&tfull[b]);
+      }
+      __syncwarp();
+      if (c == kc_mask) ++tt;
+    }
+  } else if (warp < 4) {
+    // ===================== epilogue =====================
+    const int row = warp * 32 + lane;
+    for (int64_t tt = 0; tt < my_tiles; ++tt) {
+      const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
+      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
+      tc::mbar_wait(&tfull[b], tph);
+      tc::fence_after();
+      const int64_t t = (int64_t)blockIdx.x + tt * gridDim.x;
+      float2* out = p.C + (t << (7 + TMT));
+#pragma unroll 1
+      for (int c0 = 0; c0 < NP; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * NP + c0), v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) out[row + ((int64_t)(c0 / 2 + j) << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&tempty[b]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+}
+
+}  // namespace jt

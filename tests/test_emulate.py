@@ -58,9 +58,9 @@ def test_describe_exec_layout(jet):
     assert d["total_bytes"] == plan.workspace_bytes("c64")
     for n in d["nodes"]:
         assert n["block"] % 32 == 0 and n["block"] <= (416 if n["kind"] == 1 else 256)
-        if n["kind"] == 1:   # K3: 128-row MMA tiles, all of A in the tile
+        if n["kind"] in (1, 2):   # K3 / K3g: 128-row MMA tiles
             assert n["n_out"] == 2 ** (7 + n["tc_tm"] + n["tc_outer"])
-            assert 3 <= n["tc_tm"] <= 7 and 2 <= n["tc_tk"] <= 8 and n["smem"] <= 220 * 1024
+            assert 3 <= n["tc_tm"] <= 7 and 2 <= n["tc_tk"] and n["smem"] <= 220 * 1024
         else:
             assert n["tm"] + n["tk"] <= 12 and n["tk"] + n["tn"] <= 12 and n["tm"] + n["tn"] <= 12
             assert n["n_out"] == 2 ** (n["tm"] + n["tn"] + n["n_outer"])
@@ -73,4 +73,17 @@ def test_emulated_k3_matches_oracle_c2_slices(jet):
     assert sum(n["kind"] for n in plan.describe_exec("c64")["nodes"]) > 0
     ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[5]))
     v = jet.debug_emulate_host(plan, 5, 6, "c64")
+    assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4
+
+
+def test_emulated_k3g_matches_oracle_c2_slice(jet, monkeypatch):
+    """K3g (both operands streamed) descriptors: force the K3-eligible C2 nodes onto K3g."""
+    monkeypatch.setenv("JETB200_TCG_FORCE", "1")
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6, bytes_weight=5.0)
+    kinds = [n["kind"] for n in plan.describe_exec("c64")["nodes"]]
+    assert kinds.count(2) > 0
+    ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[9]))
+    v = jet.debug_emulate_host(plan, 9, 10, "c64")
     assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4

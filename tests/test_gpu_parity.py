@@ -315,3 +315,20 @@ def test_c3_fsim_identity_closed_form_full_amplitude(jet):
     torch.cuda.synchronize()
     amp = complex(acc[0].item(), acc[1].item())
     assert rel(amp, want) < 1e-4
+
+
+def test_k3g_streamed_operands_parity(jet, c2_plan, monkeypatch):
+    """K3g (tcgen05 with both operands streamed, K in 16-complex chunks): force the C2 nodes
+    K3 would take onto K3g and compare 8 slices with the oracle."""
+    circ, bits, net, plan = c2_plan
+    monkeypatch.setenv("JETB200_TCG_FORCE", "1")
+    assert [n["kind"] for n in plan.describe_exec("c64")["nodes"]].count(2) >= 10
+    idx = list(range(0, 64, 8))
+    ref = contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=idx)
+    import torch
+
+    ex = jet.Exec(plan, "c64")
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    for i, r in zip(idx, ref):
+        v = ex.contract(i, i + 1, acc, slice_values=True)[0]
+        assert abs(v - r) <= 1e-4 * abs(r), (i, v, r)
