@@ -191,6 +191,42 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def tensor_peak_alg(dtype):
+    """Algorithmic complex-FLOP peak of the tensor path: TF32 = measured bf16 burst x 1/2 (the
+    guide's nominal TF32:BF16 ratio), divided by 3 for the 3xTF32 split (the 4M real expansion
+    does exactly the complex work: 4 real MACs = 8 real FLOP per complex MAC).  c128 runs on
+    CUDA-core FP64: nominal 37 TFLOP/s."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    bf16 = json.load(open(p)).get("bf16_tflops", 1590.0) if os.path.exists(p) else 1590.0
+    if dtype == "c128":
+        return 37.0, "nominal FP64 (B200 datasheet 37 TFLOP/s)"
+    return bf16 * 0.5 / 3.0, f"measured bf16 {bf16} x 0.5 (TF32) / 3 (3xTF32)"
+
+
+def roofline_entry(args, dom, gbs, tfs, dom_bytes, dom_n, dom_ms, peak, peak_kind, ms_max, prof_steps, kern, dtype):
+    tpeak, tkind = tensor_peak_alg(dtype)
+    fh = (gbs / peak) if gbs else None
+    ft = (tfs / tpeak) if tfs else None
+    bound = "tensor" if (ft or 0) > (fh or 0) else "hbm"
+    e = {
+        "bound": bound,
+        "achieved": tfs if bound == "tensor" else gbs,
+        "peak": tpeak if bound == "tensor" else peak,
+        "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+        "frac": ft if bound == "tensor" else fh,
+        "traffic": profile_traffic(args.config, dom),
+        "kernel": (f"{dom} ({'tcgen05 3xTF32 (K3/K3g)' if dom == 'K3' else 'CUDA-core GETT'}); achieved = algorithmic "
+                   f"{'complex FLOP' if bound == 'tensor' else 'bytes |A|+|B|+|C|'} per launch / CUDA-event launch time"),
+        "peak_kind": tkind if bound == "tensor" else peak_kind,
+        "other": {"GBps": gbs, "frac_hbm": fh, "TFLOPs_alg": tfs, "frac_tensor": ft, "tensor_peak_alg": tpeak},
+        "achieved_per_launch_bytes": dom_bytes / dom_n if dom_n else None,
+        "launches_profiled": dom_n,
+        "share_of_step": (dom_ms / (ms_max / args.steps * prof_steps)) if ms_max > 0 else None,
+        "kernels": kern,
+    }
+    return e
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -348,10 +384,15 @@ def run_ours(args, cfg):
     n3, n2 = pst["k3_timed_launches"], pst["k2_timed_launches"] - pst["k3_timed_launches"]
     dom = "K3" if t3 >= t2 else "K2"
     dom_ms, dom_bytes, dom_n = (t3, b3, n3) if dom == "K3" else (t2, b2, n2)
+    f3, f2 = pst["k3_timed_flop"], pst["k2_timed_flop"] - pst["k3_timed_flop"]
+    dom_flop = f3 if dom == "K3" else f2
     dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
+    dom_tfs = dom_flop / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
     kern_info = {
-        "K3_gett_tc_kernel": {"launches": n3, "ms": t3, "GBps": (b3 / (t3 / 1e3) / 1e9) if t3 > 0 else None},
-        "K2_gett_kernel": {"launches": n2, "ms": t2, "GBps": (b2 / (t2 / 1e3) / 1e9) if t2 > 0 else None},
+        "K3_tcgen05": {"launches": n3, "ms": t3, "GBps": (b3 / (t3 / 1e3) / 1e9) if t3 > 0 else None,
+                       "TFLOPs_alg": (f3 / (t3 / 1e3) / 1e12) if t3 > 0 else None},
+        "K2_cuda_core": {"launches": n2, "ms": t2, "GBps": (b2 / (t2 / 1e3) / 1e9) if t2 > 0 else None,
+                         "TFLOPs_alg": (f2 / (t2 / 1e3) / 1e12) if t2 > 0 else None},
     }
     prof_steps = max(1, min(args.steps, 2))
 
@@ -406,17 +447,8 @@ def run_ours(args, cfg):
             "amplitude_time_s_extrapolated": c["prefix"] / max(world, 1) / (flop_rate / max(world, 1)),
             "gpu_launches": int(tot_launch),
             "clocks": clk,
-            "roofline": {
-                "bound": "hbm", "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
-                "frac": (dom_gbs / peak) if dom_gbs else None,
-                "traffic": profile_traffic(args.config, dom),
-                "kernel": (f"{dom} ({'gett_tc_kernel, tcgen05 3xTF32' if dom == 'K3' else 'gett_kernel, CUDA cores'}), "
-                           "algorithmic bytes |A|+|B|+|C| per launch / CUDA-event launch time"),
-                "achieved_per_launch_bytes": dom_bytes / dom_n if dom_n else None,
-                "peak_kind": peak_kind, "launches_profiled": dom_n,
-                "share_of_step": (dom_ms / (ms_max / args.steps * prof_steps)) if ms_max > 0 else None,
-                "kernels": kern_info,
-            },
+            "roofline": roofline_entry(args, dom, dom_gbs, dom_tfs, dom_bytes, dom_n, dom_ms, peak, peak_kind,
+                                       ms_max, prof_steps, kern_info, cfg["dtype"]),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "algorithmic_gbs_step": tot_bytes / (ms_max / 1e3) / 1e9,

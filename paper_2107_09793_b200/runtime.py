@@ -87,7 +87,7 @@ def modeled_time(plan, dtype="c64", bw=MODEL_HBM_BPS, flops=None):
     t = 0.0
     for n in d["nodes"]:
         runs = dq ** (n["maxpos"] + 1)
-        f = MODEL_FLOPS_TC if n.get("kind", 0) == 1 else flops
+        f = MODEL_FLOPS_TC if n.get("kind", 0) >= 1 else flops
         t += runs * (max(n["bytes"] / bw, n["flop"] / f) + 3e-6)   # + launch gap
     return t, d["total_bytes"]
 
