@@ -193,6 +193,13 @@ jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, doub
 jt_status jt_debug_emulate_host(const jt_plan* plan, jt_dtype dtype, int64_t b, int64_t e, double* h_vals,
                                 int32_t reuse);
 
+/* DEBUG ONLY: time `reps` back-to-back launches of the node at execution-order index
+   `order_index` (CUDA events on the exec stream; inputs as currently in the workspace).
+   Returns the mean ms per launch, the node's algorithmic bytes and FLOP, and its kernel kind
+   (0 K2, 1 K3, 2 K3g).  For kernel tuning on real plan shapes. */
+jt_status jt_debug_time_node(jt_exec* ex, int64_t order_index, int32_t reps, double* ms, double* bytes,
+                             double* flop, int32_t* kind);
+
 /* ---- K1 index permutation ("two (partial) tensor transposes") ------- */
 /* dst[pi(i)] = src[i] for a tensor of 2^n_bits elements of the dtype, where the address
    bit b of src moves to bit perm[b] of dst (perm is a permutation of 0..n_bits-1).

@@ -18,6 +18,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
 void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_vals, bool reuse);
 void exec_contract_host(jt_exec* ex, int64_t b, int64_t e, double* h_acc);
 void exec_invalidate(jt_exec* ex);
+void debug_time_node(jt_exec* ex, int64_t idx, int reps, double* ms, double* bytes, double* flop, int* kind);
 void exec_set_profiling(jt_exec* ex, bool on);
 void upload_leaves(jt_exec* ex);
 void exec_stats(const jt_exec* ex, jt_exec_stats* out);
@@ -237,6 +238,14 @@ jt_status jt_debug_emulate_host(const jt_plan* plan, jt_dtype dtype, int64_t b, 
   return guarded([&] {
     NEED(plan && (h_vals || b == e), "jt_debug_emulate_host");
     debug_emulate_host(*plan, dtype, b, e, h_vals, reuse != 0);
+  });
+}
+
+jt_status jt_debug_time_node(jt_exec* ex, int64_t order_index, int32_t reps, double* ms, double* bytes,
+                             double* flop, int32_t* kind) {
+  return guarded([&] {
+    NEED(ex && ms && bytes && flop && kind, "jt_debug_time_node");
+    debug_time_node(ex, order_index, reps, ms, bytes, flop, kind);
   });
 }
 

@@ -92,6 +92,7 @@ _sig("jt_exec_stats_reset", c_i32, [c_vp])
 _sig("jt_exec_invalidate", c_i32, [c_vp])
 _sig("jt_exec_destroy", None, [c_vp])
 _sig("jt_debug_emulate_host", c_i32, [c_vp, c_i32, c_i64, c_i64, P_dbl, c_i32])
+_sig("jt_debug_time_node", c_i32, [c_vp, c_i64, c_i32, P_dbl, P_dbl, P_dbl, P_i32])
 _sig("jt_amplitude", c_i32, [c_vp, c_i32, c_i32, P_dbl])
 _sig("jt_permute", c_i32, [c_i32, c_vp, c_vp, c_i32, P_i32, c_vp])
 
@@ -101,7 +102,8 @@ EXPORTED = ["jt_last_error", "jt_version", "jt_network_create", "jt_network_add_
             "jt_plan_destroy", "jt_exec_workspace_bytes", "jt_exec_describe", "jt_exec_create", "jt_exec_contract",
             "jt_exec_contract_noreuse", "jt_exec_contract_host", "jt_exec_stats_get",
             "jt_exec_upload_leaves", "jt_exec_set_profiling", "jt_exec_stats_reset",
-            "jt_exec_invalidate", "jt_exec_destroy", "jt_amplitude", "jt_permute", "jt_debug_emulate_host"]
+            "jt_exec_invalidate", "jt_exec_destroy", "jt_amplitude", "jt_permute", "jt_debug_emulate_host",
+            "jt_debug_time_node"]
 
 
 class JetError(RuntimeError):
@@ -301,6 +303,13 @@ class Exec:
 
     def set_profiling(self, on=True):
         _check(_lib.jt_exec_set_profiling(self._h, 1 if on else 0))
+
+    def time_node(self, order_index, reps=5):
+        """DEBUG: mean ms per launch of one node (see jetb200.h)."""
+        ms, by, fl, kd = c_dbl(), c_dbl(), c_dbl(), c_i32()
+        _check(_lib.jt_debug_time_node(self._h, order_index, reps, ctypes.byref(ms), ctypes.byref(by),
+                                       ctypes.byref(fl), ctypes.byref(kd)))
+        return {"ms": ms.value, "bytes": by.value, "flop": fl.value, "kind": kd.value}
 
     def invalidate(self):
         _check(_lib.jt_exec_invalidate(self._h))
