@@ -217,7 +217,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (int i = 0; i < kt; ++i) en.tcB_k.push_back(sb[K[i].second]);
   en.kind = 1;
   en.smem = (size_t)smem;
-  en.block = kTcThreads;
+  en.block = 416;
   en.n_out = t.n_tiles << (7 + tm);
   en.grid_x = t.n_tiles;
   en.args.splits = 1;
@@ -934,8 +934,8 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
       continue;
     }
     if (en.kind == 1) {
-      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc)),
-                                                            kTcThreads, en.smem));
+      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc)), 416,
+                                                            en.smem));
       nb = std::min<int>(nb, 512 / (int)en.tc.tmem_cols);  // TMEM columns per SM
       if (nb < 1) fail(JT_EINTERNAL, "exec: a K3 tile does not fit on an SM");
       en.grid_x = std::min<int64_t>(en.tc.n_tiles, (int64_t)nb * n_sm);
@@ -1061,7 +1061,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
-    launch_pdl(pick_tc(t.tkc), dim3((unsigned)en.grid_x), dim3(kTcThreads), en.smem, ex->stream, ex->pdl, t);
+    launch_pdl(pick_tc(t.tkc), dim3((unsigned)en.grid_x), dim3(416), en.smem, ex->stream, ex->pdl, t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else {
@@ -1206,37 +1206,6 @@ void exec_contract_host(jt_exec* ex, int64_t b, int64_t e, double* h_acc) {
   exec_contract(ex, b, e, d_acc, nullptr, true);
   JT_CUDA(cudaMemcpyAsync(h_acc, d_acc, 16, cudaMemcpyDeviceToHost, ex->stream));
   JT_CUDA(cudaStreamSynchronize(ex->stream));
-}
-
-// DEBUG: time `reps` back-to-back launches of execution-order node `idx` (CUDA events on the
-// exec stream); the node reads whatever its inputs currently hold.
-void debug_time_node(jt_exec* ex, int64_t idx, int reps, double* ms_out, double* bytes, double* flop, int* kind) {
-  if (idx < 0 || idx >= (int64_t)ex->L.order.size() || reps < 1) fail(JT_EUSAGE, "debug_time_node: bad index");
-  ExecNode& en = ex->L.order[idx];
-  ex->cur_stats = &ex->stats;
-  const bool prof = ex->profiling;
-  ex->profiling = false;
-  cudaEvent_t a, b;
-  JT_CUDA(cudaEventCreate(&a));
-  JT_CUDA(cudaEventCreate(&b));
-  auto one = [&]() {
-    if (ex->dtype == JT_C64) launch_node<float>(ex, en);
-    else launch_node<double>(ex, en);
-  };
-  one();
-  JT_CUDA(cudaEventRecord(a, ex->stream));
-  for (int r = 0; r < reps; ++r) one();
-  JT_CUDA(cudaEventRecord(b, ex->stream));
-  JT_CUDA(cudaEventSynchronize(b));
-  float ms = 0;
-  JT_CUDA(cudaEventElapsedTime(&ms, a, b));
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  ex->profiling = prof;
-  *ms_out = ms / reps;
-  *bytes = en.bytes;
-  *flop = en.flop;
-  *kind = en.kind;
 }
 
 void exec_invalidate(jt_exec* ex) { ex->last = -1; }

@@ -76,10 +76,6 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
 template <int N>
 __device__ __forceinline__ void tmem_st(uint32_t taddr, const float (&v)[N]);
 template <>
-__device__ __forceinline__ void tmem_st<2>(uint32_t taddr, const float (&v)[2]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "f"(v[0]), "f"(v[1]) : "memory");
-}
-template <>
 __device__ __forceinline__ void tmem_st<4>(uint32_t taddr, const float (&v)[4]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "f"(v[0]), "f"(v[1]),
                "f"(v[2]), "f"(v[3])
@@ -164,22 +160,18 @@ __device__ __forceinline__ int tc_off(int r, int kk, int sbo, int swz) {
 
 // Warp-specialised K3 with the streamed operand in tensor memory.
 //   warps 0-3  epilogue: TMEM accumulator -> registers -> 256-B coalesced global stores
-//   warps 4-19 producers (16, four per TMEM lane quarter, each a quarter of the chunk row): cp.async gathers each item's B rows into a raw shared stage
+//   warps 4-11 producers: cp.async gathers each item's B rows into a raw shared stage
 //              (rstages-1 items in flight, no registers held); after a producer barrier each
 //              thread takes one row (its TMEM lane) and half of the K chunk, splits it into
 //              hi/lo TF32 and writes both into a TMEM X stage with tcgen05.st
-//   warp 20    MMA issuer: tcgen05.mma kind::tf32 with A = X from TMEM ([a_tmem], the "TS" form)
+//   warp 12    MMA issuer: tcgen05.mma kind::tf32 with A = X from TMEM ([a_tmem], the "TS" form)
 //              and B = Y (expanded small operand, resident in shared memory), 3xTF32
 // Barriers: xfull/xempty per TMEM X stage, tfull/tempty per accumulator.
 // TKC = K bits per chunk (row of the X stage = 2*2^TKC TF32 = hi or lo).
-constexpr int kTcProducerWarps = 16;
-constexpr int kTcThreads = (5 + kTcProducerWarps) * 32;  // epilogue 4 + producers + MMA 1
-
 template <int TKC>
-__global__ void __launch_bounds__(kTcThreads, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
-  constexpr int PW = kTcProducerWarps, NTHR = PW * 32;
-  constexpr int PER = (128 << TKC) / NTHR;     // B elements each producer thread copies per item
-  constexpr int NCOL = (2 << TKC) / (PW / 4);  // fp32 columns (of hi or lo) each producer thread writes
+__global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
+  constexpr int PER = (128 << TKC) / 256;  // B elements each producer thread copies per item
+  constexpr int NCOL = 1 << TKC;           // fp32 columns (of hi or lo) each producer thread writes
   constexpr int KPC = 2 << TKC;            // TF32 columns of one X row (hi or lo)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tg[2][64];
@@ -213,7 +205,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gett_tc_kernel(const __grid_con
   }
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) {
-      tc::mbar_init(&xfull[i], NTHR);
+      tc::mbar_init(&xfull[i], 256);
       tc::mbar_init(&xempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -259,11 +251,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) gett_tc_kernel(const __grid_con
   const uint32_t lbo = p.swz ? 16u : 128u;
   const uint32_t kstep = p.swz ? 32u : 256u;  // Y descriptor advance per 8-TF32 K step
 
-  if (warp >= 4 && warp < 4 + PW) {
+  if (warp >= 4 && warp < 12) {
     // ===================== producers =====================
-    const int ptid = tid - 128;  // 0..NTHR-1
+    const int ptid = tid - 128;  // 0..255
     const int64_t boff = slice_off(p.sv, false);
-    const int quarter = warp & 3, part = (warp - 4) >> 2;
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int row = quarter * 32 + lane;  // this thread's TMEM lane (row n of the tile)
     const int RS = p.rstages, XS = p.xstages;
     // raw row layout: 16-B chunk c of row n lives at chunk c ^ (n & (chunks-1))
@@ -274,7 +266,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gett_tc_kernel(const __grid_con
     int32_t soff[PER];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      const int e = ptid + i * NTHR;
+      const int e = ptid + i * 256;
       goff[i] = tg[0][e & 63] + tg[1][e >> 6];
       soff[i] = ts[0][e & 63] ^ ts[1][e >> 6];
     }
@@ -283,10 +275,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gett_tc_kernel(const __grid_con
       const int64_t t = (int64_t)blockIdx.x + (it >> lg_kc) * gridDim.x;
       const int c = (int)(it & ((1 << lg_kc) - 1));
       // tile base offset: lane j contributes outer bit j, butterfly-summed over the warp
-      int64_t tb = (lane < p.n_outer && ((t >> lane) & 1)) ? p.o_sB[lane] : 0;
+      int64_t part = (lane < p.n_outer && ((t >> lane) & 1)) ? p.o_sB[lane] : 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tb += __shfl_xor_sync(0xffffffffu, tb, o);
-      int64_t src = boff + tb;
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      int64_t src = boff + part;
       for (int j = 0; j < lg_kc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
       unsigned char* raw = R + (int)(it % RS) * p.rbytes;
       const float2* srcp = p.B + src;
@@ -306,7 +298,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gett_tc_kernel(const __grid_con
         case 5: cp_async_wait<3>(); break;
         default: cp_async_wait<4>(); break;
       }
-      tc::bar_sync(1, NTHR);  // all producers' copies of item it landed; raw stage of it-1 is free
+      tc::bar_sync(1, 256);  // all producers' copies of item it landed; raw stage of it-1 is free
       if (it + RS - 1 < items) copy(it + RS - 1);
       cp_async_commit();
       const int xs = (int)(it % XS);
@@ -315,24 +307,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) gett_tc_kernel(const __grid_con
       const unsigned char* raw = R + (int)(it % RS) * p.rbytes + row * rb;
       float hi[NCOL], lo[NCOL];
 #pragma unroll
-      for (int j = 0; j < NCOL / 2; ++j) {
-        const int byte = (part * NCOL + 2 * j) * 4;  // 8-B complex of this row
-        const float2 v = *reinterpret_cast<const float2*>(
-            raw + ((((byte >> 4) ^ (row & (chunks - 1))) << 4) | (byte & 15)));
-        hi[2 * j] = tc::tf32_trunc(v.x);
-        lo[2 * j] = v.x - hi[2 * j];
-        hi[2 * j + 1] = tc::tf32_trunc(v.y);
-        lo[2 * j + 1] = v.y - hi[2 * j + 1];
+      for (int j = 0; j < NCOL / 4; ++j) {
+        const int cc = half * (NCOL / 4) + j;  // 16-B chunk of this row = 2 complex
+        const float4 v = *reinterpret_cast<const float4*>(raw + ((cc ^ (row & (chunks - 1))) << 4));
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hi[4 * j + q] = tc::tf32_trunc(x[q]);
+          lo[4 * j + q] = x[q] - hi[4 * j + q];
+        }
       }
       const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-      const uint32_t col = xcol0 + (uint32_t)(xs * 2 * KPC + part * NCOL);
+      const uint32_t col = xcol0 + (uint32_t)(xs * 2 * KPC + half * NCOL);
       tc::tmem_st<NCOL>(lane_addr + col, hi);
       tc::tmem_st<NCOL>(lane_addr + col + KPC, lo);
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(&xfull[xs]);
     }
-  } else if (warp == 4 + PW) {
+  } else if (warp == 12) {
     // ===================== MMA issuer =====================
     const bool leader = lane == 0;
     int64_t tt = 0;
