@@ -273,6 +273,11 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   t.n_oN = (int)oN.size();
   t.n_oM = (int)oM.size();
   t.tmt = tmt;
+  {
+    const char* e = getenv("JETB200_TCG_BM");  // tuning knob: band height (log2 M tiles)
+    t.lg_bm = std::min(e ? atoi(e) : 4, t.n_oM);
+    if (t.lg_bm < 0) t.lg_bm = 0;
+  }
   t.lg_kc = (int)ko.size();
   t.nXb = 11;
   t.nAb = tmt + 4;
@@ -1206,6 +1211,37 @@ void exec_contract_host(jt_exec* ex, int64_t b, int64_t e, double* h_acc) {
   exec_contract(ex, b, e, d_acc, nullptr, true);
   JT_CUDA(cudaMemcpyAsync(h_acc, d_acc, 16, cudaMemcpyDeviceToHost, ex->stream));
   JT_CUDA(cudaStreamSynchronize(ex->stream));
+}
+
+// DEBUG: time `reps` back-to-back launches of execution-order node `idx` (CUDA events on the
+// exec stream); the node reads whatever its inputs currently hold.
+void debug_time_node(jt_exec* ex, int64_t idx, int reps, double* ms_out, double* bytes, double* flop, int* kind) {
+  if (idx < 0 || idx >= (int64_t)ex->L.order.size() || reps < 1) fail(JT_EUSAGE, "debug_time_node: bad index");
+  ExecNode& en = ex->L.order[idx];
+  ex->cur_stats = &ex->stats;
+  const bool prof = ex->profiling;
+  ex->profiling = false;
+  cudaEvent_t a, b;
+  JT_CUDA(cudaEventCreate(&a));
+  JT_CUDA(cudaEventCreate(&b));
+  auto one = [&]() {
+    if (ex->dtype == JT_C64) launch_node<float>(ex, en);
+    else launch_node<double>(ex, en);
+  };
+  one();
+  JT_CUDA(cudaEventRecord(a, ex->stream));
+  for (int r = 0; r < reps; ++r) one();
+  JT_CUDA(cudaEventRecord(b, ex->stream));
+  JT_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  JT_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  ex->profiling = prof;
+  *ms_out = ms / reps;
+  *bytes = en.bytes;
+  *flop = en.flop;
+  *kind = en.kind;
 }
 
 void exec_invalidate(jt_exec* ex) { ex->last = -1; }

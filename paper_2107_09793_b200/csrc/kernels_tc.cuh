@@ -176,9 +176,15 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
+  __shared__ int64_t kc_off[16];  // B offset of K chunk c (n_kc <= 16)
   __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < 16) {
+    int64_t o = 0;
+    for (int j = 0; j < p.K - p.tkc; ++j) if ((tid >> j) & 1) o += p.o_kB[j];
+    kc_off[tid] = o;
+  }
   // 1024-B aligned carve: Y planes [hi c=0..n_kc-1 | lo ...], then the raw stages
   unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* Yhi = base;
@@ -246,7 +252,6 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   const uint32_t xcol0 = (uint32_t)(p.acc_bufs * p.Np);  // first TMEM column of the X stages
   const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles * p.n_kc;
-  auto tile_of = [&](int64_t it) { return (int64_t)blockIdx.x + (it / p.n_kc) * gridDim.x; };
   const uint32_t layout = p.swz ? 2u : 0u;
   const uint32_t lbo = p.swz ? 16u : 128u;
   const uint32_t kstep = p.swz ? 32u : 256u;  // Y descriptor advance per 8-TF32 K step
@@ -270,25 +275,36 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       goff[i] = tg[0][e & 63] + tg[1][e >> 6];
       soff[i] = ts[0][e & 63] ^ ts[1][e >> 6];
     }
-    const int lg_kc = p.K - p.tkc;  // n_kc = 2^lg_kc
-    auto copy = [&](int64_t it) {
-      const int64_t t = (int64_t)blockIdx.x + (it >> lg_kc) * gridDim.x;
-      const int c = (int)(it & ((1 << lg_kc) - 1));
-      // tile base offset: lane j contributes outer bit j, butterfly-summed over the warp
-      int64_t part = (lane < p.n_outer && ((t >> lane) & 1)) ? p.o_sB[lane] : 0;
+    // copy cursor: the next item to gather (tile number ct of this CTA, K chunk cc); the tile
+    // base offset is re-summed (lane j holds outer bit j's stride) only when the tile changes
+    const int64_t o_s = lane < p.n_outer ? p.o_sB[lane] : 0;
+    auto tile_base = [&](int64_t ct) {
+      const int64_t t = (int64_t)blockIdx.x + ct * gridDim.x;
+      int64_t tb = ((t >> lane) & 1) ? o_s : 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      int64_t src = boff + part;
-      for (int j = 0; j < lg_kc; ++j) if ((c >> j) & 1) src += p.o_kB[j];
-      unsigned char* raw = R + (int)(it % RS) * p.rbytes;
-      const float2* srcp = p.B + src;
+      for (int o = 16; o > 0; o >>= 1) tb += __shfl_xor_sync(0xffffffffu, tb, o);
+      return boff + tb;
+    };
+    int64_t ct = 0, cbase = tile_base(0);
+    int cc = 0, wst = 0;  // wst = raw stage the next copy lands in
+    auto copy = [&]() {
+      unsigned char* raw = R + wst * p.rbytes;
+      const float2* srcp = p.B + (cbase + kc_off[cc]);
 #pragma unroll
       for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], srcp + goff[i]);
+      if (++wst == RS) wst = 0;
+      if (++cc == p.n_kc) {
+        cc = 0;
+        ++ct;
+        cbase = tile_base(ct);
+      }
     };
     for (int q = 0; q < RS - 1; ++q) {
-      if (q < items) copy(q);
+      if (q < items) copy();
       cp_async_commit();
     }
+    int rst = 0, xs = 0;
+    uint32_t xph = 0;
     for (int64_t it = 0; it < items; ++it) {
       // own copies of item it have landed (RS-1+it groups committed, RS-2 may stay pending)
       switch (RS) {
@@ -299,12 +315,12 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
         default: cp_async_wait<4>(); break;
       }
       tc::bar_sync(1, 256);  // all producers' copies of item it landed; raw stage of it-1 is free
-      if (it + RS - 1 < items) copy(it + RS - 1);
+      if (it + RS - 1 < items) copy();
       cp_async_commit();
-      const int xs = (int)(it % XS);
-      tc::mbar_wait(&xempty[xs], (uint32_t)(((it / XS) & 1) ^ 1));  // TMEM X stage free
+      tc::mbar_wait(&xempty[xs], xph ^ 1);  // TMEM X stage free
       tc::fence_after();
-      const unsigned char* raw = R + (int)(it % RS) * p.rbytes + row * rb;
+      const unsigned char* raw = R + rst * p.rbytes + row * rb;
+      if (++rst == RS) rst = 0;
       float hi[NCOL], lo[NCOL];
 #pragma unroll
       for (int j = 0; j < NCOL / 4; ++j) {
@@ -324,19 +340,20 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(&xfull[xs]);
+      if (++xs == XS) { xs = 0; xph ^= 1; }
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
     const bool leader = lane == 0;
     int64_t tt = 0;
     const int XS = p.xstages;
+    int xs = 0, c = 0;
+    uint32_t xph = 0;
     for (int64_t it = 0; it < items; ++it) {
-      const int xs = (int)(it % XS);
-      const int c = (int)(it % p.n_kc);
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
       if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
-      tc::mbar_wait(&xfull[xs], (uint32_t)((it / XS) & 1));
+      tc::mbar_wait(&xfull[xs], xph);
       tc::fence_after();
       if (leader) {
         const uint32_t d = tmem + (uint32_t)(b * p.Np);
@@ -355,6 +372,8 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       }
       __syncwarp();
       if (c == p.n_kc - 1) ++tt;
+      if (++c == p.n_kc) c = 0;
+      if (++xs == XS) { xs = 0; xph ^= 1; }
     }
   } else if (warp < 4) {
     // ===================== epilogue =====================

@@ -27,6 +27,7 @@ struct TcgArgs {
   int32_t Np;               // MMA N = 2 * 2^tmt
   uint32_t idesc, tmem_cols;
   int32_t rstages, rbytes_b, rbytes_a, acc_bufs;
+  int32_t lg_bm;            // tile raster: bands of 2^lg_bm M tiles (<= n_oM) walked N-major
   int64_t o_B[32], o_A[32]; // outer N bit strides in B / outer M bit strides in A
   int64_t k_B[32], k_A[32]; // chunk-index bit strides in B / in A
   int64_t gB[12], gA[12];   // chunk-tile bits (stride order): global strides
@@ -43,6 +44,17 @@ __device__ __forceinline__ int64_t bits_sum(int64_t v, int n, const int64_t* str
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   return part;
+}
+// Processing order -> canonical tile index (N bits low, M bits high).  Consecutive t (the
+// CTAs of one wave) cover 2^lg_bm M tiles x ~148/2^lg_bm N tiles, so each B chunk is read
+// from HBM once per band and served to the band's other CTAs from L2 (and each A chunk to
+// the wave's N tiles), instead of once per M tile.
+__device__ __forceinline__ int64_t raster(int64_t t, const TcgArgs& p) {
+  const int lb = p.lg_bm;
+  const int64_t mlo = t & ((int64_t(1) << lb) - 1);
+  const int64_t n = (t >> lb) & ((int64_t(1) << p.n_oN) - 1);
+  const int64_t band = t >> (lb + p.n_oN);
+  return n | (((band << lb) | mlo) << p.n_oN);
 }
 }  // namespace tcg
 
@@ -128,13 +140,15 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       goffA[i] = tga[0][e & 63] + tga[1][e >> 6];
       soffA[i] = tsa[0][e & 63] ^ tsa[1][e >> 6];
     }
+    int wst = 0;  // raw stage the next copy lands in
     auto copy = [&](int64_t it) {
-      const int64_t t = (int64_t)blockIdx.x + (it >> p.lg_kc) * gridDim.x;
+      const int64_t t = tcg::raster((int64_t)blockIdx.x + (it >> p.lg_kc) * gridDim.x, p);
       const int64_t c = it & kc_mask;
       const int64_t tb = tcg::bits_sum(t, p.n_oN, p.o_B, lane) + tcg::bits_sum(c, p.lg_kc, p.k_B, lane);
       const int64_t ta = tcg::bits_sum(t >> p.n_oN, p.n_oM, p.o_A, lane) + tcg::bits_sum(c, p.lg_kc, p.k_A, lane);
-      unsigned char* rb = RB + (int)(it % RS) * p.rbytes_b;
-      unsigned char* ra = RA + (int)(it % RS) * p.rbytes_a;
+      unsigned char* rb = RB + wst * p.rbytes_b;
+      unsigned char* ra = RA + wst * p.rbytes_a;
+      if (++wst == RS) wst = 0;
       const float2* sb = p.B + boff + tb;
       const float2* sa = p.A + aoff + ta;
 #pragma unroll
@@ -147,6 +161,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       if (q < items) copy(q);
       cp_async_commit();
     }
+    int rst = 0;  // raw stage of item it
     for (int64_t it = 0; it < items; ++it) {
       switch (RS) {
         case 2: cp_async_wait<0>(); break;
@@ -164,7 +179,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       tc::fence_after();
       // ---- X: this thread's row, half of the chunk -> hi/lo TF32 in TMEM
       {
-        const unsigned char* raw = RB + (int)(it % RS) * p.rbytes_b + row * 128;
+        const unsigned char* raw = RB + rst * p.rbytes_b + row * 128;
         float hi[16], lo[16];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -184,7 +199,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       }
       // ---- Y: expand the A chunk into [[Re,-Im],[Im,Re]] hi/lo (SWIZZLE_128B, K-major)
       {
-        const unsigned char* raw = RA + (int)(it % RS) * p.rbytes_a;
+        const unsigned char* raw = RA + rst * p.rbytes_a;
         unsigned char* yhi = Y + ys * 2 * NP * 128;
         unsigned char* ylo = yhi + NP * 128;
 #pragma unroll
@@ -217,6 +232,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(&full[xs]);
+      if (++rst == RS) rst = 0;
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
@@ -256,7 +272,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
       tc::mbar_wait(&tfull[b], tph);
       tc::fence_after();
-      const int64_t t = (int64_t)blockIdx.x + tt * gridDim.x;
+      const int64_t t = tcg::raster((int64_t)blockIdx.x + tt * gridDim.x, p);
       float2* out = p.C + (t << (7 + TMT));
 #pragma unroll 1
       for (int c0 = 0; c0 < NP; c0 += 16) {
