@@ -121,9 +121,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "JT_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra JT_WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
+      "r"(phase), "r"(0x100000)  // suspend-time hint: sleep until the phase flips, don't spin
       : "memory");
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -148,7 +148,14 @@ __device__ __forceinline__ float tf32_hi(float x) {
 // 3xTF32 split by truncation: hi = x with the low 13 mantissa bits cleared (exactly a TF32
 // value, so the MMA reads it exactly whatever its own rounding), lo = x - hi (exact in fp32);
 // lo is then read at TF32 precision (relative error 2^-11 of lo, ~2^-22 of x).
-__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// Round-to-nearest TF32 (low 13 mantissa bits zero).  The 3xTF32 split is hi = rna(x),
+// lo = rna(x - hi): both are exact TF32 inputs, so |x - hi - lo| <= 2^-22 |x| and the MMA's
+// own handling of the low mantissa bits never enters (a truncated split loses ~4x more).
+// (Integer form of cvt.rna.tf32.f32, which ptxas expands with an Inf/NaN branch; the
+// operands here are finite.)
+__device__ __forceinline__ float tf32_rna(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 }  // namespace tc
 
@@ -238,9 +245,9 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
         for (int t = 0; t < 2; ++t) {
           const int byte = c * p.yplane + tc_off(2 * m + s, 2 * kl + t, p.sbo_y, p.swz);
           const float x = vals[s][t];
-          const float hi = tc::tf32_trunc(x);
+          const float hi = tc::tf32_rna(x);
           *reinterpret_cast<float*>(Yhi + byte) = hi;
-          *reinterpret_cast<float*>(Ylo + byte) = x - hi;
+          *reinterpret_cast<float*>(Ylo + byte) = tc::tf32_rna(x - hi);
         }
     }
   }
@@ -329,8 +336,8 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
         const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          hi[4 * j + q] = tc::tf32_trunc(x[q]);
-          lo[4 * j + q] = x[q] - hi[4 * j + q];
+          hi[4 * j + q] = tc::tf32_rna(x[q]);
+          lo[4 * j + q] = tc::tf32_rna(x[q] - hi[4 * j + q]);
         }
       }
       const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tgb[2][64], tga[2][64];
   __shared__ int32_t tsb[2][64], tsa[2][64];
+  __shared__ int64_t dkB[32], dkA[32];  // chunk c -> c+1 offset steps, by trailing ones of c
   __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -89,6 +90,12 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       tgb[h][i] = g; tsb[h][i] = s;
       tga[h][i] = ga; tsa[h][i] = sa;
     }
+  }
+  if (tid < p.lg_kc) {
+    int64_t b = p.k_B[tid], a = p.k_A[tid];
+    for (int j = 0; j < tid; ++j) { b -= p.k_B[j]; a -= p.k_A[j]; }
+    dkB[tid] = b;
+    dkA[tid] = a;
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_base_sh)),
@@ -140,22 +147,46 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       goffA[i] = tga[0][e & 63] + tga[1][e >> 6];
       soffA[i] = tsa[0][e & 63] ^ tsa[1][e >> 6];
     }
+    // copy cursor: tile ct of this CTA, chunk cc; tile bases re-summed (lane j holds outer
+    // bit j's stride) only when the tile changes, chunk offsets stepped through dkB/dkA
+    const int64_t ob = lane < p.n_oN ? p.o_B[lane] : 0, oa = lane < p.n_oM ? p.o_A[lane] : 0;
+    int64_t ct = 0, cc = 0, tileB = 0, tileA = 0, kB = 0, kA = 0;
+    auto tile_bases = [&]() {
+      const int64_t t = tcg::raster((int64_t)blockIdx.x + ct * gridDim.x, p);
+      int64_t b = ((t >> lane) & 1) ? ob : 0;
+      int64_t a = (((t >> p.n_oN) >> lane) & 1) ? oa : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+      }
+      tileB = boff + b;
+      tileA = aoff + a;
+    };
+    tile_bases();
     int wst = 0;  // raw stage the next copy lands in
-    auto copy = [&](int64_t it) {
-      const int64_t t = tcg::raster((int64_t)blockIdx.x + (it >> p.lg_kc) * gridDim.x, p);
-      const int64_t c = it & kc_mask;
-      const int64_t tb = tcg::bits_sum(t, p.n_oN, p.o_B, lane) + tcg::bits_sum(c, p.lg_kc, p.k_B, lane);
-      const int64_t ta = tcg::bits_sum(t >> p.n_oN, p.n_oM, p.o_A, lane) + tcg::bits_sum(c, p.lg_kc, p.k_A, lane);
+    auto copy = [&](int64_t) {
       unsigned char* rb = RB + wst * p.rbytes_b;
       unsigned char* ra = RA + wst * p.rbytes_a;
       if (++wst == RS) wst = 0;
-      const float2* sb = p.B + boff + tb;
-      const float2* sa = p.A + aoff + ta;
+      const float2* sb = p.B + (tileB + kB);
+      const float2* sa = p.A + (tileA + kA);
 #pragma unroll
       for (int i = 0; i < PERB; ++i) cp_async8(rb + soffB[i], sb + goffB[i]);
 #pragma unroll
       for (int i = 0; i < PERA; ++i)
         if (ptid + i * 256 < MT * 16) cp_async8(ra + soffA[i], sa + goffA[i]);
+      if (cc == kc_mask) {
+        cc = 0;
+        kB = kA = 0;
+        ++ct;
+        tile_bases();
+      } else {
+        const int tz = __ffsll(~cc) - 1;  // trailing ones of cc
+        kB += dkB[tz];
+        kA += dkA[tz];
+        ++cc;
+      }
     };
     for (int q = 0; q < RS - 1; ++q) {
       if (q < items) copy(q);
@@ -188,8 +219,8 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
           const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            hi[4 * j + q] = tc::tf32_trunc(x[q]);
-            lo[4 * j + q] = x[q] - hi[4 * j + q];
+            hi[4 * j + q] = tc::tf32_rna(x[q]);
+            lo[4 * j + q] = tc::tf32_rna(x[q] - hi[4 * j + q]);
           }
         }
         const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -213,10 +244,10 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
             float h0[4], l0[4], h1[4], l1[4];
 #pragma unroll
             for (int z = 0; z < 4; ++z) {
-              h0[z] = tc::tf32_trunc(r0[z]);
-              l0[z] = r0[z] - h0[z];
-              h1[z] = tc::tf32_trunc(r1[z]);
-              l1[z] = r1[z] - h1[z];
+              h0[z] = tc::tf32_rna(r0[z]);
+              l0[z] = tc::tf32_rna(r0[z] - h0[z]);
+              h1[z] = tc::tf32_rna(r1[z]);
+              l1[z] = tc::tf32_rna(r1[z] - h1[z]);
             }
             const int ra0 = 2 * m, ra1 = 2 * m + 1;
             const int b0 = (ra0 & 7) * 128 + (ra0 >> 3) * 1024 + ((kp ^ (ra0 & 7)) << 4);
