@@ -75,7 +75,7 @@ typedef struct {
 /* Cost counters (PAPER.md l.140-146 Eq. sliced_flops, l.205-212 Eq. task_based;
    FLOP convention: 8 real FLOP x prod(distinct dims) per pairwise step, reading A11). */
 typedef struct {
-  int64_t n_sl;            /* N_sl = prod of sliced dims */
+  int64_t n_sl;            /* N_sl = prod of sliced (summed) dims, per amplitude */
   double flop_sl;          /* FLOP of one slice */
   double flop_shared;      /* FLOP of nodes with S(v) = {} (f_sl = flop_shared / flop_sl) */
   double e_flsl;           /* N_sl * FLOP_sl */
@@ -86,6 +86,9 @@ typedef struct {
   double bytes_sl;         /* algorithmic bytes of one slice at 8 B/elem: sum_v (|A|+|B|+|C|) */
   int64_t n_steps;         /* SSA path length */
   int32_t n_sliced;
+  int64_t n_batch;         /* amplitudes per run (d^open wires, jt_network_close_batch); 1 otherwise.
+                              e_flsl / e_fltask / exact_reuse / prefix count all n_sl x n_batch
+                              contractions of the multi-contraction */
 } jt_cost;
 
 /* Execution statistics accumulated by jt_exec_contract. */
@@ -120,6 +123,18 @@ jt_status jt_network_create(int32_t n_wires, int32_t d, jt_network** out);
 jt_status jt_network_add_gate(jt_network* net, int32_t k, const int32_t* wires, const double* u);
 /* Attach <x_w| to every wire (l.83); x: n_wires digits in [0,d); copied; once. */
 jt_status jt_network_close(jt_network* net, const int32_t* x);
+/* Batch of amplitudes ("computing batches of amplitudes" as a
+   multi-contraction with shared work).  Like jt_network_close, but every wire in
+   open_wires[0..n_open) gets the d x d identity with labels (wire label, batch label) in
+   place of its bra; the batch labels are new labels n_labels.. n_labels+n_open-1 in
+   open-wire order and sit on that one tensor.  A plan of this network loops over
+   (summed slice, batch digits) with the batch labels innermost; fixing batch label i to y_i
+   turns the identity into <y_i|, so run r = sigma * n_batch + y computes s_sigma of the
+   amplitude <x with x[open_wires[i]] = y_i|U|0>, y mixed radix with open_wires[0] most
+   significant.  The prefix cache then recomputes only the nodes that depend on the batch
+   digits (the bra-attached subtrees) per bitstring.  x digits of open wires are ignored.
+   Errors: 2 for a repeated or out-of-range open wire. */
+jt_status jt_network_close_batch(jt_network* net, const int32_t* x, const int32_t* open_wires, int32_t n_open);
 /* Counts of the raw network (kets + gates + bras) and labels. */
 jt_status jt_network_info(const jt_network* net, int64_t* n_tensors, int64_t* n_labels);
 /* Neutral JSON file: wires, d, per tensor its labels (data are not written). */
@@ -129,7 +144,8 @@ void jt_network_destroy(jt_network* net);
 /* ---- plan (path + slices) ------------------------------- */
 /* ssa_path: 2*n_steps ids; sliced_labels: n_sliced bond labels in loop order.  The network
    must be closed.  Validation (error 3): ids consumed once, one tensor left, sliced labels
-   are bonds, no duplicates. */
+   are bonds, no duplicates.  Batch labels of the network are appended to the loop order
+   (innermost) automatically and are not listed by jt_plan_get. */
 jt_status jt_plan_create(const jt_network* net, const int64_t* ssa_path, int64_t n_steps,
                          const int64_t* sliced_labels, int32_t n_sliced, jt_plan** out);
 /* Host greedy planner: absorption of rank<=2 tensors, randomised greedy, subtree
@@ -162,14 +178,17 @@ jt_status jt_exec_create(const jt_plan* plan, jt_dtype dtype, int32_t device, vo
    adding sum s_sigma into d_acc (device complex128, 2 doubles) in order -- async on the
    stream.  If h_slice_vals is non-NULL the call synchronises the stream and writes
    (end-begin) complex128 values s_sigma there (at most min(N_sl, 2^20) per call, else
-   error 2).  The cache persists across calls. */
+   error 2).  The cache persists across calls.
+   Batch plans (jt_network_close_batch): the index runs over N_sl x n_batch runs
+   r = sigma * n_batch + y and d_acc holds n_batch complex128 (2 * n_batch doubles);
+   run r adds into d_acc[2y], d_acc[2y+1]. */
 jt_status jt_exec_contract(jt_exec* ex, int64_t slice_begin, int64_t slice_end, double* d_acc,
                            double* h_slice_vals);
 /* Same with the prefix cache disabled: every node is recomputed for every slice (E-flsl). */
 jt_status jt_exec_contract_noreuse(jt_exec* ex, int64_t slice_begin, int64_t slice_end,
                                    double* d_acc, double* h_slice_vals);
 /* Host-buffer path: copies nothing else; equals jt_exec_contract + D2H of the sum.  h_acc
-   receives the complex128 sum of the range (synchronous). */
+   receives the complex128 sum of the range (synchronous); n_batch complex128 for batch plans. */
 jt_status jt_exec_contract_host(jt_exec* ex, int64_t slice_begin, int64_t slice_end, double* h_acc);
 /* Re-upload the leaf tensors (the network data) from host memory through a pinned staging
    buffer, H2D on the stream (the per-step input copy of the end-to-end path). */
@@ -183,8 +202,9 @@ jt_status jt_exec_stats_reset(jt_exec* ex);
 jt_status jt_exec_invalidate(jt_exec* ex);
 void jt_exec_destroy(jt_exec* ex);
 
-/* 1-GPU convenience, synchronous: allocates its own workspace. out = (re, im). */
-jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, double out[2]);
+/* 1-GPU convenience, synchronous: allocates its own workspace. out = (re, im); for batch
+   plans out holds n_batch complex128 amplitudes (2 * n_batch doubles), y-indexed. */
+jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, double* out);
 
 /* TEST ONLY (never called by jt_exec_*): execute the compiled K2 descriptors, workspace
    layout and prefix-cache schedule for slices [b,e) on the host with the kernels' index

@@ -130,3 +130,42 @@ def amplitude(net, ssa_path, sliced_labels=()):
     for v in vals:
         acc += v
     return acc
+
+
+def batch_bitstrings(bitstring, open_wires, d):
+    """The bitstrings of a batch of amplitudes: bitstring with the digits of open_wires
+    enumerated lexicographically, open_wires[0] most significant (reading A23)."""
+    out = []
+    for digits in itertools.product(range(d), repeat=len(open_wires)):
+        x = [int(v) for v in bitstring]
+        for w, v in zip(open_wires, digits):
+            x[w] = v
+        out.append(x)
+    return out
+
+
+def batch_run_values(circuit, bitstring, open_wires, ssa_path, sliced_labels, runs):
+    """Batch of amplitudes as a multi-contraction ("computing batches of
+    amplitudes"): run r = sigma * n_batch + y is s_sigma of the amplitude of the y-th batch
+    bitstring, each a plain closed network contracted along the same SSA path (the tensor
+    ids do not depend on the bra digits, so one path serves every bitstring)."""
+    from .network import build_network
+
+    xs = batch_bitstrings(bitstring, open_wires, circuit.d)
+    nb = len(xs)
+    nets = {}
+    out = []
+    for r in runs:
+        sig, y = divmod(int(r), nb)
+        if y not in nets:
+            nets[y] = build_network(circuit, xs[y])
+        out.append(slice_values(nets[y], ssa_path, list(sliced_labels), [sig])[0])
+    return out
+
+
+def batch_amplitudes(circuit, bitstring, open_wires, ssa_path, sliced_labels=()):
+    """Every amplitude of the batch, y-indexed: Eq. sliced_sum per bitstring."""
+    from .network import build_network
+
+    return [amplitude(build_network(circuit, x), ssa_path, sliced_labels)
+            for x in batch_bitstrings(bitstring, open_wires, circuit.d)]

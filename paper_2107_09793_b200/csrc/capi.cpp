@@ -8,7 +8,7 @@
 namespace jt {
 jt_network* network_create(int32_t n_wires, int32_t d);
 void network_add_gate(jt_network* net, int32_t k, const int32_t* wires, const double* u);
-void network_close(jt_network* net, const int32_t* x);
+void network_close(jt_network* net, const int32_t* x, const int32_t* open_wires, int32_t n_open);
 void network_export(const jt_network* net, const char* path);
 void plan_export(const jt_plan* plan, const char* path);
 int64_t workspace_bytes(const jt_plan& plan, jt_dtype dt);
@@ -24,7 +24,7 @@ void upload_leaves(jt_exec* ex);
 void exec_stats(const jt_exec* ex, jt_exec_stats* out);
 void exec_stats_reset(jt_exec* ex);
 void exec_destroy(jt_exec* ex);
-void amplitude(const jt_plan& plan, jt_dtype dt, int device, double out[2]);
+void amplitude(const jt_plan& plan, jt_dtype dt, int device, double* out);
 void permute(jt_dtype dt, const void* src, void* dst, int n, const int32_t* perm, void* stream);
 
 static thread_local std::string g_last_error;
@@ -72,7 +72,10 @@ jt_status jt_network_add_gate(jt_network* net, int32_t k, const int32_t* wires, 
   return guarded([&] { network_add_gate(net, k, wires, u); });
 }
 jt_status jt_network_close(jt_network* net, const int32_t* x) {
-  return guarded([&] { network_close(net, x); });
+  return guarded([&] { network_close(net, x, nullptr, 0); });
+}
+jt_status jt_network_close_batch(jt_network* net, const int32_t* x, const int32_t* open_wires, int32_t n_open) {
+  return guarded([&] { network_close(net, x, open_wires, n_open); });
 }
 jt_status jt_network_info(const jt_network* net, int64_t* n_tensors, int64_t* n_labels) {
   return guarded([&] {
@@ -101,6 +104,8 @@ jt_status jt_plan_create(const jt_network* net, const int64_t* ssa_path, int64_t
       p->net = *net;
       p->path.assign(ssa_path, ssa_path + 2 * n_steps);
       p->sliced.assign(sliced_labels, sliced_labels + n_sliced);
+      p->n_summed = n_sliced;
+      p->sliced.insert(p->sliced.end(), net->batch_labels.begin(), net->batch_labels.end());
       build_plan_tree(*p);
     } catch (...) {
       delete p;
@@ -120,6 +125,8 @@ jt_status jt_plan_greedy(const jt_network* net, const jt_planner_opts* opts, jt_
     try {
       p->net = *net;
       greedy_plan(*net, o, p->path, p->sliced);
+      p->n_summed = (int)p->sliced.size();
+      p->sliced.insert(p->sliced.end(), net->batch_labels.begin(), net->batch_labels.end());
       build_plan_tree(*p);
     } catch (...) {
       delete p;
@@ -133,14 +140,14 @@ jt_status jt_plan_sizes(const jt_plan* plan, int64_t* n_steps, int32_t* n_sliced
   return guarded([&] {
     NEED(plan, "jt_plan_sizes");
     if (n_steps) *n_steps = (int64_t)plan->path.size() / 2;
-    if (n_sliced) *n_sliced = (int32_t)plan->sliced.size();
+    if (n_sliced) *n_sliced = (int32_t)plan->n_summed;
   });
 }
 jt_status jt_plan_get(const jt_plan* plan, int64_t* ssa_path, int64_t* sliced_labels) {
   return guarded([&] {
     NEED(plan, "jt_plan_get");
     if (ssa_path) std::memcpy(ssa_path, plan->path.data(), plan->path.size() * sizeof(int64_t));
-    if (sliced_labels) std::memcpy(sliced_labels, plan->sliced.data(), plan->sliced.size() * sizeof(int64_t));
+    if (sliced_labels) std::memcpy(sliced_labels, plan->sliced.data(), plan->n_summed * sizeof(int64_t));
   });
 }
 jt_status jt_plan_cost(const jt_plan* plan, jt_cost* out) {
@@ -249,7 +256,7 @@ jt_status jt_debug_time_node(jt_exec* ex, int64_t order_index, int32_t reps, dou
   });
 }
 
-jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, double out[2]) {
+jt_status jt_amplitude(const jt_plan* plan, jt_dtype dtype, int32_t device, double* out) {
   return guarded([&] {
     NEED(plan && out, "jt_amplitude");
     amplitude(*plan, dtype, device, out);

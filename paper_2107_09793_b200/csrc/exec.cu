@@ -661,7 +661,7 @@ Layout compile(const jt_plan& plan, int esize) {
   L.vals_cap = 1;
   while (L.vals_cap < plan.n_sl && L.vals_cap < (int64_t(1) << 20)) L.vals_cap <<= 1;
   L.acc_base = align_up(L.vals_base + L.vals_cap * 16);
-  L.state_base = align_up(L.acc_base + 16);
+  L.state_base = align_up(L.acc_base + 16 * plan.n_batch);
   L.total = align_up(L.state_base + (int64_t)sizeof(SliceState));
   return L;
 }
@@ -851,8 +851,10 @@ struct jt_exec {
   char* ws = nullptr;
   int64_t ws_bytes = 0;
   cudaStream_t stream = nullptr;
-  int64_t n_sl = 1;
-  int k = 0, d = 2;
+  int64_t n_sl = 1;       // runs: summed slices x batch
+  int k = 0, d = 2;       // loop positions (summed + batch), qudit dimension
+  int n_summed = 0;       // first batch position
+  int64_t n_batch = 1;
   int64_t last = -1;  // last slice whose values are in the prefix cache, -1 = cold
   jt_exec_stats stats{};
   std::vector<char> host_leaves;   // leaf data converted to the exec dtype
@@ -932,8 +934,10 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   set_smem_attrs();
   int n_sm = 148;
   JT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+  const char* kdbg = std::getenv("JETB200_K3_DBG");  // DEBUG: K3 roofline split (skip stores / loads)
   for (ExecNode& en : L.order) {
     int nb = 1;
+    if (kdbg) en.tc.dbg = std::atoi(kdbg);
     if (en.kind == 2) {
       en.grid_x = std::min<int64_t>(en.tcg.n_tiles, n_sm);  // one CTA per SM (512 TMEM columns)
       continue;
@@ -983,6 +987,8 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   ex->n_sl = plan.n_sl;
   ex->k = (int)plan.sliced.size();
   ex->d = plan.net.d;
+  ex->n_summed = plan.n_summed;
+  ex->n_batch = plan.n_batch;
   // leaves converted to the exec dtype, uploaded through a pinned staging buffer
   ex->host_leaves.assign(ex->L.leaf_bytes, 0);
   const int64_t nt = (int64_t)plan.net.tensors.size();
@@ -1107,7 +1113,8 @@ void slice_sequence(jt_exec* ex, int j, double* d_acc) {
   const ExecNode& root = ex->L.order.back();
   launch_pdl(accumulate_kernel<R>, dim3(1), dim3(32), 0, ex->stream, ex->pdl,
              reinterpret_cast<const C2*>(ex->ws + root.out_off), d_acc,
-             reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), (const SliceState*)state);
+             reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), (const SliceState*)state, ex->n_summed,
+             ex->k - ex->n_summed, ex->d);
   ex->cur_stats->kernel_launches++;
   ex->cur_stats->slices_done++;
 }
@@ -1207,9 +1214,9 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
 void exec_contract_host(jt_exec* ex, int64_t b, int64_t e, double* h_acc) {
   double* d_acc = reinterpret_cast<double*>(ex->ws + ex->L.acc_base);
   JT_CUDA(cudaSetDevice(ex->device));
-  JT_CUDA(cudaMemsetAsync(d_acc, 0, 16, ex->stream));
+  JT_CUDA(cudaMemsetAsync(d_acc, 0, 16 * ex->n_batch, ex->stream));
   exec_contract(ex, b, e, d_acc, nullptr, true);
-  JT_CUDA(cudaMemcpyAsync(h_acc, d_acc, 16, cudaMemcpyDeviceToHost, ex->stream));
+  JT_CUDA(cudaMemcpyAsync(h_acc, d_acc, 16 * ex->n_batch, cudaMemcpyDeviceToHost, ex->stream));
   JT_CUDA(cudaStreamSynchronize(ex->stream));
 }
 
@@ -1251,7 +1258,7 @@ void exec_stats(const jt_exec* ex, jt_exec_stats* out) { *out = ex->stats; }
 void exec_stats_reset(jt_exec* ex) { ex->stats = jt_exec_stats{}; }
 void exec_destroy(jt_exec* ex) { delete ex; }
 
-void amplitude(const jt_plan& plan, jt_dtype dt, int device, double out[2]) {
+void amplitude(const jt_plan& plan, jt_dtype dt, int device, double* out) {
   JT_CUDA(cudaSetDevice(device));
   int64_t bytes = workspace_bytes(plan, dt);
   void* ws = nullptr;

@@ -39,6 +39,9 @@ struct jt_network {
   int64_t n_labels = 0;
   int64_t n_gates = 0;
   bool closed = false;
+  // batch of amplitudes: the bra of an open wire is the d x d
+  // identity with labels (wire label, batch label); fixing the batch label to y gives <y|.
+  std::vector<int64_t> batch_labels;  // one per open wire, in open-wire order
 };
 
 namespace jt {
@@ -59,10 +62,13 @@ struct PlanNode {
 struct jt_plan {
   jt_network net;                       // closed network (copy, with leaf data)
   std::vector<int64_t> path;            // 2 * n_steps SSA ids
-  std::vector<int64_t> sliced;          // sliced labels, loop order (pos 0 outermost)
+  std::vector<int64_t> sliced;          // loop labels, pos 0 outermost: the n_summed sliced
+                                        // (summed) labels, then the network's batch labels
+  int n_summed = 0;                     // sliced labels that are summed (user-visible k)
+  int64_t n_batch = 1;                  // amplitudes per run = d^(batch labels)
   std::vector<jt::PlanNode> nodes;      // n_tensors leaves + n_steps internal; root = back()
   std::unordered_map<int64_t, int> slice_pos;
-  int64_t n_sl = 1;
+  int64_t n_sl = 1;                     // runs = N_sl (summed slices) x n_batch
 };
 
 namespace jt {

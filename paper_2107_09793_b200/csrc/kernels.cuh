@@ -342,15 +342,20 @@ __global__ void advance_slice_kernel(SliceState* st, int k, int d) {
   }
 }
 
+// acc[y] += s (complex128), y = the batch digits of the current run (positions bpos0..bpos0+nq-1,
+// first most significant; y = 0 without a batch), in canonical order.
 template <typename R>
 __global__ void accumulate_kernel(const typename V2<R>::t* __restrict__ root, double* __restrict__ acc,
-                                  double2* __restrict__ slicevals, const SliceState* __restrict__ st) {
+                                  double2* __restrict__ slicevals, const SliceState* __restrict__ st, int bpos0,
+                                  int nq, int d) {
   pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const double re = (double)root[0].x, im = (double)root[0].y;
-    acc[0] += re;
-    acc[1] += im;
+    int64_t y = 0;
+    for (int i = 0; i < nq; ++i) y = y * d + st->digits[bpos0 + i];
+    acc[2 * y] += re;
+    acc[2 * y + 1] += im;
     slicevals[(st->s - st->base) & st->vals_mask] = make_double2(re, im);
   }
 }

@@ -43,6 +43,7 @@ struct TcArgs {
   int32_t rstages;                             // raw shared landing stages (cp.async depth rstages-1)
   int32_t rbytes;                              // bytes of one raw stage (128 rows x 8*2^tkc)
   int32_t acc_bufs;                            // TMEM accumulators (2: epilogue overlaps next tile)
+  int32_t dbg;  // DEBUG (JETB200_K3_DBG): 1 skip stores, 2 skip loads, 4 skip split+STTM, 8 skip MMAs, 16 skip LDTM
   int64_t o_sB[kMaxOuter];                     // outer (row) bit j of B: stride
   int64_t o_kB[4];                             // chunk-index bit j of B: stride
   int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto kwait = [&](uint64_t* bar, uint32_t ph) { tc::mbar_wait(bar, ph); };
   if (tid < 16) {
     int64_t o = 0;
     for (int j = 0; j < p.K - p.tkc; ++j) if ((tid >> j) & 1) o += p.o_kB[j];
@@ -297,8 +299,10 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     auto copy = [&]() {
       unsigned char* raw = R + wst * p.rbytes;
       const float2* srcp = p.B + (cbase + kc_off[cc]);
+      if (!(p.dbg & 2)) {
 #pragma unroll
-      for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], srcp + goff[i]);
+        for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], srcp + goff[i]);
+      }
       if (++wst == RS) wst = 0;
       if (++cc == p.n_kc) {
         cc = 0;
@@ -324,10 +328,16 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       tc::bar_sync(1, 256);  // all producers' copies of item it landed; raw stage of it-1 is free
       if (it + RS - 1 < items) copy();
       cp_async_commit();
-      tc::mbar_wait(&xempty[xs], xph ^ 1);  // TMEM X stage free
+      kwait(&xempty[xs], xph ^ 1);  // TMEM X stage free
       tc::fence_after();
       const unsigned char* raw = R + rst * p.rbytes + row * rb;
       if (++rst == RS) rst = 0;
+      if (p.dbg & 4) {
+        tc::fence_before();
+        tc::mbar_arrive(&xfull[xs]);
+        if (++xs == XS) { xs = 0; xph ^= 1; }
+        continue;
+      }
       float hi[NCOL], lo[NCOL];
 #pragma unroll
       for (int j = 0; j < NCOL / 4; ++j) {
@@ -359,10 +369,10 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     for (int64_t it = 0; it < items; ++it) {
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
-      if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
-      tc::mbar_wait(&xfull[xs], xph);
+      if (c == 0) kwait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
+      kwait(&xfull[xs], xph);
       tc::fence_after();
-      if (leader) {
+      if (leader && !(p.dbg & 8)) {
         const uint32_t d = tmem + (uint32_t)(b * p.Np);
         const uint32_t xh = tmem + xcol0 + (uint32_t)(xs * 2 * KPC), xl = xh + KPC;
         const uint32_t yh = tc::smem_u32(Yhi + c * p.yplane), yl = tc::smem_u32(Ylo + c * p.yplane);
@@ -376,6 +386,9 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
         }
         tc::mma_commit(&xempty[xs]);                     // TMEM X stage free once these finish
         if (c == p.n_kc - 1) tc::mma_commit(&tfull[b]);  // tile accumulated
+      } else if (leader) {
+        tc::mbar_arrive(&xempty[xs]);
+        if (c == p.n_kc - 1) tc::mbar_arrive(&tfull[b]);
       }
       __syncwarp();
       if (c == p.n_kc - 1) ++tt;
@@ -389,17 +402,21 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     for (int64_t tt = 0; tt < my_tiles; ++tt) {
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
-      tc::mbar_wait(&tfull[b], tph);
+      kwait(&tfull[b], tph);
       tc::fence_after();
       const int64_t t = (int64_t)blockIdx.x + tt * gridDim.x;
       float2* out = p.C + (t << (7 + p.tm));
       for (int c0 = 0; c0 < p.Np; c0 += 16) {
         float v[16];
-        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.Np + c0), v);
+        if (p.dbg & 16) {
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        } else {
+          tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.Np + c0), v);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int m = c0 / 2 + j;
-          if (m < nm) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+          if (m < nm && !(p.dbg & 1)) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
         }
       }
       tc::fence_before();

@@ -52,18 +52,36 @@ void network_add_gate(jt_network* net, int32_t k, const int32_t* wires, const do
   net->n_gates++;
 }
 
-void network_close(jt_network* net, const int32_t* x) {
+void network_close(jt_network* net, const int32_t* x, const int32_t* open_wires, int32_t n_open) {
   if (!net || !x) fail(JT_EUSAGE, "jt_network_close: null argument");
   if (net->closed) fail(JT_EVALIDATION, "jt_network_close: already closed");
+  if (n_open < 0 || n_open > net->n_wires || (n_open > 0 && !open_wires))
+    fail(JT_EUSAGE, "jt_network_close_batch: bad open-wire list");
+  std::vector<int> open_idx(net->n_wires, -1);
+  for (int i = 0; i < n_open; ++i) {
+    const int w = open_wires[i];
+    if (w < 0 || w >= net->n_wires) fail(JT_EUSAGE, "jt_network_close_batch: open wire out of range");
+    if (open_idx[w] >= 0) fail(JT_EUSAGE, "jt_network_close_batch: repeated open wire");
+    open_idx[w] = i;
+  }
   for (int w = 0; w < net->n_wires; ++w)
-    if (x[w] < 0 || x[w] >= net->d) fail(JT_EUSAGE, "jt_network_close: digit out of range");
-  for (int w = 0; w < net->n_wires; ++w) {  // <x_w|, rank 1 (l.83)
+    if (open_idx[w] < 0 && (x[w] < 0 || x[w] >= net->d)) fail(JT_EUSAGE, "jt_network_close: digit out of range");
+  net->batch_labels.assign(n_open, -1);
+  for (int i = 0; i < n_open; ++i) net->batch_labels[i] = net->n_labels + i;
+  for (int w = 0; w < net->n_wires; ++w) {
     HostTensor t;
-    t.labels = {net->cur[w]};
-    t.data.assign(net->d, cplx(0, 0));
-    t.data[x[w]] = 1.0;
+    if (open_idx[w] < 0) {  // <x_w|, rank 1 (l.83)
+      t.labels = {net->cur[w]};
+      t.data.assign(net->d, cplx(0, 0));
+      t.data[x[w]] = 1.0;
+    } else {  // identity (wire label, batch label): the batch digit y selects <y|
+      t.labels = {net->cur[w], net->batch_labels[open_idx[w]]};
+      t.data.assign((size_t)net->d * net->d, cplx(0, 0));
+      for (int y = 0; y < net->d; ++y) t.data[(size_t)y * net->d + y] = 1.0;
+    }
     net->tensors.push_back(std::move(t));
   }
+  net->n_labels += n_open;
   net->closed = true;
 }
 
@@ -71,7 +89,9 @@ void network_export(const jt_network* net, const char* path) {
   std::ofstream f(path);
   if (!f) fail(JT_EUSAGE, std::string("cannot open ") + path);
   f << "{\"n_wires\": " << net->n_wires << ", \"d\": " << net->d << ", \"closed\": "
-    << (net->closed ? "true" : "false") << ", \"n_labels\": " << net->n_labels << ", \"tensors\": [";
+    << (net->closed ? "true" : "false") << ", \"n_labels\": " << net->n_labels << ", \"batch_labels\": [";
+  for (size_t i = 0; i < net->batch_labels.size(); ++i) f << (i ? ", " : "") << net->batch_labels[i];
+  f << "], \"tensors\": [";
   for (size_t t = 0; t < net->tensors.size(); ++t) {
     f << (t ? ", " : "") << "[";
     const auto& ls = net->tensors[t].labels;

@@ -22,21 +22,30 @@ void build_plan_tree(jt_plan& plan) {
   std::unordered_map<int64_t, int> carriers;
   for (const auto& t : net.tensors)
     for (int64_t l : t.labels) carriers[l]++;
+  // batch labels sit on exactly one tensor and are fixed in every run
+  std::unordered_set<int64_t> batch(net.batch_labels.begin(), net.batch_labels.end());
   for (auto& kv : carriers)
-    if (kv.second != 2) fail(JT_EVALIDATION, "plan: label " + std::to_string(kv.first) + " is not a bond");
+    if (kv.second != (batch.count(kv.first) ? 1 : 2))
+      fail(JT_EVALIDATION, "plan: label " + std::to_string(kv.first) + " is not a bond");
+  if (plan.n_summed < 0 || plan.n_summed + net.batch_labels.size() != plan.sliced.size())
+    fail(JT_EINTERNAL, "plan: loop labels != sliced + batch labels");
   plan.slice_pos.clear();
   for (size_t p = 0; p < plan.sliced.size(); ++p) {
     int64_t l = plan.sliced[p];
-    if (!carriers.count(l)) fail(JT_EVALIDATION, "plan: sliced label " + std::to_string(l) + " is not a bond");
+    const bool is_batch = (int)p >= plan.n_summed;
+    if (!carriers.count(l) || (batch.count(l) != 0) != is_batch)
+      fail(JT_EVALIDATION, "plan: sliced label " + std::to_string(l) + " is not a bond");
     if (plan.slice_pos.count(l)) fail(JT_EVALIDATION, "plan: duplicate sliced label");
     plan.slice_pos[l] = (int)p;
   }
   if (plan.sliced.size() > 62) fail(JT_EUSAGE, "plan: at most 62 sliced labels");
   const double log2d = std::log2((double)net.d);
   plan.n_sl = 1;
+  plan.n_batch = 1;
   for (size_t p = 0; p < plan.sliced.size(); ++p) {
     if (plan.n_sl > (int64_t(1) << 62) / net.d) fail(JT_EUSAGE, "plan: too many slices");
     plan.n_sl *= net.d;
+    if ((int)p >= plan.n_summed) plan.n_batch *= net.d;
   }
   plan.nodes.assign(nt + ns, PlanNode());
   for (int64_t t = 0; t < nt; ++t) {
@@ -90,8 +99,9 @@ void build_plan_tree(jt_plan& plan) {
 jt_cost plan_cost(const jt_plan& plan) {
   jt_cost c{};
   const int64_t nt = (int64_t)plan.net.tensors.size();
-  c.n_sl = plan.n_sl;
-  c.n_sliced = (int32_t)plan.sliced.size();
+  c.n_sl = plan.n_sl / plan.n_batch;
+  c.n_batch = plan.n_batch;
+  c.n_sliced = (int32_t)plan.n_summed;
   c.n_steps = (int64_t)plan.path.size() / 2;
   const double d = plan.net.d;
   for (int64_t v = nt; v < (int64_t)plan.nodes.size(); ++v) {
@@ -103,8 +113,9 @@ jt_cost plan_cost(const jt_plan& plan) {
     c.max_width = std::max(c.max_width, n.log2size);
     c.bytes_sl += n.bytes8;
   }
-  c.e_flsl = (double)c.n_sl * c.flop_sl;
-  c.e_fltask = c.flop_shared + (double)c.n_sl * (c.flop_sl - c.flop_shared);
+  // per batch of amplitudes: every (slice, bitstring) run is one contraction of the multi-contraction
+  c.e_flsl = (double)plan.n_sl * c.flop_sl;
+  c.e_fltask = c.flop_shared + (double)plan.n_sl * (c.flop_sl - c.flop_shared);
   return c;
 }
 
@@ -154,7 +165,9 @@ void plan_export(const jt_plan* plan, const char* path) {
   for (size_t s = 0; s < plan->path.size() / 2; ++s)
     f << (s ? ", " : "") << "[" << plan->path[2 * s] << ", " << plan->path[2 * s + 1] << "]";
   f << "], \"sliced_labels\": [";
-  for (size_t p = 0; p < plan->sliced.size(); ++p) f << (p ? ", " : "") << plan->sliced[p];
+  for (int p = 0; p < plan->n_summed; ++p) f << (p ? ", " : "") << plan->sliced[p];
+  f << "], \"batch_labels\": [";
+  for (size_t p = plan->n_summed; p < plan->sliced.size(); ++p) f << (p > (size_t)plan->n_summed ? ", " : "") << plan->sliced[p];
   f << "]}\n";
 }
 }  // namespace jt

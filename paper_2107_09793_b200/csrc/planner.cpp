@@ -21,6 +21,7 @@
 #include <queue>
 #include <thread>
 #include <unordered_map>
+#include <unordered_set>
 
 #include "jt_internal.hpp"
 
@@ -540,8 +541,23 @@ Absorbed absorb(const jt_network& net) {
 
 }  // namespace
 
-void greedy_plan(const jt_network& net, const jt_planner_opts& o, std::vector<int64_t>& path,
+void greedy_plan(const jt_network& net0, const jt_planner_opts& o, std::vector<int64_t>& path,
                  std::vector<int64_t>& sliced) {
+  // batch labels (open wires) are fixed in every run: plan on the network without them
+  jt_network stripped;
+  const jt_network* np = &net0;
+  if (!net0.batch_labels.empty()) {
+    stripped = net0;
+    std::unordered_set<int64_t> bl(net0.batch_labels.begin(), net0.batch_labels.end());
+    for (auto& t : stripped.tensors) {
+      std::vector<int64_t> keep;
+      for (int64_t l : t.labels)
+        if (!bl.count(l)) keep.push_back(l);
+      t.labels = keep;
+    }
+    np = &stripped;
+  }
+  const jt_network& net = *np;
   const int64_t nt = (int64_t)net.tensors.size();
   Absorbed ab = absorb(net);
   const int n_leaves = (int)ab.comp_ssa.size();

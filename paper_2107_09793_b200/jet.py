@@ -39,7 +39,7 @@ class PlannerOpts(ctypes.Structure):
 class Cost(ctypes.Structure):
     _fields_ = [("n_sl", c_i64), ("flop_sl", c_dbl), ("flop_shared", c_dbl), ("e_flsl", c_dbl),
                 ("e_fltask", c_dbl), ("exact_reuse", c_dbl), ("prefix", c_dbl), ("max_width", c_dbl),
-                ("bytes_sl", c_dbl), ("n_steps", c_i64), ("n_sliced", c_i32)]
+                ("bytes_sl", c_dbl), ("n_steps", c_i64), ("n_sliced", c_i32), ("n_batch", c_i64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -68,6 +68,7 @@ _sig("jt_version", ctypes.c_char_p, [])
 _sig("jt_network_create", c_i32, [c_i32, c_i32, ctypes.POINTER(c_vp)])
 _sig("jt_network_add_gate", c_i32, [c_vp, c_i32, P_i32, P_dbl])
 _sig("jt_network_close", c_i32, [c_vp, P_i32])
+_sig("jt_network_close_batch", c_i32, [c_vp, P_i32, P_i32, c_i32])
 _sig("jt_network_info", c_i32, [c_vp, P_i64, P_i64])
 _sig("jt_network_export", c_i32, [c_vp, ctypes.c_char_p])
 _sig("jt_network_destroy", None, [c_vp])
@@ -97,7 +98,7 @@ _sig("jt_amplitude", c_i32, [c_vp, c_i32, c_i32, P_dbl])
 _sig("jt_permute", c_i32, [c_i32, c_vp, c_vp, c_i32, P_i32, c_vp])
 
 EXPORTED = ["jt_last_error", "jt_version", "jt_network_create", "jt_network_add_gate", "jt_network_close",
-            "jt_network_info", "jt_network_export", "jt_network_destroy", "jt_plan_create", "jt_plan_greedy",
+            "jt_network_close_batch", "jt_network_info", "jt_network_export", "jt_network_destroy", "jt_plan_create", "jt_plan_greedy",
             "jt_plan_sizes", "jt_plan_get", "jt_plan_cost", "jt_plan_prefix_flop", "jt_plan_export",
             "jt_plan_destroy", "jt_exec_workspace_bytes", "jt_exec_describe", "jt_exec_create", "jt_exec_contract",
             "jt_exec_contract_noreuse", "jt_exec_contract_host", "jt_exec_stats_get",
@@ -139,13 +140,18 @@ class Network:
         _check(_lib.jt_network_create(n_wires, d, ctypes.byref(h)))
         self._h = h
         self.n_wires, self.d = n_wires, d
+        self.open_wires = ()
 
     @classmethod
-    def from_circuit(cls, circuit, bitstring):
+    def from_circuit(cls, circuit, bitstring, open_wires=None):
+        """open_wires: batch of amplitudes over these wires (jt_network_close_batch)."""
         net = cls(circuit.n_wires, circuit.d)
         for g in circuit.gates:
             net.add_gate(g.wires, g.u)
-        net.close(bitstring)
+        if open_wires is None:
+            net.close(bitstring)
+        else:
+            net.close_batch(bitstring, open_wires)
         return net
 
     def add_gate(self, wires, u):
@@ -157,6 +163,13 @@ class Network:
     def close(self, bits):
         b, bp = _i32(list(bits))
         _check(_lib.jt_network_close(self._h, bp))
+        self.open_wires = ()
+
+    def close_batch(self, bits, open_wires):
+        b, bp = _i32(list(bits))
+        o, op = _i32(list(open_wires))
+        _check(_lib.jt_network_close_batch(self._h, bp, op, len(o)))
+        self.open_wires = tuple(int(w) for w in open_wires)
 
     def info(self):
         nt, nl = c_i64(), c_i64()
@@ -286,9 +299,11 @@ class Exec:
         return None
 
     def contract_host(self, begin, end):
-        out = np.zeros(2, dtype=np.float64)
+        """Sum of runs [begin, end) on the host: a complex, or n_batch complex for batch plans."""
+        nb = self.plan.cost()["n_batch"]
+        out = np.zeros(2 * nb, dtype=np.float64)
         _check(_lib.jt_exec_contract_host(self._h, begin, end, out.ctypes.data_as(P_dbl)))
-        return complex(out[0], out[1])
+        return complex(out[0], out[1]) if nb == 1 and not self.plan.net.open_wires else out.view(np.complex128)
 
     def stats(self):
         s = ExecStats()
@@ -328,9 +343,11 @@ def debug_emulate_host(plan, begin, end, dtype="c128", reuse=True):
 
 
 def amplitude(plan, dtype="c64", device=0):
-    out = np.zeros(2, dtype=np.float64)
+    """<x|U|0> (complex), or the batch of n_batch amplitudes (complex128 array, y-indexed)."""
+    nb = plan.cost()["n_batch"]
+    out = np.zeros(2 * nb, dtype=np.float64)
     _check(_lib.jt_amplitude(plan._h, _DT[dtype], device, out.ctypes.data_as(P_dbl)))
-    return complex(out[0], out[1])
+    return complex(out[0], out[1]) if nb == 1 and not plan.net.open_wires else out.view(np.complex128)
 
 
 def permute(src, perm, out=None):

@@ -20,7 +20,7 @@ def shard_range(n_sl: int, rank: int, world: int):
 
 
 def allreduce_amplitude(acc, group=None):
-    """One SUM all-reduce of the 2-double accumulator (16 bytes per amplitude)."""
+    """One SUM all-reduce of the accumulator (16 bytes per amplitude of the batch)."""
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
@@ -32,7 +32,9 @@ def run_amplitude(plan, dtype="c64", exec_=None, slices=None):
     """Amplitude <x|U|0> = sum over all slices, sharded over the process group.
 
     Each rank contracts its block on its own GPU (current CUDA device) into a device
-    complex128 accumulator, then one all-reduce; returns (amplitude, per-rank info)."""
+    complex128 accumulator, then one all-reduce; returns (amplitude, per-rank info).  For a
+    batch plan (open wires) the runs are N_sl x n_batch and the result is the y-indexed
+    complex128 array of the batch's amplitudes."""
     import torch
     import torch.distributed as dist
 
@@ -40,15 +42,19 @@ def run_amplitude(plan, dtype="c64", exec_=None, slices=None):
 
     world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank() if world > 1 else 0
-    n_sl = plan.cost()["n_sl"]
-    b, e = slices if slices is not None else shard_range(n_sl, rank, world)
+    c = plan.cost()
+    nb = c["n_batch"]
+    b, e = slices if slices is not None else shard_range(c["n_sl"] * nb, rank, world)
     ex = exec_ if exec_ is not None else jet.Exec(plan, dtype)
-    acc = torch.zeros(2, dtype=torch.float64, device=ex.device)
+    acc = torch.zeros(2 * nb, dtype=torch.float64, device=ex.device)
     if e > b:
         ex.contract(b, e, acc)
     allreduce_amplitude(acc)
     a = acc.cpu().numpy()
-    return complex(a[0], a[1]), {"rank": rank, "world": world, "range": (b, e)}
+    info = {"rank": rank, "world": world, "range": (b, e)}
+    if plan.net.open_wires:
+        return a.view(np.complex128).copy(), info
+    return complex(a[0], a[1]), info
 
 
 def host_shard_sum(values_per_rank):

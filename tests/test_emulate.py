@@ -39,6 +39,40 @@ def test_emulated_descriptors_match_oracle_c1(jet, k):
         assert np.array_equal(v64, off)
 
 
+@pytest.mark.parametrize("open_wires,k", [([4], 2), ([7, 2], 0), ([8, 0, 3], 3), (list(range(9)), 1)])
+def test_emulated_batch_matches_oracle_c1(jet, open_wires, k):
+    """f1 batch of amplitudes: every run r = sigma * n_batch + y of a batch plan reproduces the
+    oracle's s_sigma of the y-th batch bitstring; reuse on/off bitwise identical."""
+    circ, _ = workload("C1")
+    bits = random_bitstring(9, 2, 77)
+    net = jet.Network.from_circuit(circ, bits, open_wires=open_wires)
+    plan = jet.Plan.greedy(net, seed=3, trials=8, n_sliced=k)
+    c = plan.cost()
+    nb = 2 ** len(open_wires)
+    assert c["n_batch"] == nb and c["n_sl"] == 2 ** k and len(plan.sliced_labels) == k
+    n = c["n_sl"] * nb
+    ref = np.array(contract.batch_run_values(circ, bits, open_wires, plan.ssa_path, plan.sliced_labels, range(n)))
+    v = jet.debug_emulate_host(plan, 0, n, "c128")
+    assert np.max(np.abs(v - ref)) <= 1e-12 * np.max(np.abs(ref))
+    v64 = jet.debug_emulate_host(plan, 0, n, "c64")
+    assert np.max(np.abs(v64 - ref)) <= 1e-5 * np.max(np.abs(ref))
+    assert np.array_equal(v64, jet.debug_emulate_host(plan, 0, n, "c64", reuse=False))
+    # the prefix cache recomputes only what depends on the changed digits: executed FLOP over
+    # the batch is below N_sl * n_batch independent contractions
+    assert plan.prefix_flop(0, n) < c["e_flsl"]
+
+
+def test_batch_validation(jet):
+    circ, bits = workload("C1")
+    for bad in ([9], [-1], [3, 3]):
+        net = jet.Network(9, 2)
+        for g in circ.gates:
+            net.add_gate(g.wires, g.u)
+        with pytest.raises(jet.JetError) as e:
+            net.close_batch(bits, bad)
+        assert e.value.code == 2
+
+
 def test_emulated_descriptors_match_oracle_gbs(jet):
     circ = generate_gbs(2, 2, 1, 0.5, 4, seed=2)
     for seed in range(3):

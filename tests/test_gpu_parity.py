@@ -332,3 +332,54 @@ def test_k3g_streamed_operands_parity(jet, c2_plan, monkeypatch):
     for i, r in zip(idx, ref):
         v = ex.contract(i, i + 1, acc, slice_values=True)[0]
         assert abs(v - r) <= 1e-4 * abs(r), (i, v, r)
+
+
+# ------------------------------------------------------------- f1 batches of amplitudes
+def run_batch(jet, plan, dtype, ranges):
+    import torch
+
+    c = plan.cost()
+    ex = jet.Exec(plan, dtype)
+    acc = torch.zeros(2 * c["n_batch"], dtype=torch.float64, device="cuda")
+    vals = [ex.contract(b, e, acc, slice_values=True) for b, e in ranges]
+    torch.cuda.synchronize()
+    return acc.cpu().numpy().view(np.complex128), np.concatenate(vals), ex
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_c1_batch_all_512_amplitudes(jet, dtype):
+    """Every wire open: one batch plan yields all 512 amplitudes of C1, each against the state
+    vector and the oracle (f1); split ranges agree with one range."""
+    circ, _ = workload("C1")
+    psi = statevector.final_state(circ).reshape(-1)
+    bits = [0] * 9
+    net = jet.Network.from_circuit(circ, bits, open_wires=list(range(9)))
+    plan = jet.Plan.greedy(net, seed=2, trials=16, n_sliced=2)
+    n = plan.cost()["n_sl"] * 512
+    amps, vals, ex = run_batch(jet, plan, dtype, [(0, 700), (700, n)])
+    ref = np.array(contract.batch_amplitudes(circ, bits, list(range(9)), plan.ssa_path, plan.sliced_labels))
+    assert np.max(np.abs(ref - psi)) < 1e-12
+    assert np.max(np.abs(amps - ref) / np.abs(ref)) < TOL[dtype]
+    assert ex.stats()["flop_executed"] == plan.prefix_flop(0, n)
+    amps1 = jet.amplitude(plan, dtype)
+    assert np.max(np.abs(amps1 - ref) / np.abs(ref)) < TOL[dtype]
+
+
+def test_c2_batch_sampled_runs(jet):
+    """Sycamore-53 m=10 batch over 4 open wires (16 bitstrings) x 2^6 slices: sampled runs
+    s_(sigma, y) against the oracle, c64 on the tensor-core path."""
+    circ, bits = workload("C2")
+    ow = [3, 17, 30, 52]
+    net = jet.Network.from_circuit(circ, bits, open_wires=ow)
+    plan = jet.Plan.greedy(net, seed=1, trials=128, n_sliced=6, bytes_weight=5.0)
+    n = plan.cost()["n_sl"] * 16
+    amps, vals, ex = run_batch(jet, plan, "c64", [(0, n)])
+    sample = [0, 1, 15, 16, 17, 500, n - 1]
+    ref = contract.batch_run_values(circ, bits, ow, plan.ssa_path, plan.sliced_labels, sample)
+    for r, want in zip(sample, ref):
+        assert abs(vals[r] - want) <= 1e-4 * abs(want)
+    # amplitudes are the per-bitstring sums of the runs (canonical order, complex128)
+    for y in range(16):
+        assert abs(amps[y] - sum(vals[y::16])) <= 1e-12 * abs(amps[y])
+    # prefix cache: nodes off the bra-attached subtrees are shared across the 16 bitstrings
+    assert ex.stats()["flop_executed"] == plan.prefix_flop(0, n) < plan.cost()["e_flsl"]

@@ -131,6 +131,30 @@ def test_c1_all_amplitudes_vs_statevector(c1):
     assert abs(tot - 1.0) < 1e-12                                        # P3
 
 
+def test_batch_amplitudes_vs_statevector(c1):
+    """f1 batch of amplitudes: the y-th amplitude of the batch equals the
+    state-vector entry of the y-th batch bitstring (open_wires[0] most significant), and the
+    per-run values s_(sigma, y) sum over sigma to it (Eq. sliced_sum per bitstring)."""
+    circ, psi = c1
+    base = [1, 0, 1, 1, 0, 0, 1, 0, 1]
+    p = path.greedy_path(build_network(circ, base))
+    for open_wires in ([4], [7, 2], [8, 0, 3], list(range(9))):
+        amps = contract.batch_amplitudes(circ, base, open_wires, p)
+        assert len(amps) == 2 ** len(open_wires)
+        for y, a in enumerate(amps):
+            x = list(base)
+            for i, w in enumerate(open_wires):
+                x[w] = (y >> (len(open_wires) - 1 - i)) & 1
+            assert abs(a - psi[tuple(x)]) < 1e-12
+    net = build_network(circ, base)
+    sliced = sorted(l for l, ts in net.carriers().items() if 9 <= l < 40)[:3]
+    open_wires = [5, 1]
+    runs = contract.batch_run_values(circ, base, open_wires, p, sliced, range(8 * 4))
+    amps = contract.batch_amplitudes(circ, base, open_wires, p)
+    for y in range(4):
+        assert abs(sum(runs[s * 4 + y] for s in range(8)) - amps[y]) < 1e-12
+
+
 def test_statevector_norm_sycamore_grid():
     for seed in (2, 3):
         psi = statevector.final_state(grid_rqc(3, 4, 6, seed))
