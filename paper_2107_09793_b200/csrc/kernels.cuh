@@ -93,6 +93,23 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+// cp.async.wait_group with a run-time count (0..11), for rings sized at launch
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::); break;
+    case 3: asm volatile("cp.async.wait_group 3;\n" ::); break;
+    case 4: asm volatile("cp.async.wait_group 4;\n" ::); break;
+    case 5: asm volatile("cp.async.wait_group 5;\n" ::); break;
+    case 6: asm volatile("cp.async.wait_group 6;\n" ::); break;
+    case 7: asm volatile("cp.async.wait_group 7;\n" ::); break;
+    case 8: asm volatile("cp.async.wait_group 8;\n" ::); break;
+    case 9: asm volatile("cp.async.wait_group 9;\n" ::); break;
+    case 10: asm volatile("cp.async.wait_group 10;\n" ::); break;
+    default: asm volatile("cp.async.wait_group 11;\n" ::); break;
+  }
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 

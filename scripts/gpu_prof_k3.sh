@@ -1,5 +1,7 @@
 #!/bin/bash
+# K3 stage split + one full ncu capture of the top C3 contraction launch
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 300 python scripts/bench_permute.py > gpurun_out/permute.log 2>&1
-TAG=k3v2 SKIPS="1336 1343" bash scripts/gpu_ncu_ids.sh
+TAG=${TAG:-k3}
+timeout 900 python scripts/k3_split.py C3 6 ${MODES:-0,32,3,35,31,63} > gpurun_out/k3_split_$TAG.log 2>&1
+CFG=C3 SPS=2 TAG=$TAG timeout 1500 bash scripts/gpu_prof_top.sh
