@@ -51,8 +51,7 @@ struct TcArgs {
                                                //   instead of 3); the epilogue adds the two column halves
   int32_t nw;                                  // accumulator width in TMEM columns (Np, or 2*Np with ycat)
   int32_t dbg;  // DEBUG (JETB200_K3_DBG): 1 skip stores, 2 skip loads, 4 skip split+STTM, 8 skip MMAs, 16 skip LDTM,
-                //   32 one xfull/tempty arrival per warp, 64 no fence.proxy.async, 128 one MMA per K step
-                //   (64/128: timing only)
+                //   32 one xfull/tempty arrival per warp, 64 no fence.proxy.async (timing only)
   unsigned long long* trace;  // DEBUG (JETB200_K3_TRACE): clock64 stamps of CTA 0, items [kTrBegin, +64)
   int64_t o_sB[kMaxOuter];                     // outer (row) bit j of B: stride
   int64_t o_kB[4];                             // chunk-index bit j of B: stride
@@ -79,10 +78,14 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)layout << 61;
   return d;
 }
+// The MMA / commit wrappers are executed by the WHOLE issuing warp with warp-uniform operands;
+// elect.sync inside the asm picks the one lane that issues.  (Issuing from a divergent
+// single-lane branch costs ~150 cycles per tcgen05.mma; warp-uniform issue ~20-60, i.e. the
+// tensor core's own rate -- measured by scripts/mma_probe.cu.)
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
@@ -118,15 +121,70 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
+// All MMAs of one item in ONE asm block with one elect.sync: every operand is moved to the
+// uniform datapath before the first tcgen05.mma, so the MMAs issue back to back (separate asm
+// statements interleave an R2UR/ELECT round trip with every MMA, ~100 cycles each).
+// K3 ycat: per K step s, D += X_s * Ycat_s (A from shared memory) and D += Xlo_s * Ycat_s (A from
+// tensor memory); `acc` enables accumulation for the first MMA (all later ones accumulate).
+template <int KS>
+__device__ __forceinline__ void mma_item_ycat(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[KS],
+                                              const uint64_t (&dy)[KS], const uint32_t (&xl)[KS]);
+#define JT_MMA_SS(D, A, B, P) "@e tcgen05.mma.cta_group::1.kind::tf32 [" D "], " A ", " B ", %1, " P ";\n\t"
+#define JT_MMA_TS(D, A, B) "@e tcgen05.mma.cta_group::1.kind::tf32 [" D "], [" A "], " B ", %1, 1;\n\t"
+template <>
+__device__ __forceinline__ void mma_item_ycat<1>(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[1],
+                                                 const uint64_t (&dy)[1], const uint32_t (&xl)[1]) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      JT_MMA_SS("%0", "%3", "%4", "p") JT_MMA_TS("%0", "%5", "%4") "}\n" ::"r"(d),
+      "r"(idesc), "r"(acc), "l"(dx[0]), "l"(dy[0]), "r"(xl[0])
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void mma_item_ycat<2>(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[2],
+                                                 const uint64_t (&dy)[2], const uint32_t (&xl)[2]) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      JT_MMA_SS("%0", "%3", "%5", "p") JT_MMA_TS("%0", "%7", "%5")
+      JT_MMA_SS("%0", "%4", "%6", "1") JT_MMA_TS("%0", "%8", "%6") "}\n" ::"r"(d),
+      "r"(idesc), "r"(acc), "l"(dx[0]), "l"(dx[1]), "l"(dy[0]), "l"(dy[1]), "r"(xl[0]), "r"(xl[1])
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void mma_item_ycat<4>(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[4],
+                                                 const uint64_t (&dy)[4], const uint32_t (&xl)[4]) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      JT_MMA_SS("%0", "%3", "%7", "p") JT_MMA_TS("%0", "%11", "%7")
+      JT_MMA_SS("%0", "%4", "%8", "1") JT_MMA_TS("%0", "%12", "%8")
+      JT_MMA_SS("%0", "%5", "%9", "1") JT_MMA_TS("%0", "%13", "%9")
+      JT_MMA_SS("%0", "%6", "%10", "1") JT_MMA_TS("%0", "%14", "%10") "}\n" ::"r"(d),
+      "r"(idesc), "r"(acc), "l"(dx[0]), "l"(dx[1]), "l"(dx[2]), "l"(dx[3]), "l"(dy[0]), "l"(dy[1]), "l"(dy[2]),
+      "l"(dy[3]), "r"(xl[0]), "r"(xl[1]), "r"(xl[2]), "r"(xl[3])
+      : "memory");
+}
+// Classic 3xTF32 per K step (wide N): D += X*Yhi + X*Ylo + Xlo*Yhi, one K step per asm block.
+__device__ __forceinline__ void mma_step3(uint32_t d, uint32_t idesc, uint32_t acc, uint64_t dx, uint64_t dyh,
+                                          uint64_t dyl, uint32_t xl) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      JT_MMA_SS("%0", "%3", "%4", "p") JT_MMA_SS("%0", "%3", "%5", "1") JT_MMA_TS("%0", "%6", "%4") "}\n" ::"r"(d),
+      "r"(idesc), "r"(acc), "l"(dx), "l"(dyh), "l"(dyl), "r"(xl)
+      : "memory");
+}
+#undef JT_MMA_SS
+#undef JT_MMA_TS
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -344,8 +402,11 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     int64_t ct = 0, cbase = tile_base(0);
     int cc = 0, wst = 0;  // wst = ring stage the next copy lands in
     uint32_t wph = 0;     // use parity of that stage
+    int64_t trit = -1;
+    const int trr = warp == 4 ? 0 : (warp == 11 ? 1 : -1);
     auto copy = [&]() {
       kwait(&xempty[wst], wph ^ 1);  // the stage's previous item is consumed by the MMAs
+      if (trr >= 0 && trit >= 0) tr(trr, trit, 6);
       unsigned char* raw = R + wst * p.rbytes;
       const char* src = Bb + (cbase + kc_off[cc]);
       if (!(p.dbg & 2)) {
@@ -366,7 +427,6 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     int rst = 0;  // ring stage of item it
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     const int sw = (row >> SWS) & (CHUNKS - 1);
-    const int trr = warp == 4 ? 0 : (warp == 11 ? 1 : -1);
     for (int64_t it = 0; it < items; ++it) {
       if (trr >= 0) tr(trr, it, 0);
       cp_async_wait_dyn(D - 1);  // own copies of item it landed (D groups ahead were committed)
@@ -399,13 +459,13 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       }
       if (trr >= 0) tr(trr, it, 4);
       if (++rst == S) rst = 0;
+      trit = it;
       if (it + D < items) copy();
       cp_async_commit();
       if (trr >= 0) tr(trr, it, 5);
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
-    const bool leader = lane == 0;
     int64_t tt = 0;
     const int S = p.xstages;
     int xs = 0, c = 0;
@@ -419,31 +479,32 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       kwait(&xfull[xs], xph);
       tr(2, it, 2);
       tc::fence_after();
-      if (leader && !(p.dbg & 8)) {
+      if (!(p.dbg & 8)) {  // whole warp: the wrappers elect the issuing lane
         const uint32_t d = tmem + (uint32_t)(b * p.nw);
         const uint32_t xl = tmem + xcol0 + (uint32_t)(xs * KPC);
         const uint32_t xr = tc::smem_u32(R + xs * p.rbytes);
         const uint32_t yh = tc::smem_u32(Yhi + c * p.yplane), yl = tc::smem_u32(Ylo + c * p.yplane);
+        constexpr int KS = KPC / 8;
+        const uint32_t acc = c > 0 ? 1u : 0u;
+        uint64_t dx[KS], dy[KS];
+        uint32_t xls[KS];
 #pragma unroll
-        for (int ks = 0; ks < KPC / 8; ++ks) {
-          const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
-          const uint64_t dx = tc::sdesc(xr + ks * 32, 16, 8 * RB, ALAYOUT);
-          const uint64_t dyh = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
-          if (p.ycat) {  // D[:, 0:2Np] += hi*[Yhi|Ylo] + lo*[Yhi|Ylo]
-            tc::mma_tf32(d, dx, dyh, p.idesc, acc);
-            if (p.dbg & 128) continue;  // DEBUG timing: one MMA per K step
-            tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
-          } else {  // D += hi*Yhi + hi*Ylo + lo*Yhi
-            const uint64_t dyl = tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout);
-            tc::mma_tf32(d, dx, dyh, p.idesc, acc);
-            if (p.dbg & 128) continue;
-            tc::mma_tf32(d, dx, dyl, p.idesc, 1u);
-            tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
-          }
+        for (int ks = 0; ks < KS; ++ks) {
+          dx[ks] = tc::sdesc(xr + ks * 32, 16, 8 * RB, ALAYOUT);
+          dy[ks] = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
+          xls[ks] = xl + ks * 8;
+        }
+        if (p.ycat) {  // D[:, 0:2Np] += (hi + lo) * [Yhi|Ylo]
+          tc::mma_item_ycat<KS>(d, p.idesc, acc, dx, dy, xls);
+        } else {  // D += hi*Yhi + hi*Ylo + lo*Yhi
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks)
+            tc::mma_step3(d, p.idesc, (c > 0 || ks > 0) ? 1u : 0u, dx[ks], dy[ks],
+                          tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout), xls[ks]);
         }
         tc::mma_commit(&xempty[xs]);                     // ring stage free once these finish
         if (c == p.n_kc - 1) tc::mma_commit(&tfull[b]);  // tile accumulated
-      } else if (leader) {
+      } else if (lane == 0) {
         tc::mbar_arrive(&xempty[xs]);
         if (c == p.n_kc - 1) tc::mbar_arrive(&tfull[b]);
       }

@@ -20,7 +20,7 @@ ex = jet.Exec(plan, "c64", stream=stream)
 acc = torch.zeros(2, dtype=torch.float64, device="cuda")
 ex.contract(0, 1, acc)
 torch.cuda.synchronize()
-names = {0: ["start", "landed", "split", "sttm", "arrive", "copied"], 1: ["start", "landed", "split", "sttm", "arrive", "copied"],
+names = {0: ["start", "landed", "split", "sttm", "arrive", "xempty", "copied"], 1: ["start", "landed", "split", "sttm", "arrive", "xempty", "copied"],
          2: ["start", "tempty", "xfull", "issued"], 3: ["start", "tfull", "stored", "arrived"]}
 for i in cands:
     path = f"/tmp/k3trace_{i}.bin"
@@ -34,6 +34,8 @@ for i in cands:
     for role in range(4):
         ks = names[role]
         st = t[role, :, :len(ks)]
+        if role < 2:  # slot 6 (xempty) sits between slots 4 and 5
+            st = t[role][:, [0, 1, 2, 3, 4, 6, 5]]
         ok = st[:, 0] > 0
         st = st[ok]
         if len(st) < 3:
