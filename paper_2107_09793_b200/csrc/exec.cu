@@ -156,24 +156,17 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   const int tkc = swz ? 4 : kt;
   const int n_kc = 1 << (kt - tkc);
   const int Kpc = 2 << tkc, Np = 2 << tm;
-  // ring stages = raw shared stage (the hi operand) + Kpc TMEM lo columns; TMEM accumulators:
-  // acc_bufs buffers (2: the epilogue drains one while the next tile accumulates) of nw columns.
-  // ycat (Y planes [Yhi | Ylo] along N, nw = 2 Np) takes 2 MMAs per K step instead of 3; the
-  // tensor core's time per MMA hardly depends on N up to 128, so it needs 2/3 of the MMA time.
-  // Used when 2 buffers and >= 4 stages still fit.  JETB200_K3_YCAT=0 (debug) disables it.
-  const int rbytes = 128 * (8 << tkc);
-  bool ycat = 2 * (2 * Np) + 4 * Kpc <= 512;
-  if (const char* e = std::getenv("JETB200_K3_YCAT")) ycat = ycat && e[0] != '0';
-  const int nw = ycat ? 2 * Np : Np;
-  const int yplane = ycat ? 2 * Np * Kpc * 4 : Np * Kpc * 4;
-  const int64_t ybytes = ((ycat ? 1LL : 2LL) * n_kc * yplane + 1023) / 1024 * 1024;
-  const int64_t budget = 220 * 1024 - 1024 - ybytes;
-  const int smem_stages = (int)std::min<int64_t>(kTcMaxStages, budget / rbytes);
-  const int acc_bufs = (2 * nw + 3 * Kpc <= 512) ? 2 : 1;
-  const int xstages = std::min(smem_stages, (512 - acc_bufs * nw) / Kpc);
+  const int yplane = Np * Kpc * 4;
+  // TMEM: accumulators (2 when they fit beside >= 2 X stages) + X stages of 2*Kpc columns
+  int acc_bufs = (2 * Np + 2 * 2 * Kpc <= 512) ? 2 : 1;
+  int xstages = std::min(4, (512 - acc_bufs * Np) / (2 * Kpc));
   if (xstages < 2) return false;
-  const int rstages = std::max(1, xstages - kTcLag);
-  const int64_t smem = ybytes + (int64_t)xstages * rbytes + 1024;
+  const int rbytes = 128 * (8 << tkc);
+  const int64_t ybytes = 2LL * n_kc * yplane;
+  const int64_t budget = 220 * 1024 - 1024 - ybytes;
+  const int rstages = (int)std::min<int64_t>(6, budget / rbytes);
+  if (rstages < 2) return false;
+  const int64_t smem = ybytes + (int64_t)rstages * rbytes + 1024;
   std::sort(M.begin(), M.end());
   std::sort(N.begin(), N.end());
   std::sort(K.begin(), K.end());
@@ -197,28 +190,20 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   t.rstages = rstages;
   t.rbytes = rbytes;
   t.acc_bufs = acc_bufs;
-  t.ycat = ycat ? 1 : 0;
-  t.nw = nw;
-  t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(nw >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t cols = 32;
-  while ((int)cols < acc_bufs * nw + xstages * Kpc) cols <<= 1;
+  while ((int)cols < acc_bufs * Np + xstages * 2 * Kpc) cols <<= 1;
   t.tmem_cols = cols;
-  // chunk-tile bits in B-stride order with their byte offsets in the raw landing stage, the UMMA
-  // K-major swizzled layout (SW128/64/32 for rows of 128/64/32 B): row n, complex k at
-  // n*rb + ((k>>1) ^ ((n >> (4-tkc)) & (chunks-1)))*16 + (k&1)*8 -- XOR-combinable per bit
-  const int rb = 8 << tkc, lg_chunks = tkc - 1, sws = 4 - tkc;
-  std::vector<std::tuple<int64_t, int32_t, int>> tb;  // (B stride, raw offset, role: row bit i / 7 + K bit i)
-  for (int i = 0; i < 7; ++i)
-    tb.push_back({sb[tN[i]], (rb << i) ^ (i >= sws && i < sws + lg_chunks ? (16 << (i - sws)) : 0), i});
-  for (int i = 0; i < tkc; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : (16 << (i - 1)), 7 + i});
+  // chunk-tile bits in B-stride order with their byte offsets in the raw landing stage:
+  // row n, complex k at n*rb + ((k>>1) ^ (n & (chunks-1)))*16 + (k&1)*8 (XOR-combinable)
+  const int rb = 8 << tkc, lg_chunks = tkc - 1;
+  std::vector<std::pair<int64_t, int32_t>> tb;
+  for (int i = 0; i < 7; ++i) tb.push_back({sb[tN[i]], (rb << i) ^ (i < lg_chunks ? (16 << i) : 0)});
+  for (int i = 0; i < tkc; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : (16 << (i - 1))});
   std::sort(tb.begin(), tb.end());
   for (size_t j = 0; j < tb.size(); ++j) {
-    t.gX[j] = std::get<0>(tb[j]);
-    t.sX[j] = std::get<1>(tb[j]);
-    const int role = std::get<2>(tb[j]);
-    if (role == 5) t.wpos[0] = (int)j;
-    if (role == 6) t.wpos[1] = (int)j;
-    if (role == 7 + tkc - 1) t.wpos[2] = (int)j;
+    t.gX[j] = tb[j].first;
+    t.sX[j] = tb[j].second;
   }
   for (int j = 0; j < kt - tkc; ++j) t.o_kB[j] = sb[K[tkc + j].second];
   for (int i = 0; i < tm; ++i) t.aM[i] = sa[M[i].second];
@@ -747,40 +732,6 @@ void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector
   const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
   const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
   float2* C = reinterpret_cast<float2*>(ws + off[2].first);
-  // the producers' gather mapping (warp-local shares, gett_tc_kernel): every element of the
-  // chunk tile is copied exactly once, by the warp that converts its row / chunk half, to the
-  // raw-stage slot of its (row, k) and from B's offset of (row, k)
-  {
-    const int rb = 8 << p.tkc, chunks = rb >> 4, per = 1 << (p.tkc - 1);
-    std::vector<int> seen((size_t)128 << p.tkc, 0);
-    for (int w = 0; w < 8; ++w) {
-      const int quarter = w & 3, half = w >> 2;
-      const int wbits[3] = {quarter & 1, quarter >> 1, half};
-      for (int lane = 0; lane < 32; ++lane)
-        for (int i = 0; i < per; ++i) {
-          int sub = lane + i * 32, e = 0, sbit = 0;
-          for (int j = 0; j < p.nX; ++j) {
-            int bit;
-            if (j == p.wpos[0]) bit = wbits[0];
-            else if (j == p.wpos[1]) bit = wbits[1];
-            else if (j == p.wpos[2]) bit = wbits[2];
-            else bit = (sub >> sbit++) & 1;
-            e |= bit << j;
-          }
-          int64_t g = 0;
-          int32_t so = 0;
-          for (int j = 0; j < p.nX; ++j)
-            if ((e >> j) & 1) { g += p.gX[j]; so ^= p.sX[j]; }
-          const int n = so / rb, wb = so % rb;
-          const int chunk = (wb >> 4) ^ ((n >> (4 - p.tkc)) & (chunks - 1)), k = 2 * chunk + ((wb >> 3) & 1);
-          int64_t want = 0;
-          for (int b = 0; b < 7; ++b) if ((n >> b) & 1) want += en.tcB_n[b];
-          for (int b = 0; b < p.tkc; ++b) if ((k >> b) & 1) want += en.tcB_k[b];
-          if (n >> 5 != quarter || ((chunk >> (p.tkc - 2)) & 1) != half || g != want || seen[(size_t)n * (1 << p.tkc) + k]++)
-            fail(JT_EINTERNAL, "K3 producer gather mapping");
-        }
-    }
-  }
   const int nm = 1 << p.tm, nk = 1 << p.K;
   std::vector<float2> a((size_t)nm * nk);
   for (int m = 0; m < nm; ++m)
@@ -983,12 +934,8 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   set_smem_attrs();
   int n_sm = 148;
   JT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
-  const char* kdbg = std::getenv("JETB200_K3_DBG");  // DEBUG: K3 roofline split (skip stores / loads)
   for (ExecNode& en : L.order) {
     int nb = 1;
-    if (kdbg) en.tc.dbg = std::atoi(kdbg);
-    if (const char* lag = std::getenv("JETB200_K3_LAG"))  // DEBUG: gather distance = stages - lag
-      if (en.kind == 1) en.tc.rstages = std::max(1, std::min(en.tc.xstages, en.tc.xstages - std::atoi(lag)));
     if (en.kind == 2) {
       en.grid_x = std::min<int64_t>(en.tcg.n_tiles, n_sm);  // one CTA per SM (512 TMEM columns)
       continue;
@@ -1287,26 +1234,6 @@ void debug_time_node(jt_exec* ex, int64_t idx, int reps, double* ms_out, double*
     else launch_node<double>(ex, en);
   };
   one();
-  // DEBUG: one traced K3 launch (clock64 stamps of CTA 0, see TcArgs::trace) written as raw
-  // uint64 [role 4][item 64][slot 8] to the file named by JETB200_K3_TRACE
-  if (const char* tp = std::getenv("JETB200_K3_TRACE"))
-    if (en.kind == 1) {
-      const size_t nb = 4 * 64 * 8 * sizeof(unsigned long long);
-      unsigned long long* dtr = nullptr;
-      JT_CUDA(cudaMalloc(&dtr, nb));
-      JT_CUDA(cudaMemset(dtr, 0, nb));
-      en.tc.trace = dtr;
-      one();
-      en.tc.trace = nullptr;
-      JT_CUDA(cudaStreamSynchronize(ex->stream));
-      std::vector<unsigned long long> h(nb / 8);
-      JT_CUDA(cudaMemcpy(h.data(), dtr, nb, cudaMemcpyDeviceToHost));
-      JT_CUDA(cudaFree(dtr));
-      if (FILE* f = std::fopen(tp, "wb")) {
-        std::fwrite(h.data(), 1, nb, f);
-        std::fclose(f);
-      }
-    }
   JT_CUDA(cudaEventRecord(a, ex->stream));
   for (int r = 0; r < reps; ++r) one();
   JT_CUDA(cudaEventRecord(b, ex->stream));

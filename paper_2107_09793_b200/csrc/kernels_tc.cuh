@@ -26,10 +26,7 @@
 
 namespace jt {
 
-constexpr int kTcMaxTile = 12;    // 7 row bits + up to 5 K bits per chunk
-constexpr int kTcMaxStages = 12;  // K3 ring stages (raw smem + TMEM lo)
-constexpr int kTcLag = 3;
-constexpr int kTrBegin = 200;  // first traced item (steady state)         // K3 ring stages between the item being gathered and the oldest in use
+constexpr int kTcMaxTile = 12;  // 7 row bits + up to 5 K bits per chunk
 
 struct TcArgs {
   const float2* A;  // small operand (all bits in the tile)
@@ -42,23 +39,14 @@ struct TcArgs {
   int32_t xbuf, yplane;                        // bytes of one X buffer / one Y chunk plane (hi or lo)
   uint32_t idesc;                              // kind::tf32, M=128, N=Np, F32 accumulate, K-major
   uint32_t tmem_cols;                          // 2 accumulators of Np columns
-  int32_t xstages;                             // ring stages (raw shared stage + Kpc TMEM lo columns)
-  int32_t rstages;                             // items gathered ahead (<= xstages)
+  int32_t xstages;                             // TMEM X stages (hi|lo, 2*Kpc columns each)
+  int32_t rstages;                             // raw shared landing stages (cp.async depth rstages-1)
   int32_t rbytes;                              // bytes of one raw stage (128 rows x 8*2^tkc)
-  int32_t acc_bufs;                            // TMEM accumulator buffers (2: epilogue overlaps next tile)
-  int32_t ycat;                                // 1: Y planes hold [Yhi | Ylo] along N (2*Np rows): per K step
-                                               //   D[:, 0:2Np] += X*[Yhi|Ylo] and += Xlo*[Yhi|Ylo] (2 MMAs
-                                               //   instead of 3); the epilogue adds the two column halves
-  int32_t nw;                                  // accumulator width in TMEM columns (Np, or 2*Np with ycat)
-  int32_t dbg;  // DEBUG (JETB200_K3_DBG): 1 skip stores, 2 skip loads, 4 skip split+STTM, 8 skip MMAs, 16 skip LDTM,
-                //   32 one xfull/tempty arrival per warp, 64 no fence.proxy.async (timing only)
-  unsigned long long* trace;  // DEBUG (JETB200_K3_TRACE): clock64 stamps of CTA 0, items [kTrBegin, +64)
+  int32_t acc_bufs;                            // TMEM accumulators (2: epilogue overlaps next tile)
   int64_t o_sB[kMaxOuter];                     // outer (row) bit j of B: stride
   int64_t o_kB[4];                             // chunk-index bit j of B: stride
   int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
   int32_t sX[kTcMaxTile];                      //   ... and its byte offset in the raw stage (XOR-combined)
-  int32_t wpos[3];                             // positions (in gX order) of row bits 5, 6 and K bit tkc-1:
-                                               //   the bits that select a producer warp's share
   int64_t aM[8], aK[8];                        // A strides of its M bits / K bits
   SliceView sv;
 };
@@ -78,14 +66,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)layout << 61;
   return d;
 }
-// The MMA / commit wrappers are executed by the WHOLE issuing warp with warp-uniform operands;
-// elect.sync inside the asm picks the one lane that issues.  (Issuing from a divergent
-// single-lane branch costs ~150 cycles per tcgen05.mma; warp-uniform issue ~20-60, i.e. the
-// tensor core's own rate -- measured by scripts/mma_probe.cu.)
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
@@ -121,70 +105,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
-      : "memory");
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
 }
-// All MMAs of one item in ONE asm block with one elect.sync: every operand is moved to the
-// uniform datapath before the first tcgen05.mma, so the MMAs issue back to back (separate asm
-// statements interleave an R2UR/ELECT round trip with every MMA, ~100 cycles each).
-// K3 ycat: per K step s, D += X_s * Ycat_s (A from shared memory) and D += Xlo_s * Ycat_s (A from
-// tensor memory); `acc` enables accumulation for the first MMA (all later ones accumulate).
-template <int KS>
-__device__ __forceinline__ void mma_item_ycat(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[KS],
-                                              const uint64_t (&dy)[KS], const uint32_t (&xl)[KS]);
-#define JT_MMA_SS(D, A, B, P) "@e tcgen05.mma.cta_group::1.kind::tf32 [" D "], " A ", " B ", %1, " P ";\n\t"
-#define JT_MMA_TS(D, A, B) "@e tcgen05.mma.cta_group::1.kind::tf32 [" D "], [" A "], " B ", %1, 1;\n\t"
-template <>
-__device__ __forceinline__ void mma_item_ycat<1>(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[1],
-                                                 const uint64_t (&dy)[1], const uint32_t (&xl)[1]) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      JT_MMA_SS("%0", "%3", "%4", "p") JT_MMA_TS("%0", "%5", "%4") "}\n" ::"r"(d),
-      "r"(idesc), "r"(acc), "l"(dx[0]), "l"(dy[0]), "r"(xl[0])
-      : "memory");
-}
-template <>
-__device__ __forceinline__ void mma_item_ycat<2>(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[2],
-                                                 const uint64_t (&dy)[2], const uint32_t (&xl)[2]) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      JT_MMA_SS("%0", "%3", "%5", "p") JT_MMA_TS("%0", "%7", "%5")
-      JT_MMA_SS("%0", "%4", "%6", "1") JT_MMA_TS("%0", "%8", "%6") "}\n" ::"r"(d),
-      "r"(idesc), "r"(acc), "l"(dx[0]), "l"(dx[1]), "l"(dy[0]), "l"(dy[1]), "r"(xl[0]), "r"(xl[1])
-      : "memory");
-}
-template <>
-__device__ __forceinline__ void mma_item_ycat<4>(uint32_t d, uint32_t idesc, uint32_t acc, const uint64_t (&dx)[4],
-                                                 const uint64_t (&dy)[4], const uint32_t (&xl)[4]) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      JT_MMA_SS("%0", "%3", "%7", "p") JT_MMA_TS("%0", "%11", "%7")
-      JT_MMA_SS("%0", "%4", "%8", "1") JT_MMA_TS("%0", "%12", "%8")
-      JT_MMA_SS("%0", "%5", "%9", "1") JT_MMA_TS("%0", "%13", "%9")
-      JT_MMA_SS("%0", "%6", "%10", "1") JT_MMA_TS("%0", "%14", "%10") "}\n" ::"r"(d),
-      "r"(idesc), "r"(acc), "l"(dx[0]), "l"(dx[1]), "l"(dx[2]), "l"(dx[3]), "l"(dy[0]), "l"(dy[1]), "l"(dy[2]),
-      "l"(dy[3]), "r"(xl[0]), "r"(xl[1]), "r"(xl[2]), "r"(xl[3])
-      : "memory");
-}
-// Classic 3xTF32 per K step (wide N): D += X*Yhi + X*Ylo + Xlo*Yhi, one K step per asm block.
-__device__ __forceinline__ void mma_step3(uint32_t d, uint32_t idesc, uint32_t acc, uint64_t dx, uint64_t dyh,
-                                          uint64_t dyl, uint32_t xl) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %2, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      JT_MMA_SS("%0", "%3", "%4", "p") JT_MMA_SS("%0", "%3", "%5", "1") JT_MMA_TS("%0", "%6", "%4") "}\n" ::"r"(d),
-      "r"(idesc), "r"(acc), "l"(dx), "l"(dyh), "l"(dyl), "r"(xl)
-      : "memory");
-}
-#undef JT_MMA_SS
-#undef JT_MMA_TS
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -227,12 +156,6 @@ __device__ __forceinline__ float tf32_hi(float x) {
 __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
-// x - trunc_tf32(x): exact in fp32; the tensor core reads x itself as trunc_tf32(x) (it ignores
-// the low 13 mantissa bits), so hi + lo = x exactly and lo is then read at TF32 precision
-// (relative error 2^-10 of lo <= 2^-20 of x).
-__device__ __forceinline__ float tf32_lo(float x) {
-  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-}
 
 }  // namespace tc
 
@@ -242,51 +165,38 @@ __device__ __forceinline__ int tc_off(int r, int kk, int sbo, int swz) {
   return (r & 7) * 16 + (r >> 3) * sbo + (kk >> 2) * 128 + (kk & 3) * 4;
 }
 
-// Warp-specialised K3 (v12): the raw landing stage IS the MMA's A operand for the hi part.
-//   warps 4-11 producers: each warp cp.async-gathers its own share of every item (rows
-//              quarter*32..+31, chunk half `half`) into a ring stage laid out as the UMMA K-major
-//              swizzled operand (SW128/64/32 for 16/8/4 complex per K chunk); after its own
-//              copies landed (cp.async.wait + __syncwarp) each thread reads its row half, forms
-//              lo = x - trunc_tf32(x) and writes lo to the stage's TMEM columns (tcgen05.st)
-//   warp 12    MMA issuer, per 8-TF32 K step: D += X*Yhi, D += X*Ylo with A = X straight from the
-//              raw stage (the tensor core reads the top 19 bits of each fp32, i.e. hi =
-//              trunc_tf32(x)), then D += Xlo*Yhi with A = lo from TMEM (the TS form); 3xTF32
+// Warp-specialised K3 with the streamed operand in tensor memory.
 //   warps 0-3  epilogue: TMEM accumulator -> registers -> 256-B coalesced global stores
-// Barriers: xfull/xempty per ring stage (raw smem + TMEM lo), tfull/tempty per accumulator.
-// Ring: p.xstages stages, p.rstages items gathered ahead (<= xstages).
-// TKC = K bits per chunk (row of a stage = 2*2^TKC TF32).
+//   warps 4-11 producers: cp.async gathers each item's B rows into a raw shared stage
+//              (rstages-1 items in flight, no registers held); after a producer barrier each
+//              thread takes one row (its TMEM lane) and half of the K chunk, splits it into
+//              hi/lo TF32 and writes both into a TMEM X stage with tcgen05.st
+//   warp 12    MMA issuer: tcgen05.mma kind::tf32 with A = X from TMEM ([a_tmem], the "TS" form)
+//              and B = Y (expanded small operand, resident in shared memory), 3xTF32
+// Barriers: xfull/xempty per TMEM X stage, tfull/tempty per accumulator.
+// TKC = K bits per chunk (row of the X stage = 2*2^TKC TF32 = hi or lo).
 template <int TKC>
 __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
   constexpr int PER = (128 << TKC) / 256;  // B elements each producer thread copies per item
-  constexpr int NCOL = 1 << TKC;           // lo fp32 columns each producer thread writes (half a row)
-  constexpr int KPC = 2 << TKC;            // TF32 columns of one X row
-  constexpr int RB = 8 << TKC;             // raw bytes per row
-  constexpr int CHUNKS = RB >> 4;          // 16-B chunks per row
-  constexpr int SWS = 4 - TKC;             // swizzle: chunk ^= (row >> SWS) & (CHUNKS-1)
-  constexpr uint32_t ALAYOUT = TKC == 4 ? 2u : (TKC == 3 ? 4u : 6u);  // SW128 / SW64 / SW32
+  constexpr int NCOL = 1 << TKC;           // fp32 columns (of hi or lo) each producer thread writes
+  constexpr int KPC = 2 << TKC;            // TF32 columns of one X row (hi or lo)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
-  __shared__ int64_t kc_off[16];  // B byte offset of K chunk c (n_kc <= 16)
-  __shared__ __align__(8) uint64_t xfull[kTcMaxStages], xempty[kTcMaxStages], tfull[2], tempty[2];
+  __shared__ int64_t kc_off[16];  // B offset of K chunk c (n_kc <= 16)
+  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  auto kwait = [&](uint64_t* bar, uint32_t ph) { tc::mbar_wait(bar, ph); };
-  // DEBUG trace: role r (0/1 producer warps 4/11, 2 MMA warp, 3 epilogue warp 0), item i, slot k
-  auto tr = [&](int r, int64_t i, int k) {
-    if (p.trace && blockIdx.x == 0 && lane == 0 && i >= kTrBegin && i < kTrBegin + 64)
-      p.trace[((r * 64) + (i - kTrBegin)) * 8 + k] = clock64();
-  };
   if (tid < 16) {
     int64_t o = 0;
     for (int j = 0; j < p.K - p.tkc; ++j) if ((tid >> j) & 1) o += p.o_kB[j];
-    kc_off[tid] = o * 8;
+    kc_off[tid] = o;
   }
-  // 1024-B aligned carve: Y planes [hi c=0..n_kc-1 | lo ...], then the ring stages (1024-aligned)
+  // 1024-B aligned carve: Y planes [hi c=0..n_kc-1 | lo ...], then the raw stages
   unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* Yhi = base;
   unsigned char* Ylo = Yhi + p.n_kc * p.yplane;
-  unsigned char* R = base + (((p.ycat ? 1 : 2) * p.n_kc * p.yplane + 1023) & ~1023);
+  unsigned char* R = Ylo + p.n_kc * p.yplane;
   for (int i = tid; i < 64; i += blockDim.x) {
     for (int h = 0; h < 2; ++h) {
       int64_t g = 0;
@@ -296,7 +206,7 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
           const int bi = 6 * h + b;
           if (bi < p.nX) { g += p.gX[bi]; s ^= p.sX[bi]; }
         }
-      tg[h][i] = g * 8;
+      tg[h][i] = g;
       ts[h][i] = s;
     }
   }
@@ -307,13 +217,13 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int i = 0; i < p.xstages; ++i) {
-      tc::mbar_init(&xfull[i], (p.dbg & 32) ? 8 : 256);
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&xfull[i], 256);
       tc::mbar_init(&xempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], (p.dbg & 32) ? 4 : 128);
+      tc::mbar_init(&tempty[i], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -333,17 +243,11 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       const int c = k / nkc, kl = k % nkc;
       for (int s = 0; s < 2; ++s)
         for (int t = 0; t < 2; ++t) {
+          const int byte = c * p.yplane + tc_off(2 * m + s, 2 * kl + t, p.sbo_y, p.swz);
           const float x = vals[s][t];
           const float hi = tc::tf32_rna(x);
-          if (p.ycat) {  // one plane per chunk: rows [0, Np) = Yhi, [Np, 2Np) = Ylo
-            *reinterpret_cast<float*>(Yhi + c * p.yplane + tc_off(2 * m + s, 2 * kl + t, p.sbo_y, p.swz)) = hi;
-            *reinterpret_cast<float*>(Yhi + c * p.yplane + tc_off(p.Np + 2 * m + s, 2 * kl + t, p.sbo_y, p.swz)) =
-                tc::tf32_rna(x - hi);
-          } else {
-            const int byte = c * p.yplane + tc_off(2 * m + s, 2 * kl + t, p.sbo_y, p.swz);
-            *reinterpret_cast<float*>(Yhi + byte) = hi;
-            *reinterpret_cast<float*>(Ylo + byte) = tc::tf32_rna(x - hi);
-          }
+          *reinterpret_cast<float*>(Yhi + byte) = hi;
+          *reinterpret_cast<float*>(Ylo + byte) = tc::tf32_rna(x - hi);
         }
     }
   }
@@ -352,7 +256,7 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t xcol0 = (uint32_t)(p.acc_bufs * p.nw);  // first TMEM column of the lo stages
+  const uint32_t xcol0 = (uint32_t)(p.acc_bufs * p.Np);  // first TMEM column of the X stages
   const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles * p.n_kc;
   const uint32_t layout = p.swz ? 2u : 0u;
@@ -361,37 +265,26 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
 
   if (warp >= 4 && warp < 12) {
     // ===================== producers =====================
-    const int64_t boff = slice_off(p.sv, false) * 8;
+    const int ptid = tid - 128;  // 0..255
+    const int64_t boff = slice_off(p.sv, false);
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int row = quarter * 32 + lane;  // this thread's TMEM lane (row n of the tile)
-    const int S = p.xstages, D = p.rstages;
-    const char* Bb = reinterpret_cast<const char*>(p.B);
-    // Each producer warp gathers exactly the elements it converts later, so a warp only waits
-    // for its own copies (cp.async.wait + __syncwarp) and never synchronises with the other
-    // producer warps.  Its share is the tile with the three warp-select bits fixed; the other
-    // bits, lowest strides first, index lane + 32 i (coalesced).  Byte offsets, in registers.
+    const int RS = p.rstages, XS = p.xstages;
+    // raw row layout: 16-B chunk c of row n lives at chunk c ^ (n & (chunks-1))
+    const int rb = 8 << TKC;            // raw bytes per row
+    const int chunks = rb >> 4;
+    // per-thread gather offsets are the same for every item: keep them in registers
     int64_t goff[PER];
     int32_t soff[PER];
-    {
-      const int wbits[3] = {quarter & 1, quarter >> 1, half};
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        int sub = lane + i * 32, e = 0, sb = 0;
-        for (int j = 0; j < p.nX; ++j) {
-          int bit;
-          if (j == p.wpos[0]) bit = wbits[0];
-          else if (j == p.wpos[1]) bit = wbits[1];
-          else if (j == p.wpos[2]) bit = wbits[2];
-          else bit = (sub >> sb++) & 1;
-          e |= bit << j;
-        }
-        goff[i] = tg[0][e & 63] + tg[1][e >> 6];
-        soff[i] = ts[0][e & 63] ^ ts[1][e >> 6];
-      }
+    for (int i = 0; i < PER; ++i) {
+      const int e = ptid + i * 256;
+      goff[i] = tg[0][e & 63] + tg[1][e >> 6];
+      soff[i] = ts[0][e & 63] ^ ts[1][e >> 6];
     }
     // copy cursor: the next item to gather (tile number ct of this CTA, K chunk cc); the tile
     // base offset is re-summed (lane j holds outer bit j's stride) only when the tile changes
-    const int64_t o_s = lane < p.n_outer ? p.o_sB[lane] * 8 : 0;
+    const int64_t o_s = lane < p.n_outer ? p.o_sB[lane] : 0;
     auto tile_base = [&](int64_t ct) {
       const int64_t t = (int64_t)blockIdx.x + ct * gridDim.x;
       int64_t tb = ((t >> lane) & 1) ? o_s : 0;
@@ -400,119 +293,94 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       return boff + tb;
     };
     int64_t ct = 0, cbase = tile_base(0);
-    int cc = 0, wst = 0;  // wst = ring stage the next copy lands in
-    uint32_t wph = 0;     // use parity of that stage
-    int64_t trit = -1;
-    const int trr = warp == 4 ? 0 : (warp == 11 ? 1 : -1);
+    int cc = 0, wst = 0;  // wst = raw stage the next copy lands in
     auto copy = [&]() {
-      kwait(&xempty[wst], wph ^ 1);  // the stage's previous item is consumed by the MMAs
-      if (trr >= 0 && trit >= 0) tr(trr, trit, 6);
       unsigned char* raw = R + wst * p.rbytes;
-      const char* src = Bb + (cbase + kc_off[cc]);
-      if (!(p.dbg & 2)) {
+      const float2* srcp = p.B + (cbase + kc_off[cc]);
 #pragma unroll
-        for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], src + goff[i]);
-      }
-      if (++wst == S) { wst = 0; wph ^= 1; }
+      for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], srcp + goff[i]);
+      if (++wst == RS) wst = 0;
       if (++cc == p.n_kc) {
         cc = 0;
         ++ct;
         cbase = tile_base(ct);
       }
     };
-    for (int q = 0; q < D; ++q) {
+    for (int q = 0; q < RS - 1; ++q) {
       if (q < items) copy();
       cp_async_commit();
     }
-    int rst = 0;  // ring stage of item it
-    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int sw = (row >> SWS) & (CHUNKS - 1);
+    int rst = 0, xs = 0;
+    uint32_t xph = 0;
     for (int64_t it = 0; it < items; ++it) {
-      if (trr >= 0) tr(trr, it, 0);
-      cp_async_wait_dyn(D - 1);  // own copies of item it landed (D groups ahead were committed)
-      __syncwarp();              // ... and every lane's copies of this warp's share
-      if (trr >= 0) tr(trr, it, 1);
-      if (!(p.dbg & 4)) {
-        const unsigned char* raw = R + rst * p.rbytes + row * RB;
-        float lo[NCOL];
-#pragma unroll
-        for (int j = 0; j < NCOL / 4; ++j) {
-          const int ch = half * (NCOL / 4) + j;  // 16-B chunk of this row = 2 complex
-          const float4 v = *reinterpret_cast<const float4*>(raw + ((ch ^ sw) << 4));
-          lo[4 * j + 0] = tc::tf32_lo(v.x);
-          lo[4 * j + 1] = tc::tf32_lo(v.y);
-          lo[4 * j + 2] = tc::tf32_lo(v.z);
-          lo[4 * j + 3] = tc::tf32_lo(v.w);
-        }
-        if (trr >= 0) tr(trr, it, 2);
-        tc::tmem_st<NCOL>(lane_addr + xcol0 + (uint32_t)(rst * KPC + half * NCOL), lo);
-        tc::tmem_st_wait();
+      // own copies of item it have landed (RS-1+it groups committed, RS-2 may stay pending)
+      switch (RS) {
+        case 2: cp_async_wait<0>(); break;
+        case 3: cp_async_wait<1>(); break;
+        case 4: cp_async_wait<2>(); break;
+        case 5: cp_async_wait<3>(); break;
+        default: cp_async_wait<4>(); break;
       }
-      if (trr >= 0) tr(trr, it, 3);
-      if (!(p.dbg & 64)) tc::fence_proxy_async();  // this thread's cp.async data -> visible to the MMA (async proxy)
-      tc::fence_before();
-      if (p.dbg & 32) {
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&xfull[rst]);
-      } else {
-        tc::mbar_arrive(&xfull[rst]);
-      }
-      if (trr >= 0) tr(trr, it, 4);
-      if (++rst == S) rst = 0;
-      trit = it;
-      if (it + D < items) copy();
+      tc::bar_sync(1, 256);  // all producers' copies of item it landed; raw stage of it-1 is free
+      if (it + RS - 1 < items) copy();
       cp_async_commit();
-      if (trr >= 0) tr(trr, it, 5);
+      tc::mbar_wait(&xempty[xs], xph ^ 1);  // TMEM X stage free
+      tc::fence_after();
+      const unsigned char* raw = R + rst * p.rbytes + row * rb;
+      if (++rst == RS) rst = 0;
+      float hi[NCOL], lo[NCOL];
+#pragma unroll
+      for (int j = 0; j < NCOL / 4; ++j) {
+        const int cc = half * (NCOL / 4) + j;  // 16-B chunk of this row = 2 complex
+        const float4 v = *reinterpret_cast<const float4*>(raw + ((cc ^ (row & (chunks - 1))) << 4));
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hi[4 * j + q] = tc::tf32_rna(x[q]);
+          lo[4 * j + q] = tc::tf32_rna(x[q] - hi[4 * j + q]);
+        }
+      }
+      const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+      const uint32_t col = xcol0 + (uint32_t)(xs * 2 * KPC + half * NCOL);
+      tc::tmem_st<NCOL>(lane_addr + col, hi);
+      tc::tmem_st<NCOL>(lane_addr + col + KPC, lo);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&xfull[xs]);
+      if (++xs == XS) { xs = 0; xph ^= 1; }
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
+    const bool leader = lane == 0;
     int64_t tt = 0;
-    const int S = p.xstages;
+    const int XS = p.xstages;
     int xs = 0, c = 0;
     uint32_t xph = 0;
     for (int64_t it = 0; it < items; ++it) {
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
-      tr(2, it, 0);
-      if (c == 0) kwait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
-      tr(2, it, 1);
-      kwait(&xfull[xs], xph);
-      tr(2, it, 2);
+      if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
+      tc::mbar_wait(&xfull[xs], xph);
       tc::fence_after();
-      if (!(p.dbg & 8)) {  // whole warp: the wrappers elect the issuing lane
-        const uint32_t d = tmem + (uint32_t)(b * p.nw);
-        const uint32_t xl = tmem + xcol0 + (uint32_t)(xs * KPC);
-        const uint32_t xr = tc::smem_u32(R + xs * p.rbytes);
+      if (leader) {
+        const uint32_t d = tmem + (uint32_t)(b * p.Np);
+        const uint32_t xh = tmem + xcol0 + (uint32_t)(xs * 2 * KPC), xl = xh + KPC;
         const uint32_t yh = tc::smem_u32(Yhi + c * p.yplane), yl = tc::smem_u32(Ylo + c * p.yplane);
-        constexpr int KS = KPC / 8;
-        const uint32_t acc = c > 0 ? 1u : 0u;
-        uint64_t dx[KS], dy[KS];
-        uint32_t xls[KS];
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          dx[ks] = tc::sdesc(xr + ks * 32, 16, 8 * RB, ALAYOUT);
-          dy[ks] = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
-          xls[ks] = xl + ks * 8;
+        for (int ks = 0; ks < KPC / 8; ++ks) {
+          const uint64_t dyh = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
+          const uint64_t dyl = tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout);
+          tc::mma_tf32_ts(d, xh + ks * 8, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_tf32_ts(d, xh + ks * 8, dyl, p.idesc, 1u);
+          tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
         }
-        if (p.ycat) {  // D[:, 0:2Np] += (hi + lo) * [Yhi|Ylo]
-          tc::mma_item_ycat<KS>(d, p.idesc, acc, dx, dy, xls);
-        } else {  // D += hi*Yhi + hi*Ylo + lo*Yhi
-#pragma unroll
-          for (int ks = 0; ks < KS; ++ks)
-            tc::mma_step3(d, p.idesc, (c > 0 || ks > 0) ? 1u : 0u, dx[ks], dy[ks],
-                          tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout), xls[ks]);
-        }
-        tc::mma_commit(&xempty[xs]);                     // ring stage free once these finish
+        tc::mma_commit(&xempty[xs]);                     // TMEM X stage free once these finish
         if (c == p.n_kc - 1) tc::mma_commit(&tfull[b]);  // tile accumulated
-      } else if (lane == 0) {
-        tc::mbar_arrive(&xempty[xs]);
-        if (c == p.n_kc - 1) tc::mbar_arrive(&tfull[b]);
       }
       __syncwarp();
-      tr(2, it, 3);
       if (c == p.n_kc - 1) ++tt;
       if (++c == p.n_kc) c = 0;
-      if (++xs == S) { xs = 0; xph ^= 1; }
+      if (++xs == XS) { xs = 0; xph ^= 1; }
     }
   } else if (warp < 4) {
     // ===================== epilogue =====================
@@ -521,41 +389,21 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     for (int64_t tt = 0; tt < my_tiles; ++tt) {
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
-      if (warp == 0) tr(3, tt, 0);
-      kwait(&tfull[b], tph);
-      if (warp == 0) tr(3, tt, 1);
+      tc::mbar_wait(&tfull[b], tph);
       tc::fence_after();
       const int64_t t = (int64_t)blockIdx.x + tt * gridDim.x;
       float2* out = p.C + (t << (7 + p.tm));
       for (int c0 = 0; c0 < p.Np; c0 += 16) {
         float v[16];
-        if (p.dbg & 16) {
-          for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        } else {
-          const uint32_t a0 = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.nw + c0);
-          tc::tmem_ld16(a0, v);
-          if (p.ycat) {  // (hi + lo) x Yhi  +  (hi + lo) x Ylo
-            float w[16];
-            tc::tmem_ld16(a0 + (uint32_t)p.Np, w);
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) v[jj] += w[jj];
-          }
-        }
+        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.Np + c0), v);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int m = c0 / 2 + j;
-          if (m < nm && !(p.dbg & 1)) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+          if (m < nm) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
         }
       }
-      if (warp == 0) tr(3, tt, 2);
       tc::fence_before();
-      if (p.dbg & 32) {
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[b]);
-      } else {
-        tc::mbar_arrive(&tempty[b]);
-      }
-      if (warp == 0) tr(3, tt, 3);
+      tc::mbar_arrive(&tempty[b]);
     }
   }
   tc::fence_before();

@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
+    const bool leader = lane == 0;
     int64_t tt = 0;
     for (int64_t it = 0; it < items; ++it) {
       const int xs = (int)(it & 3), ys = (int)(it & 1);
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);
       tc::mbar_wait(&full[xs], (uint32_t)((it >> 2) & 1));
       tc::fence_after();
-      {  // whole warp: the MMA / commit wrappers elect the issuing lane
+      if (leader) {
         const uint32_t d = tmem + (uint32_t)(b * NP);
         const uint32_t xh = tmem + xcol0 + (uint32_t)(xs * 2 * KPC), xl = xh + KPC;
         const uint32_t yh = tc::smem_u32(Y + ys * 2 * NP * 128), yl = yh + NP * 128;
