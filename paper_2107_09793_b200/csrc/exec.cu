@@ -119,11 +119,13 @@ void set_smem_attrs() {
     const void* tcgs[3] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
                            reinterpret_cast<const void*>(gett_tcg_kernel<6>)};
     for (const void* f : tcgs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, false>),
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, 0>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, true>),
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, 1>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2, false>),
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, 2>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2, 0>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
 }
@@ -1322,9 +1324,13 @@ void permute(jt_dtype dt, const void* src, void* dst, int n, const int32_t* perm
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // element pairs stay together when bit 0 maps to bit 0 (and the tile holds >= 2 elements)
   const bool pair = esize == 8 && n >= 1 && perm[0] == 0 && p.nt >= 1 && p.in_g[0] == 1 && p.out_g[0] == 1;
-  if (esize == 8 && pair) permute_kernel<float2, true><<<(unsigned)nblk, 256, smem, s>>>(p);
-  else if (esize == 8) permute_kernel<float2, false><<<(unsigned)nblk, 256, smem, s>>>(p);
-  else permute_kernel<double2, false><<<(unsigned)nblk, 256, smem, s>>>(p);
+  // otherwise (c64, bit 0 moves) input pairs and output pairs still move as 16 B (input bit 0
+  // and output bit 0 are both tile bits)
+  const bool split = esize == 8 && !pair && p.nt >= 2 && p.in_g[0] == 1 && p.out_g[0] == 1;
+  if (esize == 8 && pair) permute_kernel<float2, 1><<<(unsigned)nblk, 256, smem, s>>>(p);
+  else if (split) permute_kernel<float2, 2><<<(unsigned)nblk, 256, smem, s>>>(p);
+  else if (esize == 8) permute_kernel<float2, 0><<<(unsigned)nblk, 256, smem, s>>>(p);
+  else permute_kernel<double2, 0><<<(unsigned)nblk, 256, smem, s>>>(p);
   JT_CUDA(cudaGetLastError());
 }
 

@@ -387,9 +387,12 @@ struct PermArgs {
   int32_t out_s[kMaxTile];  //   ... and smem stride
 };
 
-// PAIR (c64 only): address bit 0 stays bit 0, so element pairs move as 16 B on both sides.
-// The shared tile is XOR-swizzled (swz, 8-B units) so the output-order reads spread over banks.
-template <typename E, bool PAIR>
+// MODE 0: one element per access.  MODE 1 (c64): address bit 0 stays bit 0, so element pairs
+// move as 16 B on both sides.  MODE 2 (c64, bit 0 moves): 16-B loads of input-order pairs
+// (input bit 0) and 16-B stores of output-order pairs (output bit 0), the two halves of a
+// stored pair gathered from the tile with two 8-B shared loads.  The shared tile is
+// XOR-swizzled (swz, 8-B units, bit 0 kept) so the output-order reads spread over banks.
+template <typename E, int MODE>
 __global__ void __launch_bounds__(256) permute_kernel(const __grid_constant__ PermArgs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* tileb = reinterpret_cast<E*>(smem_raw);
@@ -416,13 +419,23 @@ __global__ void __launch_bounds__(256) permute_kernel(const __grid_constant__ Pe
   const E* __restrict__ src = reinterpret_cast<const E*>(p.src);
   E* __restrict__ dst = reinterpret_cast<E*>(p.dst);
   const int sz = 1 << p.nt;
-  if (PAIR) {
+  if (MODE == 1) {
     for (int e = 2 * tid; e < sz; e += 2 * blockDim.x)
       *reinterpret_cast<float4*>(tileb + swz<E>(e)) = *reinterpret_cast<const float4*>(src + bs + tin[0][e & 63] + tin[1][e >> 6]);
     __syncthreads();
     for (int f = 2 * tid; f < sz; f += 2 * blockDim.x)
       *reinterpret_cast<float4*>(dst + bd + tout[0][f & 63] + tout[1][f >> 6]) =
           *reinterpret_cast<const float4*>(tileb + swz<E>(tso[0][f & 63] + tso[1][f >> 6]));
+  } else if (MODE == 2) {
+    for (int e = 2 * tid; e < sz; e += 2 * blockDim.x)
+      *reinterpret_cast<float4*>(tileb + swz<E>(e)) = *reinterpret_cast<const float4*>(src + bs + tin[0][e & 63] + tin[1][e >> 6]);
+    __syncthreads();
+    const int s1 = tso[0][1];  // tile position of output bit 0
+    for (int f = 2 * tid; f < sz; f += 2 * blockDim.x) {
+      const int s0 = tso[0][f & 63] + tso[1][f >> 6];
+      const E a = tileb[swz<E>(s0)], b = tileb[swz<E>(s0 + s1)];
+      *reinterpret_cast<float4*>(dst + bd + tout[0][f & 63] + tout[1][f >> 6]) = make_float4(a.x, a.y, b.x, b.y);
+    }
   } else {
     for (int e = tid; e < sz; e += blockDim.x) tileb[swz<E>(e)] = src[bs + tin[0][e & 63] + tin[1][e >> 6]];
     __syncthreads();
