@@ -26,6 +26,10 @@ def workload(name: str, seed: int = 1):
         c = sycamore53(20, seed)
     elif name == "C4":
         c = generate_gbs(3, 4, 1, 0.5, 4, seed)
+    elif name == "G88d4":     # GBS-88-m1 (2-D 8x8 modes, one cycle), cutoff 4
+        c = generate_gbs(2, 8, 1, 0.5, 4, seed)
+    elif name == "G88d8":     # the same circuit at cutoff 8 (qudits of 3 address bits)
+        c = generate_gbs(2, 8, 1, 0.5, 8, seed)
     else:
         raise ValueError(name)
     return c, random_bitstring(c.n_wires, c.d, seed)
