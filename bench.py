@@ -31,6 +31,9 @@ CONFIGS = {
     "C3": dict(circ="C3", k=10, dtype="c64", sps=16, workload="sycamore53_m14_2^10slices"),
     "C5": dict(circ="C5", k=None, dtype="c64", sps=1, cap=30, seeds=2, workload="sycamore53_m20_width30_subset"),
     "C4": dict(circ="C4", k=None, dtype="c128", sps=1, cap=28, seeds=2, workload="gbs444_d4_width28_subset"),
+    # GBS-88-m1 at cutoff 4 (full amplitude per step) and 8 (sliced)
+    "G88d4": dict(circ="G88d4", k=0, dtype="c128", sps=1, seeds=2, workload="gbs88_m1_d4_full_amplitude"),
+    "G88d8": dict(circ="G88d8", k=None, dtype="c128", sps=1, cap=30, seeds=2, workload="gbs88_m1_d8_width30_subset"),
 }
 
 
@@ -195,12 +198,16 @@ def tensor_peak_alg(dtype):
     """Algorithmic complex-FLOP peak of the tensor path: TF32 = measured bf16 burst x 1/2 (the
     guide's nominal TF32:BF16 ratio), divided by 3 for the 3xTF32 split (the 4M real expansion
     does exactly the complex work: 4 real MACs = 8 real FLOP per complex MAC).  c128 runs on
-    CUDA-core FP64: nominal 37 TFLOP/s."""
+    the FP64 pipe (K4 DMMA, K2 DFMA): 37.0 TFLOP/s measured by scripts/fp64_probe.cu on B200
+    (DMMA m8n8k4 37.0, DFMA 36.2; profiles/r01_fp64_probe.txt); the guides give no B200 FP64 figure."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     bf16 = json.load(open(p)).get("bf16_tflops", 1590.0) if os.path.exists(p) else 1590.0
     if dtype == "c128":
-        return 37.0, "nominal FP64 (B200 datasheet 37 TFLOP/s)"
+        return 37.0, "measured FP64 DMMA peak 37.0 TFLOP/s (scripts/fp64_probe.cu, profiles/r01_fp64_probe.txt)"
     return bf16 * 0.5 / 3.0, f"measured bf16 {bf16} x 0.5 (TF32) / 3 (3xTF32)"
+
+
+KERNEL_NAMES = {"K3": "tcgen05 3xTF32 (K3/K3g)", "K2": "CUDA-core GETT", "K4": "FP64 tensor-core DMMA GETT"}
 
 
 def roofline_entry(args, dom, gbs, tfs, dom_bytes, dom_n, dom_ms, peak, peak_kind, ms_max, prof_steps, kern, dtype):
@@ -215,7 +222,7 @@ def roofline_entry(args, dom, gbs, tfs, dom_bytes, dom_n, dom_ms, peak, peak_kin
         "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
         "frac": ft if bound == "tensor" else fh,
         "traffic": profile_traffic(args.config, dom),
-        "kernel": (f"{dom} ({'tcgen05 3xTF32 (K3/K3g)' if dom == 'K3' else 'CUDA-core GETT'}); achieved = algorithmic "
+        "kernel": (f"{dom} ({KERNEL_NAMES[dom]}); achieved = algorithmic "
                    f"{'complex FLOP' if bound == 'tensor' else 'bytes |A|+|B|+|C|'} per launch / CUDA-event launch time"),
         "peak_kind": tkind if bound == "tensor" else peak_kind,
         "other": {"GBps": gbs, "frac_hbm": fh, "TFLOPs_alg": tfs, "frac_tensor": ft, "tensor_peak_alg": tpeak},
@@ -328,6 +335,8 @@ def run_ours(args, cfg):
 
     def step():
         b, e = next_block()
+        if b == b0:   # a new pass over this rank's slices starts cold (no cache from the last pass)
+            ex.invalidate()
         ex.contract(b, e, acc)
         with torch.cuda.stream(stream):
             allreduce_amplitude(acc)
@@ -378,22 +387,22 @@ def run_ours(args, cfg):
     ex.set_profiling(False)
     pst = ex.stats()
     # the dominant contraction kernel of the step: K3 (tcgen05) or K2 (CUDA cores)
-    t3 = pst["k3_time_ms"]
-    t2 = pst["k2_time_ms"] - t3
-    b3, b2 = pst["k3_timed_bytes"], pst["k2_timed_bytes"] - pst["k3_timed_bytes"]
-    n3, n2 = pst["k3_timed_launches"], pst["k2_timed_launches"] - pst["k3_timed_launches"]
-    dom = "K3" if t3 >= t2 else "K2"
-    dom_ms, dom_bytes, dom_n = (t3, b3, n3) if dom == "K3" else (t2, b2, n2)
-    f3, f2 = pst["k3_timed_flop"], pst["k2_timed_flop"] - pst["k3_timed_flop"]
-    dom_flop = f3 if dom == "K3" else f2
+    # (the K2 counters hold every timed contraction launch; K3 and K4 are subsets)
+    cls = {}
+    for key in ("k3", "k4"):
+        cls[key.upper()] = (pst[f"{key}_time_ms"], pst[f"{key}_timed_bytes"], pst[f"{key}_timed_launches"],
+                            pst[f"{key}_timed_flop"])
+    cls["K2"] = tuple(pst[f"k2_{f}"] - cls["K3"][i] - cls["K4"][i]
+                      for i, f in enumerate(("time_ms", "timed_bytes", "timed_launches", "timed_flop")))
+    dom = max(cls, key=lambda q: cls[q][0])
+    dom_ms, dom_bytes, dom_n, dom_flop = cls[dom]
+    dom_n = int(dom_n)
     dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     dom_tfs = dom_flop / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
-    kern_info = {
-        "K3_tcgen05": {"launches": n3, "ms": t3, "GBps": (b3 / (t3 / 1e3) / 1e9) if t3 > 0 else None,
-                       "TFLOPs_alg": (f3 / (t3 / 1e3) / 1e12) if t3 > 0 else None},
-        "K2_cuda_core": {"launches": n2, "ms": t2, "GBps": (b2 / (t2 / 1e3) / 1e9) if t2 > 0 else None,
-                         "TFLOPs_alg": (f2 / (t2 / 1e3) / 1e12) if t2 > 0 else None},
-    }
+    names = {"K3": "K3_tcgen05", "K2": "K2_cuda_core", "K4": "K4_dmma_fp64"}
+    kern_info = {names[q]: {"launches": int(v[2]), "ms": v[0], "GBps": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 else None,
+                            "TFLOPs_alg": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else None}
+                 for q, v in cls.items()}
     prof_steps = max(1, min(args.steps, 2))
 
     # end-to-end through the public API with host buffers: per step, H2D of the network
@@ -410,6 +419,8 @@ def run_ours(args, cfg):
         for _ in range(args.steps):
             ex.upload_leaves()
             b, e = next_block()
+            if b == b0:
+                ex.invalidate()
             part = ex.contract_host(b, e)
             e_slices += e - b
         torch.cuda.synchronize()

@@ -110,6 +110,10 @@ typedef struct {
   double k3_timed_bytes;
   double k3_timed_flop;
   int64_t h2d_bytes;       /* host->device bytes copied by jt_exec_create / jt_exec_upload_leaves */
+  double k4_time_ms;          /* ... the subset of the timed launches that ran on K4 (c128 DMMA) */
+  int64_t k4_timed_launches;
+  double k4_timed_bytes;
+  double k4_timed_flop;
 } jt_exec_stats;
 
 const char* jt_last_error(void);
@@ -193,7 +197,7 @@ jt_status jt_exec_contract_host(jt_exec* ex, int64_t slice_begin, int64_t slice_
 /* Re-upload the leaf tensors (the network data) from host memory through a pinned staging
    buffer, H2D on the stream (the per-step input copy of the end-to-end path). */
 jt_status jt_exec_upload_leaves(jt_exec* ex);
-/* Profiling: bracket every K2 launch with CUDA events on the exec stream; each
+/* Profiling: bracket every contraction launch (K2/K3/K3g/K4) with CUDA events on the exec stream; each
    jt_exec_contract call then synchronises and adds the event times to the stats. */
 jt_status jt_exec_set_profiling(jt_exec* ex, int32_t on);
 jt_status jt_exec_stats_get(const jt_exec* ex, jt_exec_stats* out);
@@ -216,7 +220,7 @@ jt_status jt_debug_emulate_host(const jt_plan* plan, jt_dtype dtype, int64_t b, 
 /* DEBUG ONLY: time `reps` back-to-back launches of the node at execution-order index
    `order_index` (CUDA events on the exec stream; inputs as currently in the workspace).
    Returns the mean ms per launch, the node's algorithmic bytes and FLOP, and its kernel kind
-   (0 K2, 1 K3, 2 K3g).  For kernel tuning on real plan shapes. */
+   (0 K2, 1 K3, 2 K3g, 3 K4).  For kernel tuning on real plan shapes. */
 jt_status jt_debug_time_node(jt_exec* ex, int64_t order_index, int32_t reps, double* ms, double* bytes,
                              double* flop, int32_t* kind);
 

@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_tcg.cuh"
+#include "kernels_dmma.cuh"
 
 #define JT_CUDA(x)                                                                        \
   do {                                                                                    \
@@ -92,6 +93,15 @@ TcFn pick_tc(int tkc) {
   fail(JT_EINTERNAL, "no tc instance");
 }
 
+GettFn pick_dmma(int SMT, int SNT) {
+#define JT_DCASE(a, b) \
+  if (SMT == a && SNT == b) return gett_dmma_kernel<a, b>;
+  JT_DCASE(1, 1) JT_DCASE(1, 2) JT_DCASE(1, 4) JT_DCASE(2, 1) JT_DCASE(2, 2) JT_DCASE(2, 4)
+  JT_DCASE(4, 1) JT_DCASE(4, 2) JT_DCASE(4, 4)
+#undef JT_DCASE
+  fail(JT_EINTERNAL, "no dmma instance");
+}
+
 template <typename R>
 GettFn pick_gett(int RM, int RN) {
 #define JT_CASE(a, b) \
@@ -111,6 +121,8 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<float>(a, b)),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_dmma(a, b)),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
     const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<3>),
@@ -337,6 +349,73 @@ bool tc_enabled() {
   return !(e && e[0] == '0');
 }
 
+View fill_gett(ExecNode& en, std::map<int64_t, int64_t>& sa, std::map<int64_t, int64_t>& sb,
+               const std::vector<std::pair<int64_t, int64_t>>& M, const std::vector<std::pair<int64_t, int64_t>>& N,
+               const std::vector<std::pair<int64_t, int64_t>>& K, const std::vector<char>& inM,
+               const std::vector<char>& inN, const std::vector<char>& inK, int esize, bool dmma);
+
+bool dmma_enabled() {
+  const char* e = std::getenv("JETB200_DMMA");
+  return !(e && e[0] == '0');
+}
+
+// Split the bits of a pairwise contraction into M (A only), N (B only) and K (shared), each
+// sorted by stride (lowest first).  Every shared label is summed (no hyperedges).
+void split_mnk(const View& va, const View& vb, std::map<int64_t, int64_t>& sa, std::map<int64_t, int64_t>& sb,
+               std::vector<std::pair<int64_t, int64_t>>& M, std::vector<std::pair<int64_t, int64_t>>& N,
+               std::vector<std::pair<int64_t, int64_t>>& K) {
+  for (auto& x : va.bits) sa[x.first] = x.second;
+  for (auto& x : vb.bits) sb[x.first] = x.second;
+  for (auto& x : va.bits) {
+    if (sb.count(x.first)) K.push_back({std::min(x.second, sb[x.first]), x.first});
+    else M.push_back({x.second, x.first});
+  }
+  for (auto& x : vb.bits)
+    if (!sa.count(x.first)) N.push_back({x.second, x.first});
+  std::sort(M.begin(), M.end());
+  std::sort(N.begin(), N.end());
+  std::sort(K.begin(), K.end());
+}
+
+// K4 tile selection (c128 on DMMA): C tile 2^tm x 2^tn with tm, tn in [3, 7] and tm + tn <= 13
+// (8x8 MMA sub-tiles, at most 4x4 per warp and 8 warps), tile-K 2^tk with tk in [2, 5], each
+// operand's lowest 3 address bits (128-B runs) inside the tiles, two pipeline stages within
+// 200 KB of shared memory.  Returns false when the contraction has no such tile (K2 runs it).
+bool plan_dmma(ExecNode& en, const View& va, const View& vb, View& out) {
+  std::map<int64_t, int64_t> sa, sb;
+  std::vector<std::pair<int64_t, int64_t>> M, N, K;
+  split_mnk(va, vb, sa, sb, M, N, K);
+  if (M.size() < 3 || N.size() < 3 || K.size() < 2) return false;
+  std::vector<char> inM(M.size(), 0), inN(N.size(), 0), inK(K.size(), 0);
+  auto mark_low = [&](const View& vw) {
+    std::vector<std::pair<int64_t, int64_t>> s;
+    for (auto& x : vw.bits) s.push_back({x.second, x.first});
+    std::sort(s.begin(), s.end());
+    for (size_t i = 0; i < s.size() && i < 3; ++i) {
+      for (size_t j = 0; j < M.size(); ++j) if (M[j].second == s[i].second) inM[j] = 1;
+      for (size_t j = 0; j < N.size(); ++j) if (N[j].second == s[i].second) inN[j] = 1;
+      for (size_t j = 0; j < K.size(); ++j) if (K[j].second == s[i].second) inK[j] = 1;
+    }
+  };
+  mark_low(va);
+  mark_low(vb);
+  auto cnt = [](const std::vector<char>& v) { int c = 0; for (char x : v) c += x; return c; };
+  auto grow = [&](std::vector<char>& in, int target) {
+    for (size_t i = 0; i < in.size() && cnt(in) < target; ++i) in[i] = 1;
+  };
+  grow(inK, std::min<int>((int)K.size(), 4));
+  grow(inM, std::min<int>((int)M.size(), 7));
+  grow(inN, std::min<int>((int)N.size(), std::max(3, 13 - cnt(inM))));
+  if (cnt(inN) > 7) return false;
+  const int tm = cnt(inM), tn = cnt(inN), tk = cnt(inK);
+  if (tm < 3 || tn < 3 || tk < 2 || tk > 5 || tm > 7 || tm + tn > 13) return false;
+  if (tm + tk > 12 || tk + tn > 12) return false;
+  const int64_t smem = 2 * ((int64_t(1) << (tm + tk)) + (int64_t(1) << (tk + tn))) * 16;
+  if (smem > 200 * 1024) return false;
+  out = fill_gett(en, sa, sb, M, N, K, inM, inN, inK, 16, true);
+  return true;
+}
+
 // Tile selection and argument fill for one contraction (K2).  Returns the output view.
 View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
   std::map<int64_t, int64_t> sa, sb;
@@ -429,6 +508,15 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
     if (drop_last(inK, keepK)) continue;
     fail(JT_EINTERNAL, "exec: cannot fit a contraction tile");
   }
+  return fill_gett(en, sa, sb, M, N, K, inM, inN, inK, esize, false);
+}
+
+// Argument fill for one contraction tile choice (K2, or K4 when dmma): gather tables, outer
+// and K-loop strides, thread layout, split-K and shared memory.  Returns the output view.
+View fill_gett(ExecNode& en, std::map<int64_t, int64_t>& sa, std::map<int64_t, int64_t>& sb,
+               const std::vector<std::pair<int64_t, int64_t>>& M, const std::vector<std::pair<int64_t, int64_t>>& N,
+               const std::vector<std::pair<int64_t, int64_t>>& K, const std::vector<char>& inM,
+               const std::vector<char>& inN, const std::vector<char>& inK, int esize, bool dmma) {
   std::vector<int64_t> tM, tN, tK, oM, oN, oK;
   for (size_t i = 0; i < M.size(); ++i) (inM[i] ? tM : oM).push_back(M[i].second);
   for (size_t i = 0; i < N.size(); ++i) (inN[i] ? tN : oN).push_back(N[i].second);
@@ -480,6 +568,42 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
   }
   g.n_tiles = int64_t(1) << g.n_outer;
   g.k_iters = int64_t(1) << g.n_ok;
+  int64_t splits = 1;
+  if (dmma) {
+    // K4 warp layout: 8x8 sub-tiles, up to 4x4 per warp, TY x TX warps (<= 8)
+    en.kind = 3;
+    en.RM = std::min(4, 1 << (g.tm - 3));
+    en.RN = std::min(4, 1 << (g.tn - 3));
+    g.TY = (1 << (g.tm - 3)) / en.RM;
+    g.TX = (1 << (g.tn - 3)) / en.RN;
+    g.KG = 1;
+    en.block = 32 * g.TX * g.TY;
+    // split-K to fill the machine: choose the split count (<= 8, <= K iterations) with the
+    // smallest wave-quantisation loss over ~148 x (CTAs per SM) slots
+    const int cps = en.block >= 256 ? 1 : (en.block >= 128 ? 2 : 4);
+    const double slots = 148.0 * cps;
+    double best = 1e30;
+    for (int64_t s2 = 1; s2 <= std::min<int64_t>(8, g.k_iters); ++s2) {
+      const double items = (double)(g.n_tiles * s2);
+      const double waves = std::ceil(items / slots);
+      const double loss = waves * slots / items * (1.0 + 0.01 * (double)(s2 - 1));
+      if (loss < best - 1e-9) { best = loss; splits = s2; }
+    }
+    const int64_t cbytes = (g.n_tiles << (g.tm + g.tn)) * esize;
+    while (splits > 1 && splits * cbytes > (int64_t(1) << 32)) --splits;
+    g.splits = (int32_t)splits;
+    g.vecA = g.vecB = 0;
+    g.dbuf = 1;
+    const int64_t stage = (int64_t(1) << g.nA) + (int64_t(1) << g.nB);
+    en.smem = (size_t)(2 * stage * esize + 2 * 4 * (int64_t(1) << g.tk));
+    en.n_out = g.n_tiles << (g.tm + g.tn);
+    View vc;
+    int64_t st = 1;
+    for (auto b : tN) { vc.bits.push_back({b, st}); st <<= 1; }
+    for (auto b : tM) { vc.bits.push_back({b, st}); st <<= 1; }
+    for (auto b : outer) { vc.bits.push_back({b, st}); st <<= 1; }
+    return vc;
+  }
   en.RM = std::min(4, 1 << g.tm);
   en.RN = std::min(4, 1 << g.tn);
   g.TX = (1 << g.tn) / en.RN;
@@ -489,7 +613,6 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
   en.block = std::max(32, (TXY * g.KG + 31) / 32 * 32);
   // cross-CTA split-K when the grid is small and the K loop is long
   const int64_t target = 148 * 4;
-  int64_t splits = 1;
   if (g.n_tiles < target && g.k_iters > 1) {
     splits = std::min<int64_t>(g.k_iters, (target + g.n_tiles - 1) / g.n_tiles);
     const int64_t cbytes = (g.n_tiles << (g.tm + g.tn)) * esize;
@@ -523,6 +646,7 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
 
 Layout compile(const jt_plan& plan, int esize) {
   const bool use_tc = tc_enabled();
+  const bool use_dmma = dmma_enabled();
   const char* fg = std::getenv("JETB200_TCG_FORCE");  // tests: route K3-eligible nodes to K3g
   const bool force_tcg = fg && fg[0] == '1';
   Layout L;
@@ -603,6 +727,7 @@ Layout compile(const jt_plan& plan, int esize) {
     View tv;
     if (use_tc && !force_tcg && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
     else if (use_tc && plan_tcg(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
+    else if (esize == 16 && use_dmma && plan_dmma(en, views[en.opA], views[en.opB], tv)) views[v] = tv;
     else views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
     en.maxpos = n.maxpos;
     en.flop = n.flop;
@@ -950,8 +1075,9 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
       en.grid_x = std::min<int64_t>(en.tc.n_tiles, (int64_t)nb * n_sm);
       continue;
     }
-    const void* fn = dt == JT_C64 ? reinterpret_cast<const void*>(pick_gett<float>(en.RM, en.RN))
-                                  : reinterpret_cast<const void*>(pick_gett<double>(en.RM, en.RN));
+    const void* fn = en.kind == 3   ? reinterpret_cast<const void*>(pick_dmma(en.RM, en.RN))
+                     : dt == JT_C64 ? reinterpret_cast<const void*>(pick_gett<float>(en.RM, en.RN))
+                                    : reinterpret_cast<const void*>(pick_gett<double>(en.RM, en.RN));
     JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, en.block, en.smem));
     if (nb < 1) fail(JT_EINTERNAL, "exec: a contraction tile does not fit on an SM");
     const int64_t resident = (int64_t)nb * n_sm;
@@ -1082,7 +1208,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     g.C = ex->ws + en.out_off;
     g.P = ex->ws + en.part_off;
     dim3 grid((unsigned)en.grid_x, (unsigned)g.splits);
-    GettFn fn = pick_gett<R>(en.RM, en.RN);
+    GettFn fn = en.kind == 3 ? pick_dmma(en.RM, en.RN) : pick_gett<R>(en.RM, en.RN);
     ev_begin(ex);
     launch_pdl(fn, grid, dim3(en.block), en.smem, ex->stream, ex->pdl, g);
     ev_end(ex, en);
@@ -1197,7 +1323,12 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
       ex->stats.k2_timed_launches++;
       ex->stats.k2_timed_bytes += ex->ev_work[i].first;
       ex->stats.k2_timed_flop += ex->ev_work[i].second;
-      if (ex->ev_kind[i] >= 1) {
+      if (ex->ev_kind[i] == 3) {
+        ex->stats.k4_time_ms += ms;
+        ex->stats.k4_timed_launches++;
+        ex->stats.k4_timed_bytes += ex->ev_work[i].first;
+        ex->stats.k4_timed_flop += ex->ev_work[i].second;
+      } else if (ex->ev_kind[i] >= 1) {
         ex->stats.k3_time_ms += ms;
         ex->stats.k3_timed_launches++;
         ex->stats.k3_timed_bytes += ex->ev_work[i].first;

@@ -50,7 +50,9 @@ class ExecStats(ctypes.Structure):
                 ("flop_executed", c_dbl), ("bytes_executed", c_dbl), ("k2_time_ms", c_dbl),
                 ("k2_timed_launches", c_i64), ("k2_timed_bytes", c_dbl), ("k2_timed_flop", c_dbl),
                 ("k3_time_ms", c_dbl), ("k3_timed_launches", c_i64), ("k3_timed_bytes", c_dbl),
-                ("k3_timed_flop", c_dbl), ("h2d_bytes", c_i64)]
+                ("k3_timed_flop", c_dbl), ("h2d_bytes", c_i64),
+                ("k4_time_ms", c_dbl), ("k4_timed_launches", c_i64), ("k4_timed_bytes", c_dbl),
+                ("k4_timed_flop", c_dbl)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -121,3 +121,28 @@ def test_emulated_k3g_matches_oracle_c2_slice(jet, monkeypatch):
     ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[9]))
     v = jet.debug_emulate_host(plan, 9, 10, "c64")
     assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4
+
+
+@pytest.mark.parametrize("dim,width,d", [(2, 3, 4), (2, 2, 8), (3, 2, 4)])
+def test_emulated_k4_descriptors_match_oracle_gbs(jet, dim, width, d):
+    """K4 (c128 DMMA) shares K2's descriptor format; the emulated descriptors of plans that
+    route nodes to K4 must reproduce the oracle's s_sigma (d = 8: 3-bit qudit labels, f4)."""
+    circ = generate_gbs(dim, width, 1, 0.5, d, seed=3)
+    M = circ.n_wires
+    n_k4 = 0
+    for seed in range(2):
+        bits = random_bitstring(M, d, seed + 7)
+        net = jet.Network.from_circuit(circ, bits)
+        plan = jet.Plan.greedy(net, seed=seed, trials=8, n_sliced=seed)
+        nodes = plan.describe_exec("c128")["nodes"]
+        for n in nodes:
+            if n["kind"] == 3:
+                n_k4 += 1
+                assert 3 <= n["tm"] <= 7 and 3 <= n["tn"] <= 7 and n["tm"] + n["tn"] <= 13
+                assert 2 <= n["tk"] <= 5 and n["KG"] == 1 and n["smem"] <= 200 * 1024
+                assert n["block"] == 32 * (2 ** (n["tm"] - 3) // n["RM"]) * (2 ** (n["tn"] - 3) // n["RN"])
+                assert n["n_out"] == 2 ** (n["tm"] + n["tn"] + n["n_outer"])
+        ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
+        v = jet.debug_emulate_host(plan, 0, len(ref), "c128")
+        assert np.max(np.abs(v - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1e-300)
+    assert n_k4 > 0, "no node was routed to K4"

@@ -176,6 +176,53 @@ def test_gbs_parity_and_closed_forms(jet, dim, width):
             assert abs(amp - math.cosh(r) ** (-M / 2)) < 1e-12            # P8 vacuum
 
 
+# ----------------------------------------------------------------------------- K4 (c128 DMMA)
+@pytest.mark.parametrize("dim,width,d,k", [(2, 3, 4, 0), (2, 4, 4, 2), (2, 2, 8, 1), (3, 2, 4, 1), (2, 4, 4, 3)])
+def test_k4_dmma_parity_vs_oracle_and_k2(jet, monkeypatch, dim, width, d, k):
+    """c128 contractions on the FP64 tensor cores (K4) against the oracle (1e-10) and against
+    the CUDA-core K2 path (JETB200_DMMA=0) on the same plan."""
+    circ = generate_gbs(dim, width, 1, 0.5, d, seed=5)
+    M = circ.n_wires
+    bits = random_bitstring(M, d, 11)
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=16, n_sliced=k)
+    assert any(n["kind"] == 3 for n in plan.describe_exec("c128")["nodes"])
+    ref_vals = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
+    ref = complex(np.sum(ref_vals))
+    amp, vals, _ = run(jet, plan, "c128")
+    scale = np.max(np.abs(ref_vals))
+    assert np.max(np.abs(vals - ref_vals)) <= 1e-10 * scale
+    assert rel(amp, ref) < 1e-10
+    monkeypatch.setenv("JETB200_DMMA", "0")
+    assert not any(n["kind"] == 3 for n in plan.describe_exec("c128")["nodes"])
+    amp2, vals2, _ = run(jet, plan, "c128")
+    assert np.max(np.abs(vals2 - vals)) <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("name", ["G88d4"])
+def test_gbs88_closed_forms_full_size(jet, name):
+    """f4: GBS-88-m1 (64 modes, cutoff 4) at full size on K4/K2, pinned by the
+    P8 closed forms (vacuum, sampled two-photon outputs, odd photon numbers) within 1e-10."""
+    from gbs_closed import p8_cases
+
+    circ, _ = workload(name)
+    cases = p8_cases(circ, 0.5, max_pairs=12, seed=3)
+    plan = None
+    for bits, want in cases:
+        net = jet.Network.from_circuit(circ, bits)
+        if plan is None:
+            plan = jet.Plan.greedy(net, seed=1, trials=64)
+            assert any(n["kind"] == 3 for n in plan.describe_exec("c128")["nodes"])
+            ssa, sl = plan.ssa_path, plan.sliced_labels
+        else:   # same network shape, new bra digits: the same path (PAPER.md l.312)
+            plan = jet.Plan.create(net, ssa, sl)
+        amp, _, _ = run(jet, plan, "c128")
+        if want == 0.0:
+            assert abs(amp) < 1e-14
+        else:
+            assert rel(amp, want) < 1e-10, (bits, amp, want)
+
+
 # ----------------------------------------------------------------------------- C2 (Sycamore-53 m=10)
 @pytest.fixture(scope="module")
 def c2_plan(jet):

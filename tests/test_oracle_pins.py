@@ -253,25 +253,12 @@ def test_sycamore_gate_set():
 
 
 # ---------------------------------------------------------------- P8 GBS closed forms
-def single_photon_matrix(circ):
-    """W[j][i] = <1_j|U|1_i>, the product of the BS single-photon blocks (l.219-246)."""
-    m, d = circ.n_wires, circ.d
-    W = np.eye(m, dtype=np.complex128)
-    for g in circ.gates:
-        if len(g.wires) != 2:
-            continue
-        a, b = g.wires
-        blk = np.array([[g.u[d * 1 + 0, d * 1 + 0], g.u[d * 1 + 0, d * 0 + 1]],
-                        [g.u[d * 0 + 1, d * 1 + 0], g.u[d * 0 + 1, d * 0 + 1]]])
-        e = np.eye(m, dtype=np.complex128)
-        e[np.ix_([a, b], [a, b])] = blk
-        W = e @ W
-    return W
+from gbs_closed import p8_cases, single_photon_matrix  # noqa: E402
 
 
-@pytest.mark.parametrize("dim,width", [(2, 2), (3, 2), (1, 4)])
-def test_gbs_closed_forms(dim, width):
-    r, d = 0.5, 4
+@pytest.mark.parametrize("dim,width,d", [(2, 2, 4), (3, 2, 4), (1, 4, 4), (2, 2, 8)])
+def test_gbs_closed_forms(dim, width, d):
+    r = 0.5
     circ = generate_gbs(dim, width, 1, r, d, seed=9)
     M = circ.n_wires
     pref = math.cosh(r) ** (-M / 2)
