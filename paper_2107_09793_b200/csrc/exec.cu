@@ -403,15 +403,30 @@ bool plan_dmma(ExecNode& en, const View& va, const View& vb, View& out) {
   auto grow = [&](std::vector<char>& in, int target) {
     for (size_t i = 0; i < in.size() && cnt(in) < target; ++i) in[i] = 1;
   };
-  grow(inK, std::min<int>((int)K.size(), 4));
+  grow(inK, std::min<int>((int)K.size(), 5));
   grow(inM, std::min<int>((int)M.size(), 7));
   grow(inN, std::min<int>((int)N.size(), std::max(3, 13 - cnt(inM))));
   if (cnt(inN) > 7) return false;
   const int tm = cnt(inM), tn = cnt(inN), tk = cnt(inK);
   if (tm < 3 || tn < 3 || tk < 2 || tk > 5 || tm > 7 || tm + tn > 13) return false;
-  if (tm + tk > 12 || tk + tn > 12) return false;
-  const int64_t smem = 2 * ((int64_t(1) << (tm + tk)) + (int64_t(1) << (tk + tn))) * 16;
-  if (smem > 200 * 1024) return false;
+  // tile-K 32 complex when the two stages fit (fewer per-item barriers and address updates per
+  // MMA), else 16
+  auto smem_of = [&](int k) { return 2 * ((int64_t(1) << (tm + k)) + (int64_t(1) << (k + tn))) * 16; };
+  int tkk = tk;
+  for (int i = (int)K.size() - 1; i >= 0 && (tm + tkk > 12 || tkk + tn > 12 || smem_of(tkk) > 200 * 1024); --i)
+    if (inK[i] && tkk > 4) {
+      bool low = false;   // never drop a coalescing bit
+      std::vector<std::pair<int64_t, int64_t>> s2;
+      for (auto& x : va.bits) s2.push_back({x.second, x.first});
+      std::sort(s2.begin(), s2.end());
+      for (size_t q = 0; q < s2.size() && q < 3; ++q) low |= s2[q].second == K[i].second;
+      s2.clear();
+      for (auto& x : vb.bits) s2.push_back({x.second, x.first});
+      std::sort(s2.begin(), s2.end());
+      for (size_t q = 0; q < s2.size() && q < 3; ++q) low |= s2[q].second == K[i].second;
+      if (!low) { inK[i] = 0; --tkk; }
+    }
+  if (tm + tkk > 12 || tkk + tn > 12 || smem_of(tkk) > 200 * 1024) return false;
   out = fill_gett(en, sa, sb, M, N, K, inM, inN, inK, 16, true);
   return true;
 }

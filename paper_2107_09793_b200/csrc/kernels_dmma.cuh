@@ -26,7 +26,7 @@
 namespace jt {
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
@@ -38,8 +38,16 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
   using C2 = double2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int64_t tgA[2][64], tgB[2][64];
+  __shared__ int64_t dkA[kMaxOuter], dkB[kMaxOuter];  // K-loop step deltas by trailing-zero count
   const int tid = threadIdx.x;
   const int nthr = blockDim.x;
+  for (int t = tid; t < p.n_ok; t += nthr) {
+    // it-1 -> it flips bits 0..t-1 (1 -> 0) and bit t (0 -> 1), t = ctz(it)
+    int64_t da = p.ok_sA[t], db = p.ok_sB[t];
+    for (int i = 0; i < t; ++i) { da -= p.ok_sA[i]; db -= p.ok_sB[i]; }
+    dkA[t] = da;
+    dkB[t] = db;
+  }
   for (int i = tid; i < 64; i += nthr) {
     for (int h = 0; h < 2; ++h) {
       int64_t g = 0, gb = 0;
@@ -82,15 +90,28 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
   for (int j = 0; j < SNT; ++j) offN[j] = swz<C2>(deposit(wn * 8 * SNT + 8 * j + g4, p.pN, p.tn));
   const C2* __restrict__ A = reinterpret_cast<const C2*>(p.A) + slice_off(p.sv, true);
   const C2* __restrict__ B = reinterpret_cast<const C2*>(p.B) + slice_off(p.sv, false);
-  auto offsets = [&](int64_t w, int64_t& oa, int64_t& ob) {
-    const int64_t tile = blockIdx.x + (w / nk) * gridDim.x;
-    const int64_t it = it0 + w % nk;
-    oa = 0;
-    ob = 0;
+  // operand offsets of the next item to load: recomputed from the bits at a tile start,
+  // stepped by one delta per K iteration otherwise (no per-item bit loops)
+  int64_t ld_tile = blockIdx.x, ld_k = 0, ld_oa = 0, ld_ob = 0;
+  auto tile_start = [&]() {
+    const int64_t it = it0;
+    ld_oa = 0;
+    ld_ob = 0;
     for (int j = 0; j < p.n_outer; ++j)
-      if ((tile >> j) & 1) { oa += p.o_sA[j]; ob += p.o_sB[j]; }
+      if ((ld_tile >> j) & 1) { ld_oa += p.o_sA[j]; ld_ob += p.o_sB[j]; }
     for (int j = 0; j < p.n_ok; ++j)
-      if ((it >> j) & 1) { oa += p.ok_sA[j]; ob += p.ok_sB[j]; }
+      if ((it >> j) & 1) { ld_oa += p.ok_sA[j]; ld_ob += p.ok_sB[j]; }
+  };
+  auto advance = [&]() {
+    if (++ld_k == nk) {
+      ld_k = 0;
+      ld_tile += gridDim.x;
+      tile_start();
+    } else {
+      const int t = __ffsll((unsigned long long)(it0 + ld_k)) - 1;
+      ld_oa += dkA[t];
+      ld_ob += dkB[t];
+    }
   };
   double cr[SMT][SNT][2], ci[SMT][SNT][2];
 #pragma unroll
@@ -98,20 +119,18 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
 #pragma unroll
     for (int j = 0; j < SNT; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
   if (total > 0) {
-    int64_t oa, ob;
-    offsets(0, oa, ob);
-    load_tile(sA0, A + oa, p.nA, false, tgA, tid, nthr);
-    load_tile(sA0 + szA, B + ob, p.nB, false, tgB, tid, nthr);
+    tile_start();
+    load_tile(sA0, A + ld_oa, p.nA, false, tgA, tid, nthr);
+    load_tile(sA0 + szA, B + ld_ob, p.nB, false, tgB, tid, nthr);
     cp_async_commit();
   }
   for (int64_t w = 0; w < total; ++w) {
     const int buf = (int)(w & 1);
     if (w + 1 < total) {
-      int64_t oa, ob;
-      offsets(w + 1, oa, ob);
+      advance();
       C2* nxt = sA0 + (buf ^ 1) * stage;
-      load_tile(nxt, A + oa, p.nA, false, tgA, tid, nthr);
-      load_tile(nxt + szA, B + ob, p.nB, false, tgB, tid, nthr);
+      load_tile(nxt, A + ld_oa, p.nA, false, tgA, tid, nthr);
+      load_tile(nxt + szA, B + ld_ob, p.nB, false, tgB, tid, nthr);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -128,17 +147,26 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
       for (int i = 0; i < SMT; ++i) a[i] = sA[ka ^ offM[i]];
 #pragma unroll
       for (int j = 0; j < SNT; ++j) b[j] = sB[kb ^ offN[j]];
+      // four passes over the sub-tiles, so that the two MMAs into one accumulator are
+      // 2*SMT*SNT instructions apart (DMMA latency hidden by independent accumulators)
+#pragma unroll
+      for (int i = 0; i < SMT; ++i)
+#pragma unroll
+        for (int j = 0; j < SNT; ++j) dmma884(cr[i][j], a[i].x, b[j].x);
+#pragma unroll
+      for (int i = 0; i < SMT; ++i)
+#pragma unroll
+        for (int j = 0; j < SNT; ++j) dmma884(ci[i][j], a[i].x, b[j].y);
 #pragma unroll
       for (int i = 0; i < SMT; ++i) {
         const double nai = -a[i].y;
 #pragma unroll
-        for (int j = 0; j < SNT; ++j) {
-          dmma884(cr[i][j], a[i].x, b[j].x);
-          dmma884(ci[i][j], a[i].x, b[j].y);
-          dmma884(cr[i][j], nai, b[j].y);
-          dmma884(ci[i][j], a[i].y, b[j].x);
-        }
+        for (int j = 0; j < SNT; ++j) dmma884(cr[i][j], nai, b[j].y);
       }
+#pragma unroll
+      for (int i = 0; i < SMT; ++i)
+#pragma unroll
+        for (int j = 0; j < SNT; ++j) dmma884(ci[i][j], a[i].y, b[j].x);
     }
     if (w % nk != nk - 1) {
       __syncthreads();  // this stage is refilled by the prefetch two items later

@@ -80,8 +80,9 @@ def as_complex(acc_np):
 # Roofline model of the current kernels (c64 on B200): K2 streams at most the HBM bandwidth
 # and computes complex FP32 on CUDA cores.  Used only to choose among host plans.
 MODEL_HBM_BPS = 6.0e12
-MODEL_FLOPS = {"c64": 40e12, "c128": 30e12}   # K2 (CUDA cores), measured order of magnitude
+MODEL_FLOPS = {"c64": 40e12, "c128": 13e12}   # K2 (CUDA cores), measured order of magnitude
 MODEL_FLOPS_TC = 250e12                         # K3 (tcgen05 3xTF32, algorithmic complex FLOP/s)
+MODEL_FLOPS_DMMA = 30e12                        # K4 (FP64 DMMA, c128), measured 25-31 TFLOP/s
 
 
 def modeled_time(plan, dtype="c64", bw=MODEL_HBM_BPS, flops=None):
@@ -93,7 +94,8 @@ def modeled_time(plan, dtype="c64", bw=MODEL_HBM_BPS, flops=None):
     t = 0.0
     for n in d["nodes"]:
         runs = dq ** (n["maxpos"] + 1)
-        f = MODEL_FLOPS_TC if n.get("kind", 0) >= 1 else flops
+        kind = n.get("kind", 0)
+        f = MODEL_FLOPS_DMMA if kind == 3 else (MODEL_FLOPS_TC if kind in (1, 2) else flops)
         t += runs * (max(n["bytes"] / bw, n["flop"] / f) + 3e-6)   # + launch gap
     return t, d["total_bytes"]
 

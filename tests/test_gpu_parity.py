@@ -192,7 +192,10 @@ def test_k4_dmma_parity_vs_oracle_and_k2(jet, monkeypatch, dim, width, d, k):
     amp, vals, _ = run(jet, plan, "c128")
     scale = np.max(np.abs(ref_vals))
     assert np.max(np.abs(vals - ref_vals)) <= 1e-10 * scale
-    assert rel(amp, ref) < 1e-10
+    if abs(ref) <= 1e-14 * scale:   # odd total photon number: exactly 0 (P8)
+        assert abs(amp) <= 1e-12 * scale
+    else:
+        assert rel(amp, ref) < 1e-10
     monkeypatch.setenv("JETB200_DMMA", "0")
     assert not any(n["kind"] == 3 for n in plan.describe_exec("c128")["nodes"])
     amp2, vals2, _ = run(jet, plan, "c128")
