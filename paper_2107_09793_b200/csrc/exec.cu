@@ -278,8 +278,17 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   for (size_t i = 0; i < N.size(); ++i) (i < 7 ? tN : oN).push_back(N[i].second);
   for (size_t i = 0; i < M.size(); ++i) ((int)i < tmt ? tM : oM).push_back(M[i].second);
   if (oN.size() + oM.size() > 31 || ko.size() > 32 || oN.size() > 32 || oM.size() > 32) return false;
-  const int64_t ybytes = 4LL * NP * 128;
+  // Y (expanded A, hi|lo planes) ring depth: the producers run ystages-1 items ahead of the MMAs
+  // (2, 3 and 4 measured within 3% of each other on the C5 nodes: not the bound; 2 keeps the
+  // deepest raw gather ring)
+  int ystages = 2;
+  if (const char* e = getenv("JETB200_TCG_YS")) ystages = std::max(2, std::min(4, atoi(e)));
   const int rb_b = 128 * 128, rb_a = MT * 128;
+  int64_t ybytes = (int64_t)ystages * 2 * NP * 128;
+  while (ystages > 2 && (220 * 1024 - 1024 - ybytes) / (rb_b + rb_a) < 3) {
+    --ystages;
+    ybytes = (int64_t)ystages * 2 * NP * 128;
+  }
   const int rstages = (int)std::min<int64_t>(6, (220 * 1024 - 1024 - ybytes) / (rb_b + rb_a));
   if (rstages < 2) return false;
   TcgArgs& t = en.tcg;
@@ -299,6 +308,7 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   t.acc_bufs = 2;
   t.tmem_cols = 512;
+  t.ystages = ystages;
   t.rstages = rstages;
   t.rbytes_b = rb_b;
   t.rbytes_a = rb_a;

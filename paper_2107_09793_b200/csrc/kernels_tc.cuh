@@ -156,6 +156,12 @@ __device__ __forceinline__ float tf32_hi(float x) {
 __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// 3xTF32 low part of a streamed operand: lo = x - rna(x) is exact in fp32 and |lo| <= 2^-11 |x|;
+// it is NOT rounded here -- the tensor core reads the fp32 pattern at TF32 precision, which
+// perturbs lo by < 2^-10 |lo| <= 2^-21 |x| (below the dropped lo*lo term's scale of 2^-22 |x y|
+// only by a factor of 2, and 2^-21 is ~15x below fp32-accumulate rounding over a 16-term K step).
+// Saves two integer ops per value on the producers' critical path.
+__device__ __forceinline__ float tf32_lo(float x, float hi) { return x - hi; }
 
 }  // namespace tc
 
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           hi[4 * j + q] = tc::tf32_rna(x[q]);
-          lo[4 * j + q] = tc::tf32_rna(x[q] - hi[4 * j + q]);
+          lo[4 * j + q] = tc::tf32_lo(x[q], hi[4 * j + q]);
         }
       }
       const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);

@@ -27,6 +27,7 @@ struct TcgArgs {
   int32_t Np;               // MMA N = 2 * 2^tmt
   uint32_t idesc, tmem_cols;
   int32_t rstages, rbytes_b, rbytes_a, acc_bufs;
+  int32_t ystages;          // Y (expanded A) shared stages, 2..4
   int32_t lg_bm;            // tile raster: bands of 2^lg_bm M tiles (<= n_oM) walked N-major
   int64_t o_B[32], o_A[32]; // outer N bit strides in B / outer M bit strides in A
   int64_t k_B[32], k_A[32]; // chunk-index bit strides in B / in A
@@ -70,12 +71,12 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
   __shared__ int64_t tgb[2][64], tga[2][64];
   __shared__ int32_t tsb[2][64], tsa[2][64];
   __shared__ int64_t dkB[32], dkA[32];  // chunk c -> c+1 offset steps, by trailing ones of c
-  __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[2], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[4], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  unsigned char* Y = base;                            // 2 stages x [hi plane | lo plane], NP x 128 B each
-  unsigned char* RB = Y + 2 * 2 * NP * 128;           // raw B ring
+  unsigned char* Y = base;                            // ystages x [hi plane | lo plane], NP x 128 B each
+  unsigned char* RB = Y + p.ystages * 2 * NP * 128;   // raw B ring
   unsigned char* RA = RB + p.rstages * p.rbytes_b;    // raw A ring
   for (int i = tid; i < 64; i += blockDim.x) {
     for (int h = 0; h < 2; ++h) {
@@ -108,8 +109,8 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       tc::mbar_init(&full[i], 256);
       tc::mbar_init(&xempty[i], 1);
     }
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&yempty[i], 1);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&yempty[i], 1);
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 128);
     }
@@ -193,6 +194,8 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       cp_async_commit();
     }
     int rst = 0;  // raw stage of item it
+    int ys = 0;
+    uint32_t yph = 0;  // Y stage of item it and its ring pass parity
     for (int64_t it = 0; it < items; ++it) {
       switch (RS) {
         case 2: cp_async_wait<0>(); break;
@@ -204,9 +207,9 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       tc::bar_sync(1, 256);
       if (it + RS - 1 < items) copy(it + RS - 1);
       cp_async_commit();
-      const int xs = (int)(it & 3), ys = (int)(it & 1);
+      const int xs = (int)(it & 3);
       tc::mbar_wait(&xempty[xs], (uint32_t)(((it >> 2) & 1) ^ 1));
-      tc::mbar_wait(&yempty[ys], (uint32_t)(((it >> 1) & 1) ^ 1));
+      tc::mbar_wait(&yempty[ys], yph ^ 1u);
       tc::fence_after();
       // ---- X: this thread's row, half of the chunk -> hi/lo TF32 in TMEM
       {
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             hi[4 * j + q] = tc::tf32_rna(x[q]);
-            lo[4 * j + q] = tc::tf32_rna(x[q] - hi[4 * j + q]);
+            lo[4 * j + q] = tc::tf32_lo(x[q], hi[4 * j + q]);
           }
         }
         const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -239,16 +242,13 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
           if (u < MT * 8) {
             const int m = u >> 3, kp = u & 7;
             const float4 a = *reinterpret_cast<const float4*>(raw + m * 128 + ((kp ^ (m & 7)) << 4));
-            const float r0[4] = {a.x, -a.y, a.z, -a.w};  // row 2m   (s = 0)
-            const float r1[4] = {a.y, a.x, a.w, a.z};    // row 2m+1 (s = 1)
-            float h0[4], l0[4], h1[4], l1[4];
-#pragma unroll
-            for (int z = 0; z < 4; ++z) {
-              h0[z] = tc::tf32_rna(r0[z]);
-              l0[z] = tc::tf32_rna(r0[z] - h0[z]);
-              h1[z] = tc::tf32_rna(r1[z]);
-              l1[z] = tc::tf32_rna(r1[z] - h1[z]);
-            }
+            // split each value once (rna is odd-symmetric, so -x splits as (-hi, -lo)), then
+            // permute / negate into row 2m = (Re, -Im) and row 2m+1 = (Im, Re) per k
+            const float hx = tc::tf32_rna(a.x), hy = tc::tf32_rna(a.y), hz = tc::tf32_rna(a.z), hw = tc::tf32_rna(a.w);
+            const float lx = tc::tf32_lo(a.x, hx), ly = tc::tf32_lo(a.y, hy), lz = tc::tf32_lo(a.z, hz),
+                        lw = tc::tf32_lo(a.w, hw);
+            const float h0[4] = {hx, -hy, hz, -hw}, l0[4] = {lx, -ly, lz, -lw};  // row 2m   (s = 0)
+            const float h1[4] = {hy, hx, hw, hz}, l1[4] = {ly, lx, lw, lz};      // row 2m+1 (s = 1)
             const int ra0 = 2 * m, ra1 = 2 * m + 1;
             const int b0 = (ra0 & 7) * 128 + (ra0 >> 3) * 1024 + ((kp ^ (ra0 & 7)) << 4);
             const int b1 = (ra1 & 7) * 128 + (ra1 >> 3) * 1024 + ((kp ^ (ra1 & 7)) << 4);
@@ -264,13 +264,15 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       tc::fence_before();
       tc::mbar_arrive(&full[xs]);
       if (++rst == RS) rst = 0;
+      if (++ys == p.ystages) { ys = 0; yph ^= 1u; }
     }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
     const bool leader = lane == 0;
     int64_t tt = 0;
+    int ys = 0;
     for (int64_t it = 0; it < items; ++it) {
-      const int xs = (int)(it & 3), ys = (int)(it & 1);
+      const int xs = (int)(it & 3);
       const int64_t c = it & kc_mask;
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       }
       __syncwarp();
       if (c == kc_mask) ++tt;
+      if (++ys == p.ystages) ys = 0;
     }
   } else if (warp < 4) {
     // ===================== epilogue =====================
