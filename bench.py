@@ -463,6 +463,8 @@ def run_ours(args, cfg):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "algorithmic_gbs_step": tot_bytes / (ms_max / 1e3) / 1e9,
+            # f3 memory report of the plan (jt_exec_memory, fig. m10_memory), GB
+            "memory_gb": {k: round(v / 1e9, 3) for k, v in plan.memory(cfg["dtype"]).items()},
         }
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -170,6 +170,24 @@ void jt_plan_destroy(jt_plan* plan);
 /* Device workspace bytes for this plan and dtype (leaves + intermediates with lifetime
    reuse + prefix cache + split-K scratch + slice values). */
 jt_status jt_exec_workspace_bytes(const jt_plan* plan, jt_dtype dtype, int64_t* bytes);
+/* Memory report of the compiled plan (host only, fig. m10_memory: peak memory
+   with and without deletion of intermediates, and the extra memory that shared work costs).
+   All in bytes of the exec dtype.  Intermediates are deleted after their last use: the arena
+   places every node output by first fit over its live interval in the execution order, so
+   peak_live_bytes <= arena_bytes <= no_deletion_bytes.  A caller that wants several slice
+   subsets in flight on one device can size them a priori: each extra executor needs
+   total_bytes - leaf_bytes more (leaves can be shared read-only). */
+typedef struct {
+  int64_t total_bytes;             /* = jt_exec_workspace_bytes */
+  int64_t leaf_bytes;              /* network leaves (full, unsliced data) */
+  int64_t arena_bytes;             /* intermediates as placed (with deletion) */
+  int64_t peak_live_bytes;         /* max over execution positions of the live intermediates */
+  int64_t no_deletion_bytes;       /* every intermediate kept ("without deletion") */
+  int64_t cache_bytes;             /* prefix-cache entries resident for the whole run (shared work) */
+  int64_t peak_live_noshare_bytes; /* peak live if nothing were kept across slices (no shared work) */
+  int64_t scratch_bytes;           /* split-K partial buffers */
+} jt_memory;
+jt_status jt_exec_memory(const jt_plan* plan, jt_dtype dtype, jt_memory* out);
 /* Host only: write the compiled per-node launch plan (tiles, grid, split-K, bytes, FLOP,
    prefix-cache level) and the workspace layout as JSON (for analysis and DESIGN.md). */
 jt_status jt_exec_describe(const jt_plan* plan, jt_dtype dtype, const char* path);

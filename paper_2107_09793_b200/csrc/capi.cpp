@@ -13,6 +13,7 @@ void network_export(const jt_network* net, const char* path);
 void plan_export(const jt_plan* plan, const char* path);
 int64_t workspace_bytes(const jt_plan& plan, jt_dtype dt);
 void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path);
+void exec_memory(const jt_plan& plan, jt_dtype dt, jt_memory* out);
 void debug_emulate_host(const jt_plan& plan, jt_dtype dt, int64_t b, int64_t e, double* h_vals, bool reuse);
 jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, int64_t ws_bytes, void* stream);
 void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_vals, bool reuse);
@@ -175,6 +176,12 @@ jt_status jt_exec_workspace_bytes(const jt_plan* plan, jt_dtype dtype, int64_t* 
   return guarded([&] {
     NEED(plan && bytes, "jt_exec_workspace_bytes");
     *bytes = workspace_bytes(*plan, dtype);
+  });
+}
+jt_status jt_exec_memory(const jt_plan* plan, jt_dtype dtype, jt_memory* out) {
+  return guarded([&] {
+    NEED(plan && out, "jt_exec_memory");
+    exec_memory(*plan, dtype, out);
   });
 }
 jt_status jt_exec_describe(const jt_plan* plan, jt_dtype dtype, const char* path) {

@@ -69,6 +69,8 @@ struct Layout {
   int64_t leaf_bytes = 0, inter_bytes = 0, scratch_bytes = 0;
   int64_t inter_base = 0, scratch_base = 0, vals_base = 0, acc_base = 0, state_base = 0, total = 0;
   int64_t vals_cap = 1;  // slice-value ring (per call, indexed from the call's first slice)
+  // memory report (f3, PAPER.md l.291-298 fig. m10_memory)
+  int64_t mem_no_deletion = 0, mem_peak_live = 0, mem_cache = 0, mem_peak_live_noshare = 0;
 };
 
 using GettFn = void (*)(GettArgs);
@@ -798,6 +800,31 @@ Layout compile(const jt_plan& plan, int esize) {
     inter = std::max(inter, cand + b.size);
     placed.push_back(i);
   }
+  // memory report: every intermediate kept (no deletion); the peak of live intermediates over
+  // the execution order (deletion after the last use); the prefix-cache entries resident for the
+  // whole run; the same peak if nothing were kept across slices (no shared work)
+  {
+    std::vector<int64_t> delta(ord.size() + 1, 0), delta_ns(ord.size() + 1, 0);
+    int64_t always = 0, always_ns = 0;
+    for (const Buf& b : bufs) {
+      L.mem_no_deletion += b.size;
+      const PlanNode& n = plan.nodes[b.v];
+      const bool cache = n.parent >= 0 && plan.nodes[n.parent].maxpos > n.maxpos;
+      if (cache) L.mem_cache += b.size;
+      if (b.end == INF) always += b.size;
+      else { delta[b.start] += b.size; delta[b.end + 1] -= b.size; }
+      const int64_t s0 = pos[b.v], e0 = n.parent < 0 ? (int64_t)ord.size() - 1 : pos[n.parent];
+      if (n.parent < 0) always_ns += b.size;
+      else { delta_ns[s0] += b.size; delta_ns[e0 + 1] -= b.size; }
+    }
+    int64_t cur = 0, cur_ns = 0;
+    for (size_t q = 0; q < ord.size(); ++q) {
+      cur += delta[q];
+      cur_ns += delta_ns[q];
+      L.mem_peak_live = std::max(L.mem_peak_live, cur + always);
+      L.mem_peak_live_noshare = std::max(L.mem_peak_live_noshare, cur_ns + always_ns);
+    }
+  }
   L.inter_base = align_up(L.leaf_bytes);
   L.inter_bytes = inter;
   for (const Buf& b : bufs) L.node_off[b.v] = L.inter_base + b.off;
@@ -1045,18 +1072,21 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
   Layout L = compile(plan, dt == JT_C64 ? 8 : 16);
   FILE* f = std::fopen(path, "w");
   if (!f) fail(JT_EUSAGE, std::string("cannot open ") + path);
-  std::fprintf(f, "{\"total_bytes\": %lld, \"leaf_bytes\": %lld, \"inter_bytes\": %lld, \"scratch_bytes\": %lld, \"nodes\": [",
-               (long long)L.total, (long long)L.leaf_bytes, (long long)L.inter_bytes, (long long)L.scratch_bytes);
+  std::fprintf(f, "{\"total_bytes\": %lld, \"leaf_bytes\": %lld, \"inter_bytes\": %lld, \"scratch_bytes\": %lld, "
+               "\"inter_base\": %lld, \"peak_live_bytes\": %lld, \"no_deletion_bytes\": %lld, \"cache_bytes\": %lld, \"nodes\": [",
+               (long long)L.total, (long long)L.leaf_bytes, (long long)L.inter_bytes, (long long)L.scratch_bytes,
+               (long long)L.inter_base, (long long)L.mem_peak_live, (long long)L.mem_no_deletion, (long long)L.mem_cache);
   for (size_t i = 0; i < L.order.size(); ++i) {
     const ExecNode& en = L.order[i];
     const GettArgs& g = en.args;
     std::fprintf(f, "%s{\"v\": %lld, \"maxpos\": %d, \"flop\": %.17g, \"bytes\": %.17g, \"n_out\": %lld, "
                  "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
-                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld}",
+                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld, \"parent\": %lld, \"pos\": %zu}",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
                  g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind,
                  en.kind == 2 ? en.tcg.tmt : en.tc.tm, en.kind == 2 ? 4 + en.tcg.lg_kc : en.tc.K,
-                 en.kind == 2 ? en.tcg.n_oN + en.tcg.n_oM : en.tc.n_outer, (long long)L.node_off[en.v]);
+                 en.kind == 2 ? en.tcg.n_oN + en.tcg.n_oM : en.tc.n_outer, (long long)L.node_off[en.v],
+                 (long long)plan.nodes[en.v].parent, i);
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
@@ -1064,6 +1094,20 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
 
 int64_t workspace_bytes(const jt_plan& plan, jt_dtype dt) {
   return compile(plan, dt == JT_C64 ? 8 : 16).total;
+}
+
+void exec_memory(const jt_plan& plan, jt_dtype dt, jt_memory* out) {
+  const Layout L = compile(plan, dt == JT_C64 ? 8 : 16);
+  jt_memory m{};
+  m.total_bytes = L.total;
+  m.leaf_bytes = L.leaf_bytes;
+  m.arena_bytes = L.inter_bytes;
+  m.peak_live_bytes = L.mem_peak_live;
+  m.no_deletion_bytes = L.mem_no_deletion;
+  m.cache_bytes = L.mem_cache;
+  m.peak_live_noshare_bytes = L.mem_peak_live_noshare;
+  m.scratch_bytes = L.scratch_bytes;
+  *out = m;
 }
 
 void upload_leaves(jt_exec* ex) {

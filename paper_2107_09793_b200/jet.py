@@ -77,6 +77,15 @@ _sig("jt_network_destroy", None, [c_vp])
 _sig("jt_plan_create", c_i32, [c_vp, P_i64, c_i64, P_i64, c_i32, ctypes.POINTER(c_vp)])
 _sig("jt_plan_greedy", c_i32, [c_vp, ctypes.POINTER(PlannerOpts), ctypes.POINTER(c_vp)])
 _sig("jt_plan_sizes", c_i32, [c_vp, P_i64, P_i32])
+class Memory(ctypes.Structure):
+    _fields_ = [("total_bytes", c_i64), ("leaf_bytes", c_i64), ("arena_bytes", c_i64), ("peak_live_bytes", c_i64),
+                ("no_deletion_bytes", c_i64), ("cache_bytes", c_i64), ("peak_live_noshare_bytes", c_i64),
+                ("scratch_bytes", c_i64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _sig("jt_plan_get", c_i32, [c_vp, P_i64, P_i64])
 _sig("jt_plan_cost", c_i32, [c_vp, ctypes.POINTER(Cost)])
 _sig("jt_plan_prefix_flop", c_i32, [c_vp, c_i64, c_i64, P_dbl])
@@ -84,6 +93,7 @@ _sig("jt_plan_export", c_i32, [c_vp, ctypes.c_char_p])
 _sig("jt_plan_destroy", None, [c_vp])
 _sig("jt_exec_workspace_bytes", c_i32, [c_vp, c_i32, P_i64])
 _sig("jt_exec_describe", c_i32, [c_vp, c_i32, ctypes.c_char_p])
+_sig("jt_exec_memory", c_i32, [c_vp, c_i32, ctypes.POINTER(Memory)])
 _sig("jt_exec_create", c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64, c_vp, ctypes.POINTER(c_vp)])
 _sig("jt_exec_contract", c_i32, [c_vp, c_i64, c_i64, c_vp, P_dbl])
 _sig("jt_exec_contract_noreuse", c_i32, [c_vp, c_i64, c_i64, c_vp, P_dbl])
@@ -102,7 +112,7 @@ _sig("jt_permute", c_i32, [c_i32, c_vp, c_vp, c_i32, P_i32, c_vp])
 EXPORTED = ["jt_last_error", "jt_version", "jt_network_create", "jt_network_add_gate", "jt_network_close",
             "jt_network_close_batch", "jt_network_info", "jt_network_export", "jt_network_destroy", "jt_plan_create", "jt_plan_greedy",
             "jt_plan_sizes", "jt_plan_get", "jt_plan_cost", "jt_plan_prefix_flop", "jt_plan_export",
-            "jt_plan_destroy", "jt_exec_workspace_bytes", "jt_exec_describe", "jt_exec_create", "jt_exec_contract",
+            "jt_plan_destroy", "jt_exec_workspace_bytes", "jt_exec_describe", "jt_exec_memory", "jt_exec_create", "jt_exec_contract",
             "jt_exec_contract_noreuse", "jt_exec_contract_host", "jt_exec_stats_get",
             "jt_exec_upload_leaves", "jt_exec_set_profiling", "jt_exec_stats_reset",
             "jt_exec_invalidate", "jt_exec_destroy", "jt_amplitude", "jt_permute", "jt_debug_emulate_host",
@@ -252,6 +262,19 @@ class Plan:
         b = c_i64()
         _check(_lib.jt_exec_workspace_bytes(self._h, _DT[dtype], ctypes.byref(b)))
         return b.value
+
+    def memory(self, dtype="c64"):
+        """jt_exec_memory: workspace, peak live, no-deletion and prefix-cache bytes (fig. m10_memory)."""
+        m = Memory()
+        _check(_lib.jt_exec_memory(self._h, _DT[dtype], ctypes.byref(m)))
+        return m.as_dict()
+
+    def concurrent_slices(self, budget_bytes, dtype="c64"):
+        """How many slice subsets (executors sharing the read-only leaves) fit in budget_bytes of
+        device memory, decided a priori from the memory report."""
+        m = self.memory(dtype)
+        per = m["total_bytes"] - m["leaf_bytes"]
+        return max(0, (budget_bytes - m["leaf_bytes"]) // per) if per > 0 else 0
 
     def describe_exec(self, dtype="c64"):
         import json
