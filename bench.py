@@ -28,7 +28,9 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: circuit key, sliced labels, dtype, slices per step, workload name
     "C2": dict(circ="C2", k=6, dtype="c64", sps=64, workload="sycamore53_m10_2^6slices"),
-    "C3": dict(circ="C3", k=10, dtype="c64", sps=16, workload="sycamore53_m14_2^10slices"),
+    # C3: one step = one full single amplitude (all 1024 slices of this rank's share, prefix cache
+    # cold at the start), so ms_per_step IS the amplitude time
+    "C3": dict(circ="C3", k=10, dtype="c64", sps=1024, workload="sycamore53_m14_2^10slices"),
     "C5": dict(circ="C5", k=None, dtype="c64", sps=1, cap=30, seeds=2, workload="sycamore53_m20_width30_subset"),
     "C4": dict(circ="C4", k=None, dtype="c128", sps=1, cap=28, seeds=2, workload="gbs444_d4_width28_subset"),
     # GBS-88-m1 at cutoff 4 (full amplitude per step) and 8 (sliced)

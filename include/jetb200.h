@@ -70,6 +70,11 @@ typedef struct {
   double model_tc_tflops;
   double model_launch_us;
   double model_esize;     /* bytes per element (8 = c64, 16 = c128) */
+  /* slice selection objective ("we greedily selected our slices
+     along a fixed contraction path to maximize shared work"): 0 -> sliced cost N_sl sum_v c(v);
+     1 -> shared-work aware: the executed cost of the one-copy prefix cache,
+     sum_v c(v) prod_{pos(l) <= maxpos(S(v))} d_l, with the candidate appended innermost */
+  int32_t slice_objective;
 } jt_planner_opts;
 
 /* Cost counters (PAPER.md l.140-146 Eq. sliced_flops, l.205-212 Eq. task_based;
@@ -155,6 +160,12 @@ jt_status jt_plan_create(const jt_network* net, const int64_t* ssa_path, int64_t
 /* Host greedy planner: absorption of rank<=2 tensors, randomised greedy, subtree
    reconfiguration, greedy slicing, slice-loop order. */
 jt_status jt_plan_greedy(const jt_network* net, const jt_planner_opts* opts, jt_plan** out);
+/* Greedy slicing along a FIXED contraction path: the path is kept as given
+   (same validation as jt_plan_create), labels are sliced one at a time by opts->slice_objective
+   until opts->n_sliced labels or the width is <= opts->width_cap (in log2 elements), and the
+   slice-loop order is chosen as in jt_plan_greedy.  trials / reconfiguration fields are ignored. */
+jt_status jt_plan_slice(const jt_network* net, const int64_t* ssa_path, int64_t n_steps,
+                        const jt_planner_opts* opts, jt_plan** out);
 /* Sizes for jt_plan_get. */
 jt_status jt_plan_sizes(const jt_plan* plan, int64_t* n_steps, int32_t* n_sliced);
 /* Caller-sized buffers: ssa_path[2*n_steps], sliced_labels[n_sliced]. */

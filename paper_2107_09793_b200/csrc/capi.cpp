@@ -137,6 +137,39 @@ jt_status jt_plan_greedy(const jt_network* net, const jt_planner_opts* opts, jt_
   });
 }
 
+jt_status jt_plan_slice(const jt_network* net, const int64_t* ssa_path, int64_t n_steps, const jt_planner_opts* opts,
+                        jt_plan** out) {
+  return guarded([&] {
+    NEED(net && out && opts, "jt_plan_slice");
+    if (!net->closed) fail(JT_EVALIDATION, "jt_plan_slice: network is not closed");
+    if (n_steps < 0) fail(JT_EUSAGE, "jt_plan_slice: negative size");
+    if (n_steps > 0) NEED(ssa_path, "jt_plan_slice");
+    auto* p = new jt_plan();
+    try {
+      p->net = *net;
+      p->path.assign(ssa_path, ssa_path + 2 * n_steps);
+      p->sliced.assign(net->batch_labels.begin(), net->batch_labels.end());
+      p->n_summed = 0;
+      build_plan_tree(*p);   // validates the path before the slicer walks it
+      std::vector<int64_t> sl;
+      slice_fixed_path(*net, p->path, *opts, sl);
+      jt_plan* q = new jt_plan();
+      q->net = *net;
+      q->path = p->path;
+      q->sliced = sl;
+      q->n_summed = (int)sl.size();
+      q->sliced.insert(q->sliced.end(), net->batch_labels.begin(), net->batch_labels.end());
+      delete p;
+      p = q;
+      build_plan_tree(*p);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
 jt_status jt_plan_sizes(const jt_plan* plan, int64_t* n_steps, int32_t* n_sliced) {
   return guarded([&] {
     NEED(plan, "jt_plan_sizes");

@@ -83,5 +83,7 @@ void slice_digits(const jt_plan& plan, int64_t s, std::vector<int>& dig);
 // planner.cpp
 void greedy_plan(const jt_network& net, const jt_planner_opts& opts, std::vector<int64_t>& path,
                  std::vector<int64_t>& sliced);
+void slice_fixed_path(const jt_network& net, const std::vector<int64_t>& path, const jt_planner_opts& opts,
+                      std::vector<int64_t>& sliced);
 
 }  // namespace jt

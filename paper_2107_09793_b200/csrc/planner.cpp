@@ -426,10 +426,34 @@ void reconf_sweeps(Tree& T, int sweeps, int F, const CostModel& cm, const uint64
 // Greedy slicing: repeatedly slice the label, taken from the current largest
 // intermediates, that minimises (max width, cost) while over the width cap, else cost; each
 // pick is followed by one reconfiguration sweep of the sliced tree.
+// Executed cost of the one-copy prefix cache for the sliced labels `labs` taken as the loop
+// order (labs[0] outermost): sum_v c(v) d^(maxpos(S(v)) + 1), S(v) = the labels of labs on the
+// leaves under v (PAPER.md l.205-212 Eq. task_based with the prefix-cache multiplicity, a6).
+double prefix_tree_cost(const Tree& T, const CostModel& cm, const uint64_t* mask, const std::vector<int>& labs,
+                        const std::vector<int>& po) {
+  const int W = T.W;
+  const int k = (int)labs.size();
+  std::vector<uint64_t> dep(T.nodes.size(), 0);
+  for (int i = 0; i < T.n_leaves; ++i)
+    for (int c = 0; c < k; ++c)
+      if (T.L(i)[labs[c] / 64] & (uint64_t(1) << (labs[c] % 64))) dep[i] |= uint64_t(1) << c;
+  double tot = 0;
+  for (int v : po) {
+    const TNode& n = T.nodes[v];
+    dep[v] = dep[n.left] | dep[n.right];
+    const int mp = dep[v] ? 63 - __builtin_clzll(dep[v]) : -1;
+    tot += cm.node_cost(pc_union_not(T.L(n.left), T.L(n.right), mask, W), pc_and_not(T.L(n.left), mask, W),
+                        pc_and_not(T.L(n.right), mask, W), pc_and_not(T.L(v), mask, W)) *
+           cm.dpow[mp + 1];
+  }
+  return tot;
+}
+
 void slice_tree(Tree& T, const CostModel& cm, int kmax, int capw, int sweeps, int F, int NL,
-                std::vector<uint64_t>& mask, std::vector<int>& chosen) {
+                std::vector<uint64_t>& mask, std::vector<int>& chosen, int objective = 0) {
   const int W = T.W;
   if (kmax == 0 || T.n_leaves <= 1) return;
+  std::vector<int> po;
   for (int iter = 0; iter < 62; ++iter) {
     int mw;
     tree_cost(T, cm, mask.data(), &mw);
@@ -453,11 +477,18 @@ void slice_tree(Tree& T, const CostModel& cm, int kmax, int capw, int sweeps, in
     double bc = 0;
     int bw = 0;
     const bool width_first = (capw < 0) || (mw > capw);
+    if (objective == 1) postorder(T, po);
+    std::vector<int> labs = chosen;
+    labs.push_back(-1);
     for (int l = 0; l < NL; ++l) {
       if (!cand[l]) continue;
       mask[l / 64] |= uint64_t(1) << (l % 64);
       int nw;
       double c = tree_cost(T, cm, mask.data(), &nw);
+      if (objective == 1 && chosen.size() < 62) {
+        labs.back() = l;
+        c = prefix_tree_cost(T, cm, mask.data(), labs, po);
+      }
       mask[l / 64] &= ~(uint64_t(1) << (l % 64));
       bool better;
       if (bl < 0) better = true;
@@ -537,6 +568,67 @@ Absorbed absorb(const jt_network& net) {
       ab.comp_labels.push_back(labs[i]);
     }
   return ab;
+}
+
+// Slice-loop order for the prefix cache (a6): labels by the cost that depends on them (heaviest
+// outermost), then adjacent swaps while the executed prefix-cache cost decreases.
+std::vector<int> loop_order(const Tree& best_tree, const CostModel& cm, const std::vector<uint64_t>& mask,
+                            const std::vector<int>& chosen, int n_leaves) {
+  const int k = (int)chosen.size();
+  const int W = best_tree.W;
+  std::vector<int> order(k);
+  struct { int W; } leaves{W};
+  if (k > 0) {
+    const int NN = (int)best_tree.nodes.size();
+    std::vector<uint64_t> dep(NN, 0);  // S(v) over chosen positions (chosen index)
+    std::vector<double> ncost(NN, 0);
+    std::vector<int> po;
+    postorder(best_tree, po);
+    for (int i = 0; i < n_leaves; ++i)
+      for (int c = 0; c < k; ++c)
+        if (best_tree.L(i)[chosen[c] / 64] & (uint64_t(1) << (chosen[c] % 64))) dep[i] |= uint64_t(1) << c;
+    for (int v : po) {
+      const TNode& n = best_tree.nodes[v];
+      dep[v] = dep[n.left] | dep[n.right];
+      ncost[v] = cm.node_cost(pc_union_not(best_tree.L(n.left), best_tree.L(n.right), mask.data(), leaves.W),
+                              pc_and_not(best_tree.L(n.left), mask.data(), leaves.W),
+                              pc_and_not(best_tree.L(n.right), mask.data(), leaves.W),
+                              pc_and_not(best_tree.L(v), mask.data(), leaves.W));
+    }
+    std::vector<double> wt(k, 0);
+    for (int v : po)
+      for (int c = 0; c < k; ++c)
+        if (dep[v] & (uint64_t(1) << c)) wt[c] += ncost[v];
+    for (int c = 0; c < k; ++c) order[c] = c;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return wt[a] > wt[b]; });
+    auto prefix_cost = [&](const std::vector<int>& ord) {
+      std::vector<int> pos(k);
+      for (int p = 0; p < k; ++p) pos[ord[p]] = p;
+      double tot = 0;
+      for (int v : po) {
+        int mp = -1;
+        for (int c = 0; c < k; ++c)
+          if (dep[v] & (uint64_t(1) << c)) mp = std::max(mp, pos[c]);
+        tot += ncost[v] * cm.dpow[mp + 1];
+      }
+      return tot;
+    };
+    double cur = prefix_cost(order);
+    for (bool improved = true; improved;) {
+      improved = false;
+      for (int p = 0; p + 1 < k; ++p) {
+        std::swap(order[p], order[p + 1]);
+        double c = prefix_cost(order);
+        if (c < cur * (1 - 1e-12)) {
+          cur = c;
+          improved = true;
+        } else {
+          std::swap(order[p], order[p + 1]);
+        }
+      }
+    }
+  }
+  return order;
 }
 
 }  // namespace
@@ -656,8 +748,17 @@ void greedy_plan(const jt_network& net0, const jt_planner_opts& o, std::vector<i
         trees[i] = tree_from_pairs(leaves, n_leaves, tpairs[idx[i]]);
         reconf_sweeps(trees[i], sweeps, F, cm, nomask.data());
         mask_c[i].assign(leaves.W, 0);
-        slice_tree(trees[i], cm, o.n_sliced, capw, sweeps, F, NL, mask_c[i], chosen_c[i]);
-        rcost[i] = tree_cost(trees[i], cm, mask_c[i].data(), nullptr) * cm.dpow[chosen_c[i].size()];
+        slice_tree(trees[i], cm, o.n_sliced, capw, sweeps, F, NL, mask_c[i], chosen_c[i], o.slice_objective);
+        if (o.slice_objective == 1) {   // compare candidates by their executed (prefix-cache) cost
+          std::vector<int> po;
+          postorder(trees[i], po);
+          const std::vector<int> ord = loop_order(trees[i], cm, mask_c[i], chosen_c[i], n_leaves);
+          std::vector<int> labs;
+          for (int c : ord) labs.push_back(chosen_c[i][c]);
+          rcost[i] = prefix_tree_cost(trees[i], cm, mask_c[i].data(), labs, po);
+        } else {
+          rcost[i] = tree_cost(trees[i], cm, mask_c[i].data(), nullptr) * cm.dpow[chosen_c[i].size()];
+        }
       }
     };
     {
@@ -675,57 +776,7 @@ void greedy_plan(const jt_network& net0, const jt_planner_opts& o, std::vector<i
 
   // ---- slice loop order: heaviest dependent FLOP outermost, then adjacent-swap search
   const int k = (int)chosen.size();
-  std::vector<int> order(k);
-  if (k > 0) {
-    const int NN = (int)best_tree.nodes.size();
-    std::vector<uint64_t> dep(NN, 0);  // S(v) over chosen positions (chosen index)
-    std::vector<double> ncost(NN, 0);
-    std::vector<int> po;
-    postorder(best_tree, po);
-    for (int i = 0; i < n_leaves; ++i)
-      for (int c = 0; c < k; ++c)
-        if (best_tree.L(i)[chosen[c] / 64] & (uint64_t(1) << (chosen[c] % 64))) dep[i] |= uint64_t(1) << c;
-    for (int v : po) {
-      const TNode& n = best_tree.nodes[v];
-      dep[v] = dep[n.left] | dep[n.right];
-      ncost[v] = cm.node_cost(pc_union_not(best_tree.L(n.left), best_tree.L(n.right), mask.data(), leaves.W),
-                              pc_and_not(best_tree.L(n.left), mask.data(), leaves.W),
-                              pc_and_not(best_tree.L(n.right), mask.data(), leaves.W),
-                              pc_and_not(best_tree.L(v), mask.data(), leaves.W));
-    }
-    std::vector<double> wt(k, 0);
-    for (int v : po)
-      for (int c = 0; c < k; ++c)
-        if (dep[v] & (uint64_t(1) << c)) wt[c] += ncost[v];
-    for (int c = 0; c < k; ++c) order[c] = c;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return wt[a] > wt[b]; });
-    auto prefix_cost = [&](const std::vector<int>& ord) {
-      std::vector<int> pos(k);
-      for (int p = 0; p < k; ++p) pos[ord[p]] = p;
-      double tot = 0;
-      for (int v : po) {
-        int mp = -1;
-        for (int c = 0; c < k; ++c)
-          if (dep[v] & (uint64_t(1) << c)) mp = std::max(mp, pos[c]);
-        tot += ncost[v] * cm.dpow[mp + 1];
-      }
-      return tot;
-    };
-    double cur = prefix_cost(order);
-    for (bool improved = true; improved;) {
-      improved = false;
-      for (int p = 0; p + 1 < k; ++p) {
-        std::swap(order[p], order[p + 1]);
-        double c = prefix_cost(order);
-        if (c < cur * (1 - 1e-12)) {
-          cur = c;
-          improved = true;
-        } else {
-          std::swap(order[p], order[p + 1]);
-        }
-      }
-    }
-  }
+  std::vector<int> order = loop_order(best_tree, cm, mask, chosen, n_leaves);
   sliced.clear();
   for (int p = 0; p < k; ++p) sliced.push_back(raw_of[chosen[order[p]]]);
 
@@ -741,6 +792,61 @@ void greedy_plan(const jt_network& net0, const jt_planner_opts& o, std::vector<i
     path.push_back(ssa[best_tree.nodes[v].right]);
     ssa[v] = next_id++;
   }
+}
+
+// Greedy slicing along a fixed path (jt_plan_slice).  The path is over raw
+// tensor ids (validated by the caller); no absorption and no reconfiguration: the tree is exactly
+// the given one.
+void slice_fixed_path(const jt_network& net0, const std::vector<int64_t>& path, const jt_planner_opts& o,
+                      std::vector<int64_t>& sliced) {
+  jt_network stripped;
+  const jt_network* np = &net0;
+  if (!net0.batch_labels.empty()) {
+    stripped = net0;
+    std::unordered_set<int64_t> bl(net0.batch_labels.begin(), net0.batch_labels.end());
+    for (auto& t : stripped.tensors) {
+      std::vector<int64_t> keep;
+      for (int64_t l : t.labels)
+        if (!bl.count(l)) keep.push_back(l);
+      t.labels = keep;
+    }
+    np = &stripped;
+  }
+  const jt_network& net = *np;
+  const int nt = (int)net.tensors.size();
+  std::unordered_map<int64_t, int> cid;
+  std::vector<int64_t> raw_of;
+  for (const auto& t : net.tensors)
+    for (int64_t l : t.labels)
+      if (!cid.count(l)) {
+        cid[l] = (int)raw_of.size();
+        raw_of.push_back(l);
+      }
+  const int NL = (int)raw_of.size();
+  BitPool leaves;
+  leaves.W = std::max(1, (NL + 63) / 64);
+  for (int i = 0; i < nt; ++i) {
+    size_t k = leaves.add();
+    for (int64_t l : net.tensors[i].labels) {
+      const int c = cid[l];
+      leaves.at(k)[c / 64] |= uint64_t(1) << (c % 64);
+    }
+  }
+  std::vector<std::pair<int, int>> pairs;
+  for (size_t q = 0; q + 1 < path.size(); q += 2) pairs.push_back({(int)path[q], (int)path[q + 1]});
+  Tree T = tree_from_pairs(leaves, nt, pairs);
+  CostModel cm;
+  cm.log2d = std::log2((double)net.d);
+  cm.R = o.bytes_weight > 0 ? o.bytes_weight : 0.0;
+  cm.dpow.resize(NL + 2);
+  for (int i = 0; i <= NL + 1; ++i) cm.dpow[i] = std::pow((double)net.d, (double)i);
+  const int capw = o.width_cap > 0 ? (int)std::floor(o.width_cap / cm.log2d + 1e-9) : -1;
+  std::vector<uint64_t> mask(leaves.W, 0);
+  std::vector<int> chosen;
+  slice_tree(T, cm, o.n_sliced, capw, 0, 8, NL, mask, chosen, o.slice_objective);
+  const std::vector<int> order = loop_order(T, cm, mask, chosen, nt);
+  sliced.clear();
+  for (size_t p = 0; p < order.size(); ++p) sliced.push_back(raw_of[chosen[order[p]]]);
 }
 
 }  // namespace jt

@@ -33,7 +33,7 @@ class PlannerOpts(ctypes.Structure):
                 ("width_cap", c_i32), ("reconf_sweeps", c_i32), ("reconf_leaves", c_i32),
                 ("time_budget_s", c_dbl), ("bytes_weight", c_dbl), ("candidates", c_i32),
                 ("model_hbm_gbs", c_dbl), ("model_cuda_tflops", c_dbl), ("model_tc_tflops", c_dbl),
-                ("model_launch_us", c_dbl), ("model_esize", c_dbl)]
+                ("model_launch_us", c_dbl), ("model_esize", c_dbl), ("slice_objective", c_i32)]
 
 
 class Cost(ctypes.Structure):
@@ -86,6 +86,7 @@ class Memory(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+_sig("jt_plan_slice", c_i32, [c_vp, P_i64, c_i64, ctypes.POINTER(PlannerOpts), ctypes.POINTER(c_vp)])
 _sig("jt_plan_get", c_i32, [c_vp, P_i64, P_i64])
 _sig("jt_plan_cost", c_i32, [c_vp, ctypes.POINTER(Cost)])
 _sig("jt_plan_prefix_flop", c_i32, [c_vp, c_i64, c_i64, P_dbl])
@@ -110,7 +111,7 @@ _sig("jt_amplitude", c_i32, [c_vp, c_i32, c_i32, P_dbl])
 _sig("jt_permute", c_i32, [c_i32, c_vp, c_vp, c_i32, P_i32, c_vp])
 
 EXPORTED = ["jt_last_error", "jt_version", "jt_network_create", "jt_network_add_gate", "jt_network_close",
-            "jt_network_close_batch", "jt_network_info", "jt_network_export", "jt_network_destroy", "jt_plan_create", "jt_plan_greedy",
+            "jt_network_close_batch", "jt_network_info", "jt_network_export", "jt_network_destroy", "jt_plan_create", "jt_plan_greedy", "jt_plan_slice",
             "jt_plan_sizes", "jt_plan_get", "jt_plan_cost", "jt_plan_prefix_flop", "jt_plan_export",
             "jt_plan_destroy", "jt_exec_workspace_bytes", "jt_exec_describe", "jt_exec_memory", "jt_exec_create", "jt_exec_contract",
             "jt_exec_contract_noreuse", "jt_exec_contract_host", "jt_exec_stats_get",
@@ -215,13 +216,27 @@ class Plan:
 
     @classmethod
     def greedy(cls, net, seed=1, trials=64, threads=0, n_sliced=0, width_cap=0, reconf_sweeps=-1,
-               reconf_leaves=0, time_budget_s=0.0, bytes_weight=0.0, candidates=0, model=None):
+               reconf_leaves=0, time_budget_s=0.0, bytes_weight=0.0, candidates=0, model=None,
+               slice_objective=0):
+        """jt_plan_greedy.  slice_objective: 0 = sliced cost, 1 = shared-work aware (executed
+        prefix-cache cost)."""
         m = model or {}
         o = PlannerOpts(seed, trials, threads, n_sliced, width_cap, reconf_sweeps, reconf_leaves, time_budget_s,
                         bytes_weight, candidates, m.get("hbm_gbs", 0.0), m.get("cuda_tflops", 0.0),
-                        m.get("tc_tflops", 0.0), m.get("launch_us", 0.0), m.get("esize", 0.0))
+                        m.get("tc_tflops", 0.0), m.get("launch_us", 0.0), m.get("esize", 0.0), slice_objective)
         h = c_vp()
         _check(_lib.jt_plan_greedy(net._h, ctypes.byref(o), ctypes.byref(h)))
+        return cls(h, net)
+
+    @classmethod
+    def slice_path(cls, net, ssa_path, n_sliced=0, width_cap=0, bytes_weight=0.0, slice_objective=1):
+        """jt_plan_slice: greedy slicing along a FIXED path, by default choosing
+        the labels that maximise shared work (the executed prefix-cache cost)."""
+        p = np.asarray(ssa_path, dtype=np.int64).reshape(-1)
+        o = PlannerOpts(0, 0, 0, n_sliced, width_cap, -1, 0, 0.0, bytes_weight, 0, 0.0, 0.0, 0.0, 0.0, 0.0,
+                        slice_objective)
+        h = c_vp()
+        _check(_lib.jt_plan_slice(net._h, p.ctypes.data_as(P_i64), len(p) // 2, ctypes.byref(o), ctypes.byref(h)))
         return cls(h, net)
 
     def sizes(self):

@@ -101,7 +101,7 @@ def modeled_time(plan, dtype="c64", bw=MODEL_HBM_BPS, flops=None):
 
 
 def plan_best(net, n_sliced, dtype="c64", seeds=(1, 2, 3, 4, 5, 6, 7, 8), trials=4096, weights=(5.0, 8.0, 10.0, 15.0),
-              width_cap=0, ws_limit=150e9, seed=None):
+              width_cap=0, ws_limit=150e9, seed=None, objectives=(0, 1)):
     """Run the host planner over seeds x roofline weights and keep the plan with the lowest
     modeled time (modeled_time) whose workspace fits ws_limit bytes.  The planner's landscape
     is rugged (x5 spread across seeds), so the outer search matters more than trials per run.
@@ -111,14 +111,18 @@ def plan_best(net, n_sliced, dtype="c64", seeds=(1, 2, 3, 4, 5, 6, 7, 8), trials
     if seed is not None:
         seeds = (seed,)
     best = None
+    if n_sliced == 0:
+        objectives = (0,)
     for sd in seeds:
         for w in weights:
-            p = jet.Plan.greedy(net, seed=sd, trials=trials, n_sliced=n_sliced, width_cap=width_cap, bytes_weight=w)
-            t, ws = modeled_time(p, dtype)
-            if ws > ws_limit:
-                continue
-            if best is None or t < best[0]:
-                best = (t, sd, w, p)
+            for obj in objectives:
+                p = jet.Plan.greedy(net, seed=sd, trials=trials, n_sliced=n_sliced, width_cap=width_cap,
+                                    bytes_weight=w, slice_objective=obj)
+                t, ws = modeled_time(p, dtype)
+                if ws > ws_limit:
+                    continue
+                if best is None or t < best[0]:
+                    best = (t, sd, w, obj, p)
     if best is None:
         raise RuntimeError("no plan fits the workspace limit")
-    return best[3], {"modeled_s": best[0], "seed": best[1], "bytes_weight": best[2]}
+    return best[4], {"modeled_s": best[0], "seed": best[1], "bytes_weight": best[2], "slice_objective": best[3]}
