@@ -154,8 +154,16 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
   using C2 = typename V2<R>::t;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int64_t tgA[2][64], tgB[2][64];
+  __shared__ int64_t dkA[kMaxOuter], dkB[kMaxOuter];  // K-loop step deltas by trailing-zero count
   const int tid = threadIdx.x;
   const int nthr = blockDim.x;
+  for (int t = tid; t < p.n_ok; t += nthr) {
+    // it-1 -> it flips bits 0..t-1 (1 -> 0) and bit t (0 -> 1), t = ctz(it)
+    int64_t da = p.ok_sA[t], db = p.ok_sB[t];
+    for (int i = 0; i < t; ++i) { da -= p.ok_sA[i]; db -= p.ok_sB[i]; }
+    dkA[t] = da;
+    dkB[t] = db;
+  }
   for (int i = tid; i < 64; i += nthr) {
     // global-offset tables: lo = tile bits 0..5, hi = tile bits 6..11 (stride order)
     for (int h = 0; h < 2; ++h) {
@@ -205,15 +213,28 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
   for (int c = 0; c < RN; ++c) offN[c] = swz<C2>(deposit(col(c), p.pN, p.tn));
   const C2* __restrict__ A = reinterpret_cast<const C2*>(p.A) + slice_off(p.sv, true);
   const C2* __restrict__ B = reinterpret_cast<const C2*>(p.B) + slice_off(p.sv, false);
-  auto offsets = [&](int64_t w, int64_t& tile, int64_t& oa, int64_t& ob) {
-    tile = blockIdx.x + (w / nk) * gridDim.x;
-    const int64_t it = it0 + w % nk;
-    oa = 0;
-    ob = 0;
+  // operand offsets of the next item to load: recomputed from the bits at a tile start, stepped
+  // by one delta per K iteration otherwise (no per-item bit loops)
+  int64_t ld_tile = blockIdx.x, ld_k = 0, ld_oa = 0, ld_ob = 0;
+  auto tile_start = [&]() {
+    const int64_t it = it0;
+    ld_oa = 0;
+    ld_ob = 0;
     for (int j = 0; j < p.n_outer; ++j)
-      if ((tile >> j) & 1) { oa += p.o_sA[j]; ob += p.o_sB[j]; }
+      if ((ld_tile >> j) & 1) { ld_oa += p.o_sA[j]; ld_ob += p.o_sB[j]; }
     for (int j = 0; j < p.n_ok; ++j)
-      if ((it >> j) & 1) { oa += p.ok_sA[j]; ob += p.ok_sB[j]; }
+      if ((it >> j) & 1) { ld_oa += p.ok_sA[j]; ld_ob += p.ok_sB[j]; }
+  };
+  auto advance = [&]() {
+    if (++ld_k == nk) {
+      ld_k = 0;
+      ld_tile += gridDim.x;
+      tile_start();
+    } else {
+      const int t = __ffsll((unsigned long long)(it0 + ld_k)) - 1;
+      ld_oa += dkA[t];
+      ld_ob += dkB[t];
+    }
   };
   C2 acc[RM][RN];
 #pragma unroll
@@ -221,20 +242,18 @@ __global__ void __launch_bounds__(256) gett_kernel(const __grid_constant__ GettA
 #pragma unroll
     for (int c = 0; c < RN; ++c) { acc[r][c].x = 0; acc[r][c].y = 0; }
   if (total > 0) {
-    int64_t t, oa, ob;
-    offsets(0, t, oa, ob);
-    load_tile(sA0, A + oa, p.nA, p.vecA, tgA, tid, nthr);
-    load_tile(sA0 + szA, B + ob, p.nB, p.vecB, tgB, tid, nthr);
+    tile_start();
+    load_tile(sA0, A + ld_oa, p.nA, p.vecA, tgA, tid, nthr);
+    load_tile(sA0 + szA, B + ld_ob, p.nB, p.vecB, tgB, tid, nthr);
     cp_async_commit();
   }
   for (int64_t w = 0; w < total; ++w) {
     const int buf = (int)(w & 1);
     if (w + 1 < total) {  // prefetch the next item into the other stage
-      int64_t t, oa, ob;
-      offsets(w + 1, t, oa, ob);
+      advance();
       C2* nxt = sA0 + (buf ^ 1) * stage;
-      load_tile(nxt, A + oa, p.nA, p.vecA, tgA, tid, nthr);
-      load_tile(nxt + szA, B + ob, p.nB, p.vecB, tgB, tid, nthr);
+      load_tile(nxt, A + ld_oa, p.nA, p.vecA, tgA, tid, nthr);
+      load_tile(nxt + szA, B + ld_ob, p.nB, p.vecB, tgB, tid, nthr);
       cp_async_commit();
       cp_async_wait<1>();
     } else {

@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "c1 or c2 or gbs or reuse or graph or errors or k4" > gpurun_out/pytest_k2inc.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_k2inc.log
+timeout 900 python bench.py --config C3 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_k2inc.json 2> gpurun_out/bench_c3_k2inc.log
