@@ -152,7 +152,7 @@ int ilog2_exact(int d) {
 }
 
 // K3 eligibility and descriptor (c64 only): small A fully inside the tile with 3..7 free
-// bits and 2..6 contracted bits, big B with >= 7 free bits (128-row MMA tiles).  Returns
+// bits and 2..8 contracted bits, big B with >= 7 free bits (128-row MMA tiles).  Returns
 // false if the contraction does not fit K3.
 bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out) {
   if (esize != 8) return false;
@@ -167,11 +167,15 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (auto& x : vb.bits)
     if (!sa.count(x.first)) N.push_back({x.second, x.first});
   const int tm = (int)M.size(), kt = (int)K.size();
+  // (1-2 free bits of A run through the padded-N path correctly but measured slower than K2 on
+  // the C3 streaming nodes -- 8-KB gather items -- so K3 takes 3..7)
   if (tm < 3 || tm > 7 || kt < 2 || kt > 8 || (int)N.size() < 7) return false;
   const int swz = kt >= 4 ? 1 : 0;        // SWIZZLE_128B needs 32 TF32 (16 complex) per row
   const int tkc = swz ? 4 : kt;
   const int n_kc = 1 << (kt - tkc);
-  const int Kpc = 2 << tkc, Np = 2 << tm;
+  // MMA N = 2 * 2^tm, padded to the M=128 minimum of 16 for 1-2 free bits of A (the padded Y
+  // rows are zero and the padded accumulator columns are never stored)
+  const int Kpc = 2 << tkc, Np = std::max(16, 2 << tm);
   const int yplane = Np * Kpc * 4;
   // TMEM: accumulators (2 when they fit beside >= 2 X stages) + X stages of 2*Kpc columns
   int acc_bufs = (2 * Np + 2 * 2 * Kpc <= 512) ? 2 : 1;

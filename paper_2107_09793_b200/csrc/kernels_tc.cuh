@@ -238,6 +238,10 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   // ---- Y = expanded small operand (hi/lo) for every K chunk: row = 2m+s, col = 2k+t
   {
     const int nm = 1 << p.tm, nk = 1 << p.K, nkc = 1 << p.tkc;
+    if (2 * nm < p.Np)  // padded MMA N: zero the Y rows past 2*nm
+      for (int i = tid; i < 2 * p.n_kc * p.yplane / 16; i += blockDim.x)
+        reinterpret_cast<float4*>(Yhi)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
     const int64_t aoff = slice_off(p.sv, true);
     for (int idx = tid; idx < nm * nk; idx += blockDim.x) {
       const int m = idx % nm, k = idx / nm;
