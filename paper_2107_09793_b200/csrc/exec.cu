@@ -59,7 +59,20 @@ struct ExecNode {
   int64_t n_out = 1;     // output elements
   double flop = 0, bytes = 0;
   int maxpos = -1;
+  // bit keys the consumer (parent) contracts: the producer puts one of them at stride 1 in its
+  // output when it can (consumer-ordered layout -> 16-B k-pair gathers in a K3 consumer)
+  std::vector<int64_t> pref_low;
 };
+
+// Move the first bit of `t` that the consumer contracts to the front (it gets stride 1 in the
+// output view); the others keep their order.
+void prefer_low(std::vector<int64_t>& t, const std::vector<int64_t>& pref) {
+  for (size_t i = 0; i < t.size(); ++i)
+    if (std::find(pref.begin(), pref.end(), t[i]) != pref.end()) {
+      std::rotate(t.begin(), t.begin() + i, t.begin() + i + 1);
+      return;
+    }
+}
 
 struct Layout {
   int esize = 8;
@@ -193,6 +206,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   std::vector<int64_t> tN, oN;
   for (size_t i = 0; i < N.size(); ++i) (i < 7 ? tN : oN).push_back(N[i].second);
   if ((int)oN.size() > 31) return false;
+  prefer_low(tN, en.pref_low);
   TcArgs& t = en.tc;
   std::memset(&t, 0, sizeof(t));
   t.tm = tm;
@@ -225,6 +239,15 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
     t.gX[j] = tb[j].first;
     t.sX[j] = tb[j].second;
   }
+  // 16-B k-pair gathers: the lowest chunk-tile bit is K bit 0 (raw offset 8) at stride 1; every
+  // other bit of B then has an even stride, so pairs stay 16-B aligned on both sides
+  {
+    // opt-in: measured slower on C3 (12.3 s vs 10.3 s per amplitude with consumer-ordered
+    // layouts, profiles/r01_bench_c3_vec*.json), so off unless JETB200_K3_VEC=1
+    const char* e = getenv("JETB200_K3_VEC");
+    t.vecB = (tb[0].first == 1 && tb[0].second == 8 && e && e[0] == '1') ? 1 : 0;
+  }
+  en.args.vecB = t.vecB;  // (reported by jt_exec_describe)
   for (int j = 0; j < kt - tkc; ++j) t.o_kB[j] = sb[K[tkc + j].second];
   for (int i = 0; i < tm; ++i) t.aM[i] = sa[M[i].second];
   for (int i = 0; i < kt; ++i) t.aK[i] = sa[K[i].second];
@@ -551,6 +574,7 @@ View fill_gett(ExecNode& en, std::map<int64_t, int64_t>& sa, std::map<int64_t, i
   std::vector<int64_t> tM, tN, tK, oM, oN, oK;
   for (size_t i = 0; i < M.size(); ++i) (inM[i] ? tM : oM).push_back(M[i].second);
   for (size_t i = 0; i < N.size(); ++i) (inN[i] ? tN : oN).push_back(N[i].second);
+  prefer_low(tN, en.pref_low);
   for (size_t i = 0; i < K.size(); ++i) (inK[i] ? tK : oK).push_back(K[i].second);
   GettArgs& g = en.args;
   std::memset(&g, 0, sizeof(g));
@@ -752,6 +776,16 @@ Layout compile(const jt_plan& plan, int esize) {
     int fl = nfree(n.left, n.right), fr = nfree(n.right, n.left);
     en.opA = fl <= fr ? n.left : n.right;
     en.opB = fl <= fr ? n.right : n.left;
+    // consumer-ordered output layouts: opt-in (JETB200_CONSUMER_LAYOUT=1); measured neutral to
+    // slightly slower on C3 without the 16-B gathers (10.34 s vs 10.03 s)
+    const char* cl = std::getenv("JETB200_CONSUMER_LAYOUT");
+    if (n.parent >= 0 && cl && cl[0] == '1') {
+      const PlanNode& par = plan.nodes[n.parent];
+      const int64_t sib = par.left == v ? par.right : par.left;
+      for (int64_t l : n.labels)
+        if (std::find(plan.nodes[sib].labels.begin(), plan.nodes[sib].labels.end(), l) != plan.nodes[sib].labels.end())
+          for (int j = 0; j < lb; ++j) en.pref_low.push_back(l * lb + j);
+    }
     if (en.opA < nt) en.sliceA = leaf_slices[en.opA];
     if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
     if (en.sliceA.size() > 4 || en.sliceB.size() > 4) fail(JT_EUSAGE, "exec: more than 4 sliced labels on one leaf");

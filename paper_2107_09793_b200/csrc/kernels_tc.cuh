@@ -48,6 +48,8 @@ struct TcArgs {
   int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
   int32_t sX[kTcMaxTile];                      //   ... and its byte offset in the raw stage (XOR-combined)
   int64_t aM[8], aK[8];                        // A strides of its M bits / K bits
+  int32_t vecB;                                // 1: chunk-tile bit 0 is a K bit at global stride 1
+                                               //    -> gather k-pairs as 16-B copies
   SliceView sv;
 };
 
@@ -286,9 +288,11 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     // per-thread gather offsets are the same for every item: keep them in registers
     int64_t goff[PER];
     int32_t soff[PER];
+    const bool vec = p.vecB != 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      const int e = ptid + i * 256;
+      // 16-B mode: the first PER/2 entries are element pairs (2q, 2q+1), q = ptid + i*256
+      const int e = vec ? (i < PER / 2 ? 2 * (ptid + i * 256) : 0) : ptid + i * 256;
       goff[i] = tg[0][e & 63] + tg[1][e >> 6];
       soff[i] = ts[0][e & 63] ^ ts[1][e >> 6];
     }
@@ -307,8 +311,13 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     auto copy = [&]() {
       unsigned char* raw = R + wst * p.rbytes;
       const float2* srcp = p.B + (cbase + kc_off[cc]);
+      if (vec) {
 #pragma unroll
-      for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], srcp + goff[i]);
+        for (int i = 0; i < PER / 2; ++i) cp_async16(raw + soff[i], srcp + goff[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) cp_async8(raw + soff[i], srcp + goff[i]);
+      }
       if (++wst == RS) wst = 0;
       if (++cc == p.n_kc) {
         cc = 0;

@@ -284,6 +284,22 @@ def test_k3_tensor_cores_vs_cuda_cores(jet, c2_plan, monkeypatch):
     assert rel(amp1, amp0) < 5e-5
 
 
+def test_k3_consumer_layout_and_pair_gathers_parity(jet, monkeypatch):
+    """Opt-in paths: consumer-ordered output layouts (a bit the parent contracts at stride 1) and
+    K3's 16-B k-pair gathers, against the oracle on the full C2 slice set (1e-4)."""
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    monkeypatch.setenv("JETB200_CONSUMER_LAYOUT", "1")
+    monkeypatch.setenv("JETB200_K3_VEC", "1")
+    plan = jet.Plan.greedy(net, seed=1, trials=256, n_sliced=6, bytes_weight=5.0)
+    nodes = plan.describe_exec("c64")["nodes"]
+    assert any(n["kind"] == 1 and n["vecB"] == 1 for n in nodes)
+    ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
+    amp, vals, _ = run(jet, plan, "c64")
+    assert np.max(np.abs(vals - ref) / np.abs(ref).max()) < 1e-4
+    assert rel(amp, complex(np.sum(ref))) < 1e-4
+
+
 def test_cuda_graph_replay_bitwise(jet, monkeypatch):
     """Per-level CUDA graphs (device-side slice digits) give the same s_sigma bit for bit as
     direct launches, across split ranges, and count the same executed FLOP."""
