@@ -8,8 +8,9 @@
 A step = one pass of the whole hot path (every executed contraction node, the slice
 accumulate and the all-reduce) over one block of consecutive slices of the amplitude; the
 prefix cache persists across steps exactly as inside one amplitude run.  Rank g contracts
-the g-th contiguous block of the canonical slice order (weak scaling: fixed slices per GPU
-per step).  Timing: CUDA events on the exec stream, barrier + synchronize on both sides,
+the g-th contiguous block of the canonical slice order.  For the default C3 workload a step is
+the rank's whole share, i.e. one full amplitude across all ranks (strong scaling: total work
+fixed); configs whose step is a fixed block per rank report weak scaling.  Timing: CUDA events on the exec stream, barrier + synchronize on both sides,
 max over ranks.  Rank 0 prints ONE JSON line.
 """
 
@@ -285,7 +286,8 @@ def run_reference(args, cfg):
     print(json.dumps({
         "impl": "reference", "metric": "Sycamore-53 m=14 amplitude time; slices/s and cGEMM TFLOP/s",
         "value": value, "unit": "slices/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sec_tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * sec_tot / args.steps, "higher_is_better": True,
+        "scaling": "strong" if (args.slices_per_step or cfg["sps"]) >= c["n_sl"] else "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded Sycamore-style RQC)",
         "config": {"workload": cfg["workload"], "n_sl": c["n_sl"], "flop_per_slice_prefix": flop_per_slice},
         "cpu_baseline": {"value": value, "unit": "slices/s", "cores": cores, "kind": "oracle", "sample": sample},
@@ -447,7 +449,10 @@ def run_ours(args, cfg):
         out = {
             "metric": "Sycamore-53 m=14 amplitude time; slices/s and cGEMM TFLOP/s",
             "value": value, "unit": "slices/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            # a step over every rank's whole share is one full amplitude: total work fixed as N
+            # grows (strong); a step of a fixed block per rank is weak scaling
+            "scaling": "strong" if sps >= rng_len else "weak",
             "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (seeded Sycamore-style RQC, A1-A5)",
             "config": {
                 "workload": cfg["workload"], "n_sl": n_sl, "slices_per_step_per_gpu": sps,
