@@ -95,6 +95,7 @@ TcgFn pick_tcg(int tmt) {
     case 4: return gett_tcg_kernel<4>;
     case 5: return gett_tcg_kernel<5>;
     case 6: return gett_tcg_kernel<6>;
+    case 7: return gett_tcg_kernel<7>;
   }
   fail(JT_EINTERNAL, "no tcg instance");
 }
@@ -143,8 +144,8 @@ void set_smem_attrs() {
     const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<3>),
                           reinterpret_cast<const void*>(gett_tc_kernel<4>)};
     for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
-    const void* tcgs[3] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
-                           reinterpret_cast<const void*>(gett_tcg_kernel<6>)};
+    const void* tcgs[4] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
+                           reinterpret_cast<const void*>(gett_tcg_kernel<6>), reinterpret_cast<const void*>(gett_tcg_kernel<7>)};
     for (const void* f : tcgs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, 0>),
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -288,7 +289,11 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   for (auto& x : vb.bits)
     if (!sa.count(x.first)) N.push_back({x.second, x.first});
   if ((int)M.size() < 4 || (int)N.size() < 7 || (int)K.size() < 4) return false;
-  const int tmt = std::min<int>((int)M.size(), 6);
+  // tile columns: up to 64 complex (MMA N 128, two TMEM accumulators) by default; 128 complex
+  // (MMA N 256, one accumulator) with JETB200_TCG_TMT=7 -- half the producer work per MMA FLOP
+  int tmt_max = 6;
+  if (const char* e = getenv("JETB200_TCG_TMT")) tmt_max = std::max(4, std::min(7, atoi(e)));
+  const int tmt = std::min<int>((int)M.size(), tmt_max);
   const int MT = 1 << tmt, NP = 2 * MT;
   std::sort(M.begin(), M.end());
   std::sort(N.begin(), N.end());
@@ -335,7 +340,7 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   t.nAb = tmt + 4;
   t.Np = NP;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  t.acc_bufs = 2;
+  t.acc_bufs = NP <= 128 ? 2 : 1;   // 512 TMEM columns = accumulators + 4 X stages of 64
   t.tmem_cols = 512;
   t.ystages = ystages;
   t.rstages = rstages;
