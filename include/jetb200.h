@@ -119,6 +119,11 @@ typedef struct {
   int64_t k4_timed_launches;
   double k4_timed_bytes;
   double k4_timed_flop;
+  double k3g_time_ms;         /* ... the subset of the K3 launches that ran on K3g (both operands
+                                 streamed; the tensor-bound GEMM-shaped nodes) */
+  int64_t k3g_timed_launches;
+  double k3g_timed_bytes;
+  double k3g_timed_flop;
 } jt_exec_stats;
 
 const char* jt_last_error(void);

@@ -275,7 +275,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
 }
 
 // K3g eligibility and descriptor (c64): both operands streamed; output tiles of 128 rows of B's
-// free bits x 2^tmt (16..64) complex columns of A's free bits; K in chunks of 16 complex.
+// free bits x 2^tmt (16..128) complex columns of A's free bits; K in chunks of 16 complex.
 bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out) {
   if (esize != 8) return false;
   std::map<int64_t, int64_t> sa, sb;
@@ -289,9 +289,10 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   for (auto& x : vb.bits)
     if (!sa.count(x.first)) N.push_back({x.second, x.first});
   if ((int)M.size() < 4 || (int)N.size() < 7 || (int)K.size() < 4) return false;
-  // tile columns: up to 64 complex (MMA N 128, two TMEM accumulators) by default; 128 complex
-  // (MMA N 256, one accumulator) with JETB200_TCG_TMT=7 -- half the producer work per MMA FLOP
-  int tmt_max = 6;
+  // tile columns: up to 128 complex (MMA N 256, one TMEM accumulator beside 4 X stages): the
+  // producers' gather + split work per MMA FLOP drops by a third against 64 columns (two
+  // accumulators); measured 124 -> 167-172 TFLOP/s on the C5 nodes.  JETB200_TCG_TMT caps it.
+  int tmt_max = 7;
   if (const char* e = getenv("JETB200_TCG_TMT")) tmt_max = std::max(4, std::min(7, atoi(e)));
   const int tmt = std::min<int>((int)M.size(), tmt_max);
   const int MT = 1 << tmt, NP = 2 * MT;
@@ -1441,6 +1442,12 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
         ex->stats.k4_timed_bytes += ex->ev_work[i].first;
         ex->stats.k4_timed_flop += ex->ev_work[i].second;
       } else if (ex->ev_kind[i] >= 1) {
+        if (ex->ev_kind[i] == 2) {
+          ex->stats.k3g_time_ms += ms;
+          ex->stats.k3g_timed_launches++;
+          ex->stats.k3g_timed_bytes += ex->ev_work[i].first;
+          ex->stats.k3g_timed_flop += ex->ev_work[i].second;
+        }
         ex->stats.k3_time_ms += ms;
         ex->stats.k3_timed_launches++;
         ex->stats.k3_timed_bytes += ex->ev_work[i].first;

@@ -52,7 +52,8 @@ class ExecStats(ctypes.Structure):
                 ("k3_time_ms", c_dbl), ("k3_timed_launches", c_i64), ("k3_timed_bytes", c_dbl),
                 ("k3_timed_flop", c_dbl), ("h2d_bytes", c_i64),
                 ("k4_time_ms", c_dbl), ("k4_timed_launches", c_i64), ("k4_timed_bytes", c_dbl),
-                ("k4_timed_flop", c_dbl)]
+                ("k4_timed_flop", c_dbl), ("k3g_time_ms", c_dbl), ("k3g_timed_launches", c_i64),
+                ("k3g_timed_bytes", c_dbl), ("k3g_timed_flop", c_dbl)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
