@@ -76,12 +76,15 @@ def make_plan(jet, cfg, args):
     net = jet.Network.from_circuit(circ, bits)
     from paper_2107_09793_b200.runtime import plan_best
 
+    from paper_2107_09793_b200.runtime import plan_shared
+
     k = cfg["k"]
     t0 = time.time()
-    plan, info = plan_best(net, k if k is not None else -1, dtype=cfg["dtype"],
-                           seeds=tuple(range(args.seed, args.seed + (args.plan_seeds or cfg.get("seeds", 8)))),
-                           trials=args.trials,
-                           width_cap=cfg.get("cap", args.width_cap) if k is None else 0)
+    # rank 0 plans, the other ranks receive the path + sliced labels (one planner per node)
+    plan, info = plan_shared(net, lambda: plan_best(
+        net, k if k is not None else -1, dtype=cfg["dtype"],
+        seeds=tuple(range(args.seed, args.seed + (args.plan_seeds or cfg.get("seeds", 8)))),
+        trials=args.trials, width_cap=cfg.get("cap", args.width_cap) if k is None else 0))
     return circ, bits, net, plan, time.time() - t0
 
 

@@ -57,6 +57,31 @@ def run_amplitude(plan, dtype="c64", exec_=None, slices=None):
     return complex(a[0], a[1]), info
 
 
+def plan_shared(net, make_plan, group=None):
+    """Plan once, use everywhere: rank 0 runs `make_plan()` (the host planner, seconds to a
+    minute and all host cores) and broadcasts the plan -- its SSA path and sliced labels, the
+    problem inputs of P:176 -- and every other rank rebuilds the identical plan with
+    jt_plan_create, so N ranks on one node do not run N planners against each other.
+    Returns (plan, info) on every rank (info is rank 0's)."""
+    import torch.distributed as dist
+
+    from . import jet
+
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if world == 1:
+        return make_plan()
+    rank = dist.get_rank(group)
+    obj = [None]
+    if rank == 0:
+        plan, info = make_plan()
+        obj = [(list(plan.ssa_path), list(plan.sliced_labels), info)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    path, sliced, info = obj[0]
+    if rank == 0:
+        return plan, info
+    return jet.Plan.create(net, path, sliced), info
+
+
 def host_shard_sum(values_per_rank):
     """Reference combination used by the CPU tests: canonical per-rank sums, then the sum of
     rank partials in rank order (what a ring all-reduce computes up to rounding order)."""

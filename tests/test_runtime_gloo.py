@@ -82,3 +82,41 @@ def test_gloo_two_ranks_single_allreduce():
     for r in range(world):
         assert abs(out[r][0] - full) < 1e-12          # every rank holds the reduced amplitude
     assert abs(tot - full) < 1e-12
+
+
+def _plan_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    import __graft_entry__
+    from circuits import workload
+    from paper_2107_09793_b200 import jet
+    from paper_2107_09793_b200.runtime import plan_shared
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    __graft_entry__.build() if rank == 0 else None
+    dist.barrier()
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    calls = []
+
+    def make():
+        calls.append(1)
+        return jet.Plan.greedy(net, seed=3, trials=32, n_sliced=6, slice_objective=1), {"who": rank}
+
+    plan, info = plan_shared(net, make)
+    out[rank] = (list(plan.ssa_path), list(plan.sliced_labels), plan.cost()["prefix"], len(calls), info["who"])
+    dist.destroy_process_group()
+
+
+def test_gloo_plan_once_broadcast():
+    """Rank 0 plans, rank 1 rebuilds the identical plan from the broadcast path + sliced labels."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_plan_worker, args=(world, port, out), nprocs=world, join=True)
+    assert out[0][3] == 1 and out[1][3] == 0          # only rank 0 ran the planner
+    assert out[0][:3] == out[1][:3]                   # same path, slices and executed FLOP
+    assert out[1][4] == 0
