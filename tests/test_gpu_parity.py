@@ -237,10 +237,15 @@ def c2_plan(jet):
     return circ, bits, net, plan
 
 
-def test_c2_full_parity(jet, c2_plan):
+@pytest.fixture(scope="module")
+def c2_ref(c2_plan):
     circ, bits, net, plan = c2_plan
-    onet = build_network(circ, bits)
-    ref_vals = contract.slice_values(onet, plan.ssa_path, plan.sliced_labels)
+    return contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels)
+
+
+def test_c2_full_parity(jet, c2_plan, c2_ref):
+    circ, bits, net, plan = c2_plan
+    ref_vals = c2_ref
     ref = sum(ref_vals)
     assert abs(ref) ** 2 * 2 ** 53 > 0.01                                    # reading A13
     amp, vals, ex = run(jet, plan, "c64")
@@ -248,6 +253,17 @@ def test_c2_full_parity(jet, c2_plan):
     for v, r in zip(vals, ref_vals):
         assert abs(v - r) <= 1e-4 * abs(r)
     assert ex.stats()["flop_executed"] == plan.cost()["prefix"]
+
+
+def test_c2_full_parity_c128(jet, c2_plan, c2_ref):
+    """The same 64 slices in complex128 (K2 FP64 + K4 DMMA on the Sycamore shapes) at 1e-10."""
+    circ, bits, net, plan = c2_plan
+    assert any(n["kind"] == 3 for n in plan.describe_exec("c128")["nodes"])
+    amp, vals, ex = run(jet, plan, "c128")
+    ref = sum(c2_ref)
+    assert rel(amp, ref) < 1e-10
+    for v, r in zip(vals, c2_ref):
+        assert abs(v - r) <= 1e-10 * abs(r)
 
 
 def test_c2_fsim_identity_closed_form(jet):
