@@ -31,6 +31,24 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Operand tile copy for CTAs of a multiple of 64 threads: thread tid copies elements
+// e = tid + i*nthr, so e & 63 = tid & 63 is fixed -- its low gather offset and the low part of
+// the (GF(2)-linear) shared-memory swizzle are hoisted; per element one table load remains.
+__device__ __forceinline__ void load_tile_c128_g64(double2* dst, const double2* src, int n, const int64_t (*tg)[64],
+                                                   int tid, int nthr) {
+  const int sz = 1 << n;
+  const int lo = tid & 63;
+  const double2* s0 = src + tg[0][lo];
+  const int d0 = swz<double2>(lo);
+  for (int e = tid; e < sz; e += nthr) cp_async16(dst + (d0 ^ swz<double2>(e & ~63)), s0 + tg[1][e >> 6]);
+}
+
+__device__ __forceinline__ void load_tile_c128(double2* dst, const double2* src, int n, const int64_t (*tg)[64],
+                                               int tid, int nthr) {
+  if ((nthr & 63) == 0) load_tile_c128_g64(dst, src, n, tg, tid, nthr);
+  else load_tile(dst, src, n, false, tg, tid, nthr);
+}
+
 // p.TY x p.TX warps (rows x columns of warp tiles), KG = 1.  2^tm = 8*SMT*TY, 2^tn = 8*SNT*TX,
 // tile-K >= 4 complex.
 template <int SMT, int SNT>
@@ -120,8 +138,8 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
     for (int j = 0; j < SNT; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
   if (total > 0) {
     tile_start();
-    load_tile(sA0, A + ld_oa, p.nA, false, tgA, tid, nthr);
-    load_tile(sA0 + szA, B + ld_ob, p.nB, false, tgB, tid, nthr);
+    load_tile_c128(sA0, A + ld_oa, p.nA, tgA, tid, nthr);
+    load_tile_c128(sA0 + szA, B + ld_ob, p.nB, tgB, tid, nthr);
     cp_async_commit();
   }
   for (int64_t w = 0; w < total; ++w) {
@@ -129,8 +147,8 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
     if (w + 1 < total) {
       advance();
       C2* nxt = sA0 + (buf ^ 1) * stage;
-      load_tile(nxt, A + ld_oa, p.nA, false, tgA, tid, nthr);
-      load_tile(nxt + szA, B + ld_ob, p.nB, false, tgB, tid, nthr);
+      load_tile_c128(nxt, A + ld_oa, p.nA, tgA, tid, nthr);
+      load_tile_c128(nxt + szA, B + ld_ob, p.nB, tgB, tid, nthr);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
