@@ -345,6 +345,8 @@ def run_ours(args, cfg):
         b, e = next_block()
         if b == b0:   # a new pass over this rank's slices starts cold (no cache from the last pass)
             ex.invalidate()
+        with torch.cuda.stream(stream):
+            acc.zero_()   # each step reduces its own slices (one full amplitude for C3)
         ex.contract(b, e, acc)
         with torch.cuda.stream(stream):
             allreduce_amplitude(acc)
@@ -371,6 +373,7 @@ def run_ours(args, cfg):
         dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    step_sum = acc.cpu().numpy().tolist()   # the last timed step's all-reduced sum of s_sigma
     st = ex.stats()
     t = torch.tensor([ms, float(slices), st["flop_executed"], st["bytes_executed"], float(st["kernel_launches"])],
                      dtype=torch.float64, device="cuda")
@@ -476,6 +479,9 @@ def run_ours(args, cfg):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "algorithmic_gbs_step": tot_bytes / (ms_max / 1e3) / 1e9,
+            # the last timed step's all-reduced slice sum: the amplitude <x|U|0> when a step is
+            # one full amplitude (C3), else the partial sum of that step's slices
+            "step_sum": {"re": step_sum[0], "im": step_sum[1], "full_amplitude": bool(sps >= rng_len)},
             # f3 memory report of the plan (jt_exec_memory, fig. m10_memory), GB
             "memory_gb": {k: round(v / 1e9, 3) for k, v in plan.memory(cfg["dtype"]).items()},
         }
