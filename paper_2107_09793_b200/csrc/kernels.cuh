@@ -140,7 +140,14 @@ __device__ __forceinline__ void load_tile(C2* dst, const C2* src, int n, bool ve
   if (sizeof(C2) == 16) {
     for (int e = tid; e < sz; e += nthr) cp_async16(dst + swz<C2>(e), src + tg[0][e & 63] + tg[1][e >> 6]);
   } else if (vec) {
-    for (int e = 2 * tid; e < sz; e += 2 * nthr) cp_async16(dst + swz<C2>(e), src + tg[0][e & 63] + tg[1][e >> 6]);
+    if ((nthr & 31) == 0) {  // 2*nthr is a multiple of 64: e & 63 is fixed per thread (swz is GF(2)-linear)
+      const int lo = (2 * tid) & 63;
+      const C2* s0 = src + tg[0][lo];
+      const int d0 = swz<C2>(lo);
+      for (int e = 2 * tid; e < sz; e += 2 * nthr) cp_async16(dst + (d0 ^ swz<C2>(e & ~63)), s0 + tg[1][e >> 6]);
+    } else {
+      for (int e = 2 * tid; e < sz; e += 2 * nthr) cp_async16(dst + swz<C2>(e), src + tg[0][e & 63] + tg[1][e >> 6]);
+    }
   } else {
     for (int e = tid; e < sz; e += nthr) cp_async8(dst + swz<C2>(e), src + tg[0][e & 63] + tg[1][e >> 6]);
   }
