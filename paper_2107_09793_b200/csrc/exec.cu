@@ -233,7 +233,18 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   // row n, complex k at n*rb + ((k>>1) ^ (n & (chunks-1)))*16 + (k&1)*8 (XOR-combinable)
   const int rb = 8 << tkc, lg_chunks = tkc - 1;
   std::vector<std::pair<int64_t, int32_t>> tb;
-  for (int i = 0; i < 7; ++i) tb.push_back({sb[tN[i]], (rb << i) ^ (i < lg_chunks ? (16 << i) : 0)});
+  // the raw-row XOR swizzle uses the lg_chunks row bits with the SMALLEST B strides (a warp's
+  // gather lanes vary those first), whatever row-bit order the output layout chose
+  int swz_rank[7];
+  {
+    std::vector<std::pair<int64_t, int>> rs;
+    for (int i = 0; i < 7; ++i) rs.push_back({sb[tN[i]], i});
+    std::sort(rs.begin(), rs.end());
+    for (int q = 0; q < 7; ++q) swz_rank[rs[q].second] = q;
+    for (int q = 0; q < 3; ++q) t.swz_row[q] = (int8_t)rs[q].second;
+  }
+  for (int i = 0; i < 7; ++i)
+    tb.push_back({sb[tN[i]], (rb << i) ^ (swz_rank[i] < lg_chunks ? (16 << swz_rank[i]) : 0)});
   for (int i = 0; i < tkc; ++i) tb.push_back({sb[K[i].second], i == 0 ? 8 : (16 << (i - 1))});
   std::sort(tb.begin(), tb.end());
   for (size_t j = 0; j < tb.size(); ++j) {

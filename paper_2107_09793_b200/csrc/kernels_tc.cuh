@@ -48,6 +48,7 @@ struct TcArgs {
   int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
   int32_t sX[kTcMaxTile];                      //   ... and its byte offset in the raw stage (XOR-combined)
   int64_t aM[8], aK[8];                        // A strides of its M bits / K bits
+  int8_t swz_row[3];                           // row bits (lowest B stride first) that drive the raw-row swizzle
   int32_t vecB;                                // 1: chunk-tile bit 0 is a K bit at global stride 1
                                                //    -> gather k-pairs as 16-B copies
   SliceView sv;
@@ -281,6 +282,8 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
     const int64_t boff = slice_off(p.sv, false);
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int row = quarter * 32 + lane;  // this thread's TMEM lane (row n of the tile)
+    // swizzle key of this row: its row bits of lowest B stride (see plan_tc)
+    const int rsw = ((row >> p.swz_row[0]) & 1) | (((row >> p.swz_row[1]) & 1) << 1) | (((row >> p.swz_row[2]) & 1) << 2);
     const int RS = p.rstages, XS = p.xstages;
     // raw row layout: 16-B chunk c of row n lives at chunk c ^ (n & (chunks-1))
     const int rb = 8 << TKC;            // raw bytes per row
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
 #pragma unroll
       for (int j = 0; j < NCOL / 4; ++j) {
         const int cc = half * (NCOL / 4) + j;  // 16-B chunk of this row = 2 complex
-        const float4 v = *reinterpret_cast<const float4*>(raw + ((cc ^ (row & (chunks - 1))) << 4));
+        const float4 v = *reinterpret_cast<const float4*>(raw + ((cc ^ (rsw & (chunks - 1))) << 4));
         const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
