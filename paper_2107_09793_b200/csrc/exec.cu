@@ -459,9 +459,16 @@ bool plan_dmma(ExecNode& en, const View& va, const View& vb, View& out) {
   auto grow = [&](std::vector<char>& in, int target) {
     for (size_t i = 0; i < in.size() && cnt(in) < target; ++i) in[i] = 1;
   };
-  grow(inK, std::min<int>((int)K.size(), 5));
+  // default caps tile-N at 32 and tile-K at 16 complex: 128-thread CTAs of 240 registers and
+  // 80 KB, two per SM whose barriers and load phases interleave (measured 29-32 TFLOP/s vs
+  // 25-31 for one 256-thread CTA with 128x64x32 tiles, profiles/r01_nodes_C4_k4_tiles.txt);
+  // JETB200_DMMA_TK / _TN override (sweeps)
+  int tk_cap = 4, tn_cap = 5;
+  if (const char* e = getenv("JETB200_DMMA_TK")) tk_cap = std::max(2, std::min(5, atoi(e)));
+  if (const char* e = getenv("JETB200_DMMA_TN")) tn_cap = std::max(3, std::min(7, atoi(e)));
+  grow(inK, std::min<int>((int)K.size(), tk_cap));
   grow(inM, std::min<int>((int)M.size(), 7));
-  grow(inN, std::min<int>((int)N.size(), std::max(3, 13 - cnt(inM))));
+  grow(inN, std::min<int>({(int)N.size(), std::max(3, 13 - cnt(inM)), tn_cap}));
   if (cnt(inN) > 7) return false;
   const int tm = cnt(inM), tn = cnt(inN), tk = cnt(inK);
   if (tm < 3 || tn < 3 || tk < 2 || tk > 5 || tm > 7 || tm + tn > 13) return false;
