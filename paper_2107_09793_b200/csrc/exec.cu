@@ -574,6 +574,11 @@ View plan_gett(ExecNode& en, const View& va, const View& vb, int esize) {
     ok = ok && ((1 << (tm + tn)) / (RM * RN) <= 256);
     if (ok) break;
     if (tm + tk > lim || tk + tn > lim) {
+      // JETB200_K2_KEEPK=1 (sweep knob): shrink the N tile before the K tile, so small K
+      // reductions stay whole inside one item (measured slower on the C3 streaming nodes:
+      // 3.04 vs 3.46 TB/s, so off by default)
+      static const bool keepk = [] { const char* e = std::getenv("JETB200_K2_KEEPK"); return e && e[0] == '1'; }();
+      if (keepk && tk + tn > lim && tn > tm && drop_last(inN, keepN)) continue;
       if (drop_last(inK, keepK)) continue;
     }
     if (tn >= tm) {
