@@ -198,7 +198,9 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   const int rbytes = 128 * (8 << tkc);
   const int64_t ybytes = 2LL * n_kc * yplane;
   const int64_t budget = 220 * 1024 - 1024 - ybytes;
-  const int rstages = (int)std::min<int64_t>(6, budget / rbytes);
+  int rs_cap = 6;  // JETB200_K3_RS: sweep knob for the raw gather ring depth
+  if (const char* e = std::getenv("JETB200_K3_RS")) rs_cap = std::max(2, std::min(6, atoi(e)));
+  const int rstages = (int)std::min<int64_t>(rs_cap, budget / rbytes);
   if (rstages < 2) return false;
   const int64_t smem = ybytes + (int64_t)rstages * rbytes + 1024;
   std::sort(M.begin(), M.end());
