@@ -113,14 +113,27 @@ def slice_assignments(net, sliced_labels):
         yield dict(zip(sliced_labels, digits))
 
 
+def slice_assignment(net, sliced_labels, index):
+    """The index-th assignment of slice_assignments (mixed radix, sliced_labels[0] most
+    significant), without enumerating the ones before it (N_sl reaches 2^36 at C4)."""
+    n = 1
+    for l in sliced_labels:
+        n *= net.dims[l]
+    if not 0 <= index < n:
+        raise ValueError(f"slice index {index} out of range [0, {n})")
+    digits = {}
+    for l in reversed(list(sliced_labels)):
+        index, digits[l] = divmod(index, net.dims[l])
+    return {l: digits[l] for l in sliced_labels}
+
+
 def slice_values(net, ssa_path, sliced_labels, indices=None):
     """s_sigma for each slice index (all, or the given subset), in canonical order."""
     validate_path(net.n_tensors, ssa_path)
     validate_slices(net, sliced_labels)
-    all_sig = list(slice_assignments(net, sliced_labels))
     if indices is None:
-        indices = range(len(all_sig))
-    return [contract_along(net, ssa_path, all_sig[i]) for i in indices]
+        return [contract_along(net, ssa_path, sig) for sig in slice_assignments(net, sliced_labels)]
+    return [contract_along(net, ssa_path, slice_assignment(net, sliced_labels, i)) for i in indices]
 
 
 def amplitude(net, ssa_path, sliced_labels=()):

@@ -77,6 +77,47 @@ def test_worked_example_slicing_e(golden_dir):
     assert rep["e_fltask"] < rep["e_flsl"]
 
 
+def test_worked_example_cost_counters_by_hand():
+    """Eq. sliced_flops and Eq. task_based_amplitude_flops on the worked
+    example sliced on e (D = 2, path of Eq. sequence), every counter computed by hand:
+      step (<c|, B_cfbe|e)   union {c,f,b}  8*2^3 = 64   S = {e}
+      step (S_ed|e, |0>_d)   union {d}      8*2   = 16   S = {e}
+      step (S_ba, |0>_a)     union {b,a}    8*2^2 = 32   S = {}    (T3, the shared task)
+      step (<f|, T1_fb)      union {f,b}    8*2^2 = 32   S = {e}
+      step (T4_b, T2)        union {b}      8*2   = 16   S = {e}
+      step (T3_b, T5_b)      union {b}      8*2   = 16   S = {e}
+    FLOP_sl = 176, shared = 32, f_sl = 32/176 (a fraction of FLOP, not of tasks),
+    E-flsl = 2 * 176 = 352, E-fltask = f_sl FLOP_sl + N_sl (1 - f_sl) FLOP_sl = 32 + 2 * 144 = 320;
+    exact dedup and the one-copy prefix cache (order [e]) both run T3 once: 320."""
+    p = [(5, 4), (3, 1), (2, 0), (6, 7), (10, 8), (9, 11)]
+    _, net = worked_example([0, 0])
+    rep = cost.cost_report(net, p, [3])
+    assert [f for f, _ in cost.tree_info(net, p, [3])] == [64, 16, 32, 32, 16, 16]
+    assert rep["flop_sl"] == 176 and rep["flop_shared"] == 32
+    assert rep["e_flsl"] == 352
+    assert rep["e_fltask"] == 320          # a per-task f_sl (1 of 6 nodes) would give 322.67
+    assert rep["exact_reuse"] == 320 and rep["prefix"] == 320
+    assert cost.prefix_flop(net, p, [3], 0, 1) == 176 and cost.prefix_flop(net, p, [3], 1, 2) == 176
+
+
+def test_slice_assignment_is_the_lexicographic_enumeration():
+    """contract.slice_assignment(i) (direct mixed radix, used for N_sl up to 2^36) is the i-th
+    element of the itertools enumeration with sliced_labels[0] most significant (reading A12),
+    on mixed dimensions 2, 3, 4."""
+    c = Circuit(3, 2)
+    c.add((0, 1), np.eye(4))
+    net = build_network(c, [0, 0, 0])
+    net.dims = {0: 2, 1: 3, 2: 4, 3: 2, 4: 3}
+    sl = [2, 0, 1]
+    allsig = list(contract.slice_assignments(net, sl))
+    assert len(allsig) == 24
+    for i, sig in enumerate(allsig):
+        assert contract.slice_assignment(net, sl, i) == sig
+    assert allsig[1] == {2: 0, 0: 0, 1: 1} and allsig[3] == {2: 0, 0: 1, 1: 0}
+    with pytest.raises(ValueError):
+        contract.slice_assignment(net, sl, 24)
+
+
 def test_worked_example_qutrit_vs_statevector():
     d = 3
     w = np.exp(2j * np.pi / 3)
