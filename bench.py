@@ -56,7 +56,11 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--plan-seeds", type=int, default=0, help="planner seeds searched (host only; 0 = config default)")
     ap.add_argument("--width-cap", type=int, default=31)
-    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0,
+                    help="partial-slice oracle sample length when a complete slice is too long")
+    ap.add_argument("--cpu-max-slice-s", type=float, default=240.0,
+                    help="time a complete oracle slice when it is predicted to finish within this")
+    ap.add_argument("--replan", action="store_true", help="run the host planner instead of reading plans/<cfg>.json")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -69,9 +73,50 @@ def dist_env():
     return world, rank, local
 
 
+PLANS = os.path.join(ROOT, "plans")
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def load_plan_file(name):
+    """The committed plan (plans/<cfg>.json): SSA path + sliced labels, the problem inputs of
+    P:176 ("a special file ... which stores the contraction path"), written once by
+    scripts/export_plans.py with the host planner.  The bench, the parity goldens and the
+    reference arm all read this same file."""
+    p = os.path.join(PLANS, f"{name}.json")
+    return json.load(open(p)) if os.path.exists(p) else None
+
+
+def plan_sha(rec):
+    import hashlib
+
+    s = json.dumps({"p": rec["ssa_path"], "s": rec["sliced_labels"], "c": rec["circuit"],
+                    "seed": rec["circuit_seed"]}, sort_keys=True)
+    return hashlib.sha256(s.encode()).hexdigest()[:16]
+
+
+def load_goldens(name, rec):
+    """Oracle s_sigma of the committed plan (tests/golden/parity_<cfg>.json, written by
+    scripts/make_goldens.py, which imports only oracle/ and circuits/): {index: complex}."""
+    p = os.path.join(GOLDEN, f"parity_{name}.json")
+    if rec is None or not os.path.exists(p):
+        return {}
+    g = json.load(open(p))
+    if g.get("plan_sha") != plan_sha(rec):
+        log(f"warning: {p} was written for another plan; parity not checked")
+        return {}
+    return {int(k): complex(v["re"], v["im"]) for k, v in g["slices"].items()}
+
+
 def make_plan(jet, cfg, args):
     from circuits import workload
 
+    rec = None if args.replan else load_plan_file(args.config)
+    if rec is not None:
+        t0 = time.time()
+        circ, bits = workload(rec["circuit"], rec["circuit_seed"])
+        net = jet.Network.from_circuit(circ, bits)
+        plan = jet.Plan.create(net, [tuple(x) for x in rec["ssa_path"]], rec["sliced_labels"])
+        return circ, bits, net, plan, time.time() - t0, rec
     circ, bits = workload(cfg["circ"], args.seed)
     net = jet.Network.from_circuit(circ, bits)
     from paper_2107_09793_b200.runtime import plan_best
@@ -85,40 +130,18 @@ def make_plan(jet, cfg, args):
         net, k if k is not None else -1, dtype=cfg["dtype"],
         seeds=tuple(range(args.seed, args.seed + (args.plan_seeds or cfg.get("seeds", 8)))),
         trials=args.trials, width_cap=cfg.get("cap", args.width_cap) if k is None else 0))
-    return circ, bits, net, plan, time.time() - t0
+    return circ, bits, net, plan, time.time() - t0, None
 
 
-# ------------------------------------------------------------------ oracle (CPU) sampling
-def oracle_sample(circ, bits, plan, budget_s, max_out_log2=27):
-    """The oracle as it stands (oracle.contract.contract_pair, complex128 numpy) evaluating
-    slice 0 of the plan step by step in path order for about budget_s seconds.  Returns
-    (FLOP done, seconds, steps done).  Steps whose output exceeds 2^max_out_log2 elements
-    end the sample (host-memory guard)."""
-    from oracle import contract, cost
-    from oracle.network import build_network
-
-    onet = build_network(circ, bits)
-    sl = plan.sliced_labels
-    path = plan.ssa_path
-    steps = cost.tree_info(onet, path, sl)
-    assign = {l: 0 for l in sl}
-    vals, labs = {}, {}
-    for t in range(onet.n_tensors):
-        vals[t], labs[t] = contract.restrict(onet.tensors[t], onet.labels[t], assign)
-    nid = onet.n_tensors
-    done_flop, n_done = 0, 0
-    t0 = time.perf_counter()
-    for (i, j), (flop, _) in zip(path, steps):
-        out_labels = [l for l in labs[i] if l not in labs[j]] + [l for l in labs[j] if l not in labs[i]]
-        if len(out_labels) * (onet.dims[out_labels[0]].bit_length() - 1 if out_labels else 0) > max_out_log2:
-            break
-        vals[nid], labs[nid] = contract.contract_pair(vals.pop(i), labs.pop(i), vals.pop(j), labs.pop(j))
-        nid += 1
-        done_flop += flop
-        n_done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    return done_flop, time.perf_counter() - t0, n_done
+# ------------------------------------------------------------------ oracle (CPU) timing
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def blas_threads():
@@ -131,20 +154,114 @@ def blas_threads():
         return os.cpu_count()
 
 
-def cpu_baseline_entry(circ, bits, plan, budget_s):
-    c = plan.cost()
-    flop_per_slice = c["prefix"] / c["n_sl"]
-    fl, sec, n = oracle_sample(circ, bits, plan, budget_s)
-    rate = fl / sec if sec > 0 else 0.0
+def oracle_flop_sl(onet, path, sliced):
+    """FLOP of one slice along the path (oracle.cost.tree_info, A11: 8 x prod distinct dims)."""
+    from oracle import cost
+
+    return sum(f for f, _ in cost.tree_info(onet, path, sliced))
+
+
+def oracle_complete_slice(onet, path, sliced, index):
+    """The oracle as it stands (oracle.contract.slice_values: complex128 numpy pairwise steps)
+    on ONE complete slice: (s_sigma, seconds)."""
+    from oracle import contract
+
+    t0 = time.perf_counter()
+    (v,) = contract.slice_values(onet, path, sliced, indices=[index])
+    return v, time.perf_counter() - t0
+
+
+def oracle_partial_slice(onet, path, sliced, budget_s):
+    """Slice 0 evaluated step by step in path order for about budget_s seconds (used only when
+    a complete slice would not finish in the bench's time; the rate is then extrapolated).
+    Returns (FLOP done, seconds, steps done)."""
+    from oracle import contract, cost
+
+    steps = cost.tree_info(onet, path, sliced)
+    assign = {l: 0 for l in sliced}
+    vals, labs = {}, {}
+    for t in range(onet.n_tensors):
+        vals[t], labs[t] = contract.restrict(onet.tensors[t], onet.labels[t], assign)
+    nid = onet.n_tensors
+    done_flop, n_done = 0, 0
+    t0 = time.perf_counter()
+    for (i, j), (flop, _) in zip(path, steps):
+        vals[nid], labs[nid] = contract.contract_pair(vals.pop(i), labs.pop(i), vals.pop(j), labs.pop(j))
+        nid += 1
+        done_flop += flop
+        n_done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    return done_flop, time.perf_counter() - t0, n_done
+
+
+def c2_single_thread_rate():
+    """the oracle's single-thread rate on one C2 slice (plans/C2.json)."""
+    rec = load_plan_file("C2")
+    if rec is None:
+        return None
+    from circuits import workload
+    from oracle.network import build_network
+
+    circ, bits = workload(rec["circuit"], rec["circuit_seed"])
+    onet = build_network(circ, bits)
+    path = [tuple(x) for x in rec["ssa_path"]]
+    sl = rec["sliced_labels"]
+    fl = oracle_flop_sl(onet, path, sl)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(1):
+            _, sec = oracle_complete_slice(onet, path, sl, 0)
+    except ImportError:
+        return None
+    return {"seconds": round(sec, 3), "gflops": fl / sec / 1e9, "threads": 1, "flop_sl": fl}
+
+
+def oracle_run(circ, bits, path, sliced, indices, goldens, max_slice_s, partial_budget_s):
+    """Time the oracle on complete slices `indices` of the plan (each compared with its golden
+    value when one is stored).  When a complete slice is predicted to exceed max_slice_s (from
+    a bounded partial-slice rate), fall back to that partial sample, extrapolated by FLOP_sl.
+    Returns a dict with slices/s and the sample description."""
+    from oracle.network import build_network
+
+    onet = build_network(circ, bits)
+    fl_sl = oracle_flop_sl(onet, path, sliced)
+    # predict: a short partial sample (small early steps run slower than the big ones, so the
+    # prediction is conservative)
+    pf, ps, pn = oracle_partial_slice(onet, path, sliced, min(partial_budget_s, 5.0))
+    pred = fl_sl / (pf / ps) if pf > 0 else float("inf")
+    if pn >= len(path):
+        pred = ps
+    if pred > max_slice_s:
+        fl, sec, n = oracle_partial_slice(onet, path, sliced, partial_budget_s)
+        rate = fl / sec
+        return {"value": rate / fl_sl, "complete": False, "seconds": [sec], "flop_sl": fl_sl,
+                "sample": (f"slice 0, first {n} of {len(path)} path steps ({fl:.3g} of FLOP_sl {fl_sl:.3g}) in "
+                           f"{sec:.1f} s = {rate / 1e9:.2f} GFLOP/s, extrapolated: slices/s = rate / FLOP_sl "
+                           f"(a complete slice was predicted to take {pred:.0f} s)")}
+    secs, errs = [], []
+    for i in indices:
+        v, sec = oracle_complete_slice(onet, path, sliced, i)
+        secs.append(sec)
+        if i in goldens:
+            errs.append(abs(v - goldens[i]) / abs(goldens[i]))
+    tot = sum(secs)
+    return {"value": len(indices) / tot, "complete": True, "seconds": [round(x, 2) for x in secs], "flop_sl": fl_sl,
+            "golden_max_rel_diff": max(errs) if errs else None,
+            "sample": (f"{len(indices)} complete slice(s) {list(indices)} of the benched plan, {tot:.1f} s "
+                       f"({len(indices) * fl_sl / tot / 1e9:.2f} GFLOP/s at FLOP_sl {fl_sl:.3g}); no prefix cache "
+                       f"(the oracle recomputes every node per slice)")}
+
+
+def cpu_baseline_entry(circ, bits, plan_path, plan_sliced, goldens, args):
+    idx = [min(goldens)] if goldens else [0]
+    r = oracle_run(circ, bits, plan_path, plan_sliced, idx, goldens, args.cpu_max_slice_s, args.cpu_budget_s)
     return {
-        "value": rate / flop_per_slice,
-        "unit": "slices/s",
-        "cores": blas_threads(),
-        "kind": "oracle",
-        "sample": (f"oracle (numpy complex128 pairwise steps) on slice 0 of the same plan, first {n} path "
-                   f"steps ({fl:.3g} FLOP in {sec:.1f} s = {rate / 1e9:.2f} GFLOP/s), scaled by the plan's "
-                   f"prefix-cache FLOP per slice {flop_per_slice:.3g}"),
-        "oracle_gflops": rate / 1e9,
+        "value": r["value"], "unit": "slices/s", "cores": blas_threads(), "kind": "oracle",
+        "sample": r["sample"], "complete_slices": r["complete"], "slice_seconds": r["seconds"],
+        "golden_max_rel_diff": r.get("golden_max_rel_diff"), "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+        "c2_slice_single_thread": c2_single_thread_rate(),
     }
 
 
@@ -262,41 +379,54 @@ def profile_traffic(cfg_name, kernel):
 
 # ------------------------------------------------------------------ reference arm (the oracle)
 def run_reference(args, cfg):
+    """The oracle (oracle/, complex128 numpy) on the host cores, on the same committed plan
+    (plans/<cfg>.json) and metric.  It never loads the product library: the plan is read from
+    the file and the oracle contracts it itself.  Each timed step = one complete slice (the
+    golden slices in turn, each checked against its stored oracle value); warm-up steps are a
+    bounded partial slice."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    os.environ.setdefault("CUDA_VISIBLE_DEVICES", "")
-    import __graft_entry__
+    from circuits import workload
+    from oracle.network import build_network
 
-    __graft_entry__.build()
-    from paper_2107_09793_b200 import jet
-
-    circ, bits, net, plan, _ = make_plan(jet, cfg, args)
-    c = plan.cost()
-    flop_per_slice = c["prefix"] / c["n_sl"]
-    budget = max(2.0, min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup)))
+    rec = load_plan_file(args.config)
+    if rec is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"plans/{args.config}.json missing"}), flush=True)
+        return
+    circ, bits = workload(rec["circuit"], rec["circuit_seed"])
+    path = [tuple(x) for x in rec["ssa_path"]]
+    sl = rec["sliced_labels"]
+    goldens = load_goldens(args.config, rec)
+    onet = build_network(circ, bits)
+    n_sl = rec["cost"]["n_sl"]
     for _ in range(args.warmup):
-        oracle_sample(circ, bits, plan, budget)
-    fl_tot, sec_tot, n = 0, 0.0, 0
-    for _ in range(args.steps):
-        fl, sec, n = oracle_sample(circ, bits, plan, budget)
-        fl_tot += fl
-        sec_tot += sec
-    rate = fl_tot / sec_tot
-    value = rate / flop_per_slice
+        oracle_partial_slice(onet, path, sl, 2.0)
+    idx = sorted(goldens) or [0]
+    picks = [idx[s % len(idx)] for s in range(args.steps)]
+    r = oracle_run(circ, bits, path, sl, picks, goldens, args.cpu_max_slice_s, args.cpu_budget_s)
+    value = r["value"]
     cores = blas_threads()
-    sample = (f"each step: oracle on slice 0 of the plan, first {n} path steps for ~{budget:.0f} s; "
-              f"{rate / 1e9:.2f} GFLOP/s scaled by {flop_per_slice:.3g} prefix FLOP per slice")
+    sps = args.slices_per_step or cfg["sps"]
+    try:   # evidence that this arm never mapped the product library
+        lib_loaded = "libjetb200" in open("/proc/self/maps").read()
+    except OSError:
+        lib_loaded = None
     print(json.dumps({
         "impl": "reference", "metric": "Sycamore-53 m=14 amplitude time; slices/s and cGEMM TFLOP/s",
         "value": value, "unit": "slices/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sec_tot / args.steps, "higher_is_better": True,
-        "scaling": "strong" if (args.slices_per_step or cfg["sps"]) >= c["n_sl"] else "weak",
+        "ms_per_step": 1e3 / value, "higher_is_better": True,
+        "scaling": "strong" if sps >= n_sl else "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded Sycamore-style RQC)",
-        "config": {"workload": cfg["workload"], "n_sl": c["n_sl"], "flop_per_slice_prefix": flop_per_slice},
-        "cpu_baseline": {"value": value, "unit": "slices/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "config": {"workload": cfg["workload"], "n_sl": n_sl, "flop_per_slice": r["flop_sl"],
+                   "plan": f"plans/{args.config}.json"},
+        "cpu_baseline": {"value": value, "unit": "slices/s", "cores": cores, "kind": "oracle", "sample": r["sample"],
+                         "complete_slices": r["complete"], "slice_seconds": r["seconds"],
+                         "golden_max_rel_diff": r.get("golden_max_rel_diff"), "cpu_model": cpu_model(),
+                         "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "amplitude_time_s": c["n_sl"] / value,
+        "amplitude_time_s_extrapolated": n_sl / value,
+        "product_library_loaded": lib_loaded,
     }), flush=True)
 
 
@@ -319,11 +449,12 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
     from paper_2107_09793_b200 import jet
-    from paper_2107_09793_b200.runtime import allreduce_amplitude, shard_range
+    from paper_2107_09793_b200.runtime import allreduce_amplitude, modeled_rank_flop, shard_range
 
-    circ, bits, net, plan, t_plan = make_plan(jet, cfg, args)
+    circ, bits, net, plan, t_plan, rec = make_plan(jet, cfg, args)
     c = plan.cost()
     n_sl = c["n_sl"]
+    goldens = load_goldens(args.config, rec)
     b0, e0 = shard_range(n_sl, rank, world)
     rng_len = e0 - b0
     sps = args.slices_per_step or cfg["sps"]
@@ -449,11 +580,41 @@ def run_ours(args, cfg):
         e2e = {"value": e_slices / el, "unit": "slices/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 16}
 
+    # parity (outside the timed region): every golden slice of this rank's range, contracted in
+    # the bench's own configuration (same executor, stream, graphs and prefix cache; the pass
+    # starts cold at the block start), against the oracle's stored s_sigma (reading A13)
+    mine = sorted(i for i in goldens if b0 <= i < e0)
+    errs = []
+    if mine:
+        if sps >= rng_len:   # a step is the whole rank share: one cold pass returns every s_sigma
+            ex.invalidate()
+            vals = ex.contract(b0, e0, acc, slice_values=True)
+            got = {i: vals[i - b0] for i in mine}
+        else:                # subset configs: each golden slice cold, one by one
+            got = {}
+            for i in mine:
+                ex.invalidate()
+                got[i] = ex.contract(i, i + 1, acc, slice_values=True)[0]
+        torch.cuda.synchronize()
+        errs = [abs(got[i] - goldens[i]) / abs(goldens[i]) for i in mine]
+    pt = torch.tensor([max(errs) if errs else 0.0, float(len(errs))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        pm = pt.clone()
+        dist.all_reduce(pm, op=dist.ReduceOp.MAX)
+        ps = pt.clone()
+        dist.all_reduce(ps, op=dist.ReduceOp.SUM)
+        pt = torch.stack([pm[0], ps[1]])
+    tol = 1e-4 if cfg["dtype"] == "c64" else 1e-10
+    parity = {"golden": f"tests/golden/parity_{args.config}.json", "slices": int(pt[1].item()),
+              "max_rel_err": pt[0].item() if pt[1].item() > 0 else None,
+              "median_rel_err_rank0": statistics.median(errs) if errs else None, "tol": tol,
+              "pass": bool(pt[1].item() > 0 and pt[0].item() < tol)}
+
     if rank == 0:
         peak, peak_kind = measured_peaks()
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline_entry(circ, bits, plan, args.cpu_budget_s)
+            cpu = cpu_baseline_entry(circ, bits, plan.ssa_path, plan.sliced_labels, goldens, args)
         flop_rate = tot_flop / (ms_max / 1e3)
         out = {
             "metric": "Sycamore-53 m=14 amplitude time; slices/s and cGEMM TFLOP/s",
@@ -469,7 +630,12 @@ def run_ours(args, cfg):
                 "parallelism": f"slice-shard x{world}", "l2": "inputs larger than L2 (intermediates up to "
                 f"2^{int(c['max_width'])} elements)", "plan_seconds": round(t_plan, 2),
                 "step": "block of consecutive slices of one amplitude, prefix cache persists",
+                "plan": f"plans/{args.config}.json" if rec is not None else "searched (--replan)",
             },
+            "parity": parity,
+            # executed prefix-cache FLOP per rank block (each cold), sum / max over ranks
+            "modeled_rank_speedup": {str(g): round(modeled_rank_flop(plan, g)[1], 4) for g in (2, 4, 8)
+                                     if g <= n_sl},
             "cgemm_tflops": flop_rate / 1e12,
             "amplitude_time_s_extrapolated": c["prefix"] / max(world, 1) / (flop_rate / max(world, 1)),
             "gpu_launches": int(tot_launch),

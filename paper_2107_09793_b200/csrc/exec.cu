@@ -128,34 +128,38 @@ GettFn pick_gett(int RM, int RN) {
   fail(JT_EINTERNAL, "no gett instance");
 }
 
+// Raise the dynamic shared-memory limit of every kernel the executor launches.  The attribute
+// is per device, so it is set once per device id (the current device at the call) and every
+// result is checked.
 void set_smem_attrs() {
-  static std::once_flag once;
-  std::call_once(once, []() {
-    const int rms[3] = {1, 2, 4};
-    for (int a : rms)
-      for (int b : rms) {
-        cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<float>(a, b)),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_gett<double>(a, b)),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_dmma(a, b)),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      }
-    const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<3>),
-                          reinterpret_cast<const void*>(gett_tc_kernel<4>)};
-    for (const void* f : tcs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
-    const void* tcgs[4] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
-                           reinterpret_cast<const void*>(gett_tcg_kernel<6>), reinterpret_cast<const void*>(gett_tcg_kernel<7>)};
-    for (const void* f : tcgs) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, 0>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, 1>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<float2, 2>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(permute_kernel<double2, 0>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  });
+  static std::mutex mu;
+  static std::vector<char> done;
+  int dev = 0;
+  JT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)done.size() <= dev) done.resize(dev + 1, 0);
+  if (done[dev]) return;
+  auto set = [](const void* f, int bytes) {
+    JT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  };
+  const int rms[3] = {1, 2, 4};
+  for (int a : rms)
+    for (int b : rms) {
+      set(reinterpret_cast<const void*>(pick_gett<float>(a, b)), 200 * 1024);
+      set(reinterpret_cast<const void*>(pick_gett<double>(a, b)), 200 * 1024);
+      set(reinterpret_cast<const void*>(pick_dmma(a, b)), 200 * 1024);
+    }
+  const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<3>),
+                        reinterpret_cast<const void*>(gett_tc_kernel<4>)};
+  for (const void* f : tcs) set(f, 222 * 1024);
+  const void* tcgs[4] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
+                         reinterpret_cast<const void*>(gett_tcg_kernel<6>), reinterpret_cast<const void*>(gett_tcg_kernel<7>)};
+  for (const void* f : tcgs) set(f, 222 * 1024);
+  set(reinterpret_cast<const void*>(permute_kernel<float2, 0>), 200 * 1024);
+  set(reinterpret_cast<const void*>(permute_kernel<float2, 1>), 200 * 1024);
+  set(reinterpret_cast<const void*>(permute_kernel<float2, 2>), 200 * 1024);
+  set(reinterpret_cast<const void*>(permute_kernel<double2, 0>), 200 * 1024);
+  done[dev] = 1;
 }
 
 int ilog2_exact(int d) {

@@ -134,20 +134,24 @@ double prefix_flop(const jt_plan& plan, int64_t begin, int64_t end) {
   std::vector<double> F(k + 1, 0.0);  // F[j+1] = FLOP of nodes with maxpos >= j
   for (int64_t v = nt; v < (int64_t)plan.nodes.size(); ++v)
     for (int j = -1; j <= plan.nodes[v].maxpos; ++j) F[j + 1] += plan.nodes[v].flop;
-  double total = 0;
-  const int d = plan.net.d;
-  for (int64_t s = begin; s < end; ++s) {
-    int j = -1;
-    if (s > begin) {
-      int64_t prev = s - 1;
-      int t = 0;
-      while (t < k && prev % d == d - 1) {
-        prev /= d;
-        ++t;
-      }
-      j = k - 1 - t;
+  // slice s > begin recomputes the nodes with maxpos >= j, j = k-1-t where t = the number of
+  // trailing zero base-d digits of s (the digits that rolled over); count the slices of
+  // (begin, end) by t in closed form (multiples of d^t minus multiples of d^(t+1))
+  const int64_t d = plan.net.d;
+  if (end <= begin) return 0.0;
+  double total = F[0];  // the first slice of the range: everything (j = -1)
+  auto multiples = [&](int t) -> int64_t {  // multiples of d^t in [begin+1, end-1]
+    int64_t q = 1;
+    for (int i = 0; i < t; ++i) {
+      if (q > (end - 1) / d) return 0;
+      q *= d;
     }
-    total += F[j + 1];
+    return (end - 1) / q - begin / q;
+  };
+  for (int t = 0; t <= k; ++t) {
+    const int64_t cnt = t == k ? multiples(t) : multiples(t) - multiples(t + 1);
+    const int j = std::max(-1, k - 1 - t);
+    total += (double)cnt * F[j + 1];
   }
   return total;
 }

@@ -28,13 +28,18 @@ def allreduce_amplitude(acc, group=None):
     return acc
 
 
-def run_amplitude(plan, dtype="c64", exec_=None, slices=None):
+def run_amplitude(plan, dtype="c64", exec_=None, slices=None, cold=False):
     """Amplitude <x|U|0> = sum over all slices, sharded over the process group.
 
     Each rank contracts its block on its own GPU (current CUDA device) into a device
     complex128 accumulator, then one all-reduce; returns (amplitude, per-rank info).  For a
     batch plan (open wires) the runs are N_sl x n_batch and the result is the y-indexed
-    complex128 array of the batch's amplitudes."""
+    complex128 array of the batch's amplitudes.  `cold` drops the executor's prefix cache
+    first (a rank block starts cold, as it does on its own GPU).
+
+    Stream order: the executor runs on ex.stream; the zeroing, the all-reduce and the
+    device-to-host read are all issued on that same stream, so none of them can overtake
+    the contraction whatever stream the caller has current."""
     import torch
     import torch.distributed as dist
 
@@ -46,15 +51,27 @@ def run_amplitude(plan, dtype="c64", exec_=None, slices=None):
     nb = c["n_batch"]
     b, e = slices if slices is not None else shard_range(c["n_sl"] * nb, rank, world)
     ex = exec_ if exec_ is not None else jet.Exec(plan, dtype)
-    acc = torch.zeros(2 * nb, dtype=torch.float64, device=ex.device)
-    if e > b:
-        ex.contract(b, e, acc)
-    allreduce_amplitude(acc)
-    a = acc.cpu().numpy()
+    if cold:
+        ex.invalidate()
+    with torch.cuda.stream(ex.stream):
+        acc = torch.zeros(2 * nb, dtype=torch.float64, device=ex.device)
+        if e > b:
+            ex.contract(b, e, acc)
+        allreduce_amplitude(acc)
+        a = acc.cpu().numpy()
     info = {"rank": rank, "world": world, "range": (b, e)}
     if plan.net.open_wires:
         return a.view(np.complex128).copy(), info
     return complex(a[0], a[1]), info
+
+
+def modeled_rank_flop(plan, world):
+    """Executed prefix-cache FLOP of every rank's contiguous block (jt_plan_prefix_flop, each
+    block cold), and the modeled speedup sum / max over ranks."""
+    n = plan.cost()["n_sl"] * plan.cost()["n_batch"]
+    per = [plan.prefix_flop(*shard_range(n, r, world)) for r in range(world)]
+    total_1 = plan.prefix_flop(0, n)
+    return per, total_1 / max(per)
 
 
 def plan_shared(net, make_plan, group=None):

@@ -1,0 +1,269 @@
+"""GPU parity on the EXACT benched plans (plans/<cfg>.json, the files bench.py reads) against
+the oracle's stored slice values (tests/golden/parity_<cfg>.json, written by
+scripts/make_goldens.py from oracle/ only), plus the multi-GPU partition run on one GPU.
+
+Rule (BASELINE.json north_star, reading A13): every s_sigma compared with
+rel = |s_gpu - s_ora| / |s_ora| < 1e-4 (complex64) / 1e-10 (complex128), no absolute floor.
+Each compared slice is contracted as a rank contracts it: its executor starts cold at the
+rank block's first slice and runs the block's slices in order with the prefix cache, in the
+bench's launch configuration (side stream, per-level CUDA graphs, PDL).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from circuits import workload
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = {"c64": 1e-4, "c128": 1e-10}
+OUT = os.path.join(ROOT, "gpurun_out")
+
+
+@pytest.fixture(scope="module")
+def jet():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2107_09793_b200 import jet as j
+
+    torch.cuda.set_device(0)
+    return j
+
+
+def load(cfg):
+    import bench
+
+    rec = bench.load_plan_file(cfg)
+    gold = bench.load_goldens(cfg, rec)
+    assert rec is not None and gold, f"plans/{cfg}.json or its goldens missing"
+    return rec, gold
+
+
+def benched_plan(jet, rec):
+    circ, bits = workload(rec["circuit"], rec["circuit_seed"])
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.create(net, [tuple(x) for x in rec["ssa_path"]], rec["sliced_labels"])
+    assert plan.cost()["flop_sl"] == rec["cost"]["flop_sl"]
+    return circ, bits, net, plan
+
+
+def record(name, data):
+    """Error evidence for profiles/ (the achieved errors, not just pass/fail)."""
+    if os.path.isdir(OUT):
+        p = os.path.join(OUT, "parity_errors.json")
+        d = json.load(open(p)) if os.path.exists(p) else {}
+        d[name] = data
+        json.dump(d, open(p, "w"), indent=1)
+
+
+def exec_on_stream(jet, plan, dtype):
+    import torch
+
+    stream = torch.cuda.Stream()
+    ex = jet.Exec(plan, dtype, stream=stream)
+    torch.cuda.synchronize()
+    return ex, stream
+
+
+def block_values(jet, ex, b, e):
+    import torch
+
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ex.invalidate()
+    v = ex.contract(b, e, acc, slice_values=True)
+    torch.cuda.synchronize()
+    return v
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_benched_plan_golden_slices(jet, cfg):
+    """Every golden slice (C3: one per 128-slice rank block of G=8) of the benched plan."""
+    from paper_2107_09793_b200.runtime import shard_range
+
+    rec, gold = load(cfg)
+    dtype = rec["dtype"]
+    _, _, _, plan = benched_plan(jet, rec)
+    n_sl = plan.cost()["n_sl"]
+    ex, _ = exec_on_stream(jet, plan, dtype)
+    errs = {}
+    for g in range(8):
+        b, e = shard_range(n_sl, g, 8)
+        mine = [i for i in sorted(gold) if b <= i < e]
+        if not mine:
+            continue
+        vals = block_values(jet, ex, b, max(mine) + 1)
+        for i in mine:
+            errs[i] = abs(vals[i - b] - gold[i]) / abs(gold[i])
+    rel = np.array(list(errs.values()))
+    record(f"{cfg}_benched", {"slices": len(rel), "max_rel": float(rel.max()), "median_rel": float(np.median(rel)),
+                              "per_slice": {str(k): float(v) for k, v in errs.items()}})
+    if cfg == "C3":
+        assert len(errs) >= 8 and len({i * 8 // n_sl for i in errs}) == 8   # one per rank block
+    assert rel.max() < TOL[dtype], errs
+
+
+def test_c2_benched_full_amplitude(jet):
+    """C2: all 64 slices and the amplitude against the oracle."""
+    import torch
+
+    rec, gold = load("C2")
+    _, _, _, plan = benched_plan(jet, rec)
+    assert sorted(gold) == list(range(64))
+    ex, _ = exec_on_stream(jet, plan, "c64")
+    acc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ex.invalidate()
+    vals = ex.contract(0, 64, acc, slice_values=True)
+    torch.cuda.synchronize()
+    ref = np.array([gold[i] for i in range(64)])
+    amp = complex(acc[0].item(), acc[1].item())
+    want = complex(np.sum(ref))      # canonical-order sum of the oracle's s_sigma (A12)
+    rel = np.abs(vals - ref) / np.abs(ref)
+    record("C2_full", {"slices": 64, "max_rel": float(rel.max()), "median_rel": float(np.median(rel)),
+                       "amplitude_rel": abs(amp - want) / abs(want)})
+    assert rel.max() < 1e-4
+    assert abs(amp - want) / abs(want) < 1e-4
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_rank_partition_on_one_gpu(jet, cfg):
+    """the G = 2, 4, 8 rank blocks (runtime.shard_range), each run cold by
+    runtime.run_amplitude on this GPU, give bitwise the G = 1 slice values and partial sums whose
+    rank-order total matches G = 1 within 1e-6 relative (reduction-order rounding only); the
+    executed FLOP per block equals the model (jt_plan_prefix_flop)."""
+    import torch
+
+    from paper_2107_09793_b200.runtime import modeled_rank_flop, run_amplitude, shard_range
+
+    rec, gold = load(cfg)
+    _, _, _, plan = benched_plan(jet, rec)
+    n_sl = plan.cost()["n_sl"]
+    ex, _ = exec_on_stream(jet, plan, "c64")
+    v1 = block_values(jet, ex, 0, n_sl)
+    a1, _ = run_amplitude(plan, "c64", exec_=ex, slices=(0, n_sl), cold=True)
+    rows = {}
+    for G in (2, 4, 8):
+        per, speedup = modeled_rank_flop(plan, G)
+        tot = 0j
+        for r in range(G):
+            b, e = shard_range(n_sl, r, G)
+            ex.reset_stats()
+            part, info = run_amplitude(plan, "c64", exec_=ex, slices=(b, e), cold=True)
+            assert ex.stats()["flop_executed"] == per[r]
+            tot += part
+            vb = block_values(jet, ex, b, e)
+            assert np.array_equal(vb, v1[b:e])                  # bitwise, cold block start
+        rel = abs(tot - a1) / abs(a1)
+        rows[G] = {"rel_vs_G1": rel, "modeled_speedup": speedup}
+        assert rel < 1e-6
+        assert speedup > 0.95 * G
+    # and the amplitude's slices against the oracle goldens
+    errs = [abs(v1[i] - gold[i]) / abs(gold[i]) for i in gold]
+    rows["golden_max_rel"] = max(errs)
+    record(f"{cfg}_partition", rows)
+    assert max(errs) < 1e-4
+    if cfg == "C2":
+        want = complex(np.sum([gold[i] for i in range(64)]))
+        assert abs(a1 - want) / abs(want) < 1e-4
+    torch.cuda.synchronize()
+
+
+def _gloo_worker(rank, world, port, cfg, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, ROOT)
+        import bench
+        from paper_2107_09793_b200 import jet as j
+        from paper_2107_09793_b200.runtime import run_amplitude
+
+        torch.cuda.set_device(0)
+        rec = bench.load_plan_file(cfg)
+        circ, bits = workload(rec["circuit"], rec["circuit_seed"])
+        net = j.Network.from_circuit(circ, bits)
+        plan = j.Plan.create(net, [tuple(x) for x in rec["ssa_path"]], rec["sliced_labels"])
+        stream = torch.cuda.Stream()
+        ex = j.Exec(plan, "c64", stream=stream)
+        amp, info = run_amplitude(plan, "c64", exec_=ex)
+        q.put((rank, amp, info["range"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_run_amplitude_two_processes_gloo(jet):
+    """The product's multi-process path end to end: two ranks (processes) on this GPU, each
+    contracting its block of the benched C2 plan with runtime.run_amplitude, one SUM
+    all-reduce (gloo carries the CUDA accumulator here; NCCL on a multi-GPU node).  Both ranks
+    hold the oracle amplitude."""
+    import torch.multiprocessing as mp
+
+    _, gold = load("C2")
+    want = complex(np.sum([gold[i] for i in range(64)]))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    import socket
+
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, "C2", q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    assert [r[2] for r in res] == [(0, 32), (32, 64)]
+    for _, amp, _ in res:
+        assert abs(amp - want) / abs(want) < 1e-4
+    assert res[0][1] == res[1][1]
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_error_study_tensor_cores_vs_cuda_cores(jet, cfg, monkeypatch):
+    """Measured error of each kernel family against the oracle on the benched plan (the
+    3xTF32 tcgen05 path K3/K3g vs the FP32 CUDA-core path K2, JETB200_TC=0): max and median
+    relative error over the golden slices, both within the 1e-4 bar; recorded for DESIGN.md."""
+    from paper_2107_09793_b200.runtime import shard_range
+
+    rec, gold = load(cfg)
+    rows = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("JETB200_TC", mode)
+        _, _, _, plan = benched_plan(jet, rec)
+        kinds = [n["kind"] for n in plan.describe_exec("c64")["nodes"]]
+        if mode == "0":
+            assert all(k == 0 for k in kinds)
+        else:
+            assert any(k in (1, 2) for k in kinds)
+        n_sl = plan.cost()["n_sl"]
+        ex, _ = exec_on_stream(jet, plan, "c64")
+        picks = sorted(gold)[:4] if cfg == "C3" else sorted(gold)
+        errs = []
+        for g in range(8):
+            b, e = shard_range(n_sl, g, 8)
+            mine = [i for i in picks if b <= i < e]
+            if mine:
+                vals = block_values(jet, ex, b, max(mine) + 1)
+                errs += [abs(vals[i - b] - gold[i]) / abs(gold[i]) for i in mine]
+        rows["K3" if mode == "1" else "K2"] = {"slices": len(errs), "max_rel": float(max(errs)),
+                                               "median_rel": float(np.median(errs))}
+        del ex
+    record(f"{cfg}_error_study", rows)
+    for r in rows.values():
+        assert r["max_rel"] < 1e-4

@@ -91,8 +91,8 @@ def test_c1_parity_vs_oracle_and_statevector(jet, dtype, k):
         assert abs(ref - psi[tuple(bits)]) < 1e-12
         amp, vals, _ = run(jet, plan, dtype)
         assert rel(amp, ref) < TOL[dtype]
-        for v, r in zip(vals, ref_vals):
-            assert abs(v - r) <= TOL[dtype] * max(abs(r), 1e-3 * abs(ref))
+        for v, r in zip(vals, ref_vals):   # A13: the same rule for every s_sigma, no floor
+            assert abs(v - r) <= TOL[dtype] * abs(r), (v, r)
 
 
 def test_reuse_on_off_bitwise_and_ranges(jet):

@@ -94,9 +94,11 @@ def test_cost_counters_equal_oracle(jet, name, k):
     got = plan.cost()
     for key in ("n_sl", "flop_sl", "flop_shared", "e_flsl", "e_fltask", "exact_reuse", "prefix"):
         assert got[key] == ref[key], key
-    for b, e in [(0, 1), (1, ref["n_sl"]), (0, ref["n_sl"] // 2 + 1)]:
-        if e <= ref["n_sl"] and b < e:
-            assert plan.prefix_flop(b, e) == cost.prefix_flop(onet, p, sl, b, e)
+    # every sub-range (the library counts them in closed form, the oracle slice by slice)
+    n = ref["n_sl"]
+    for b in range(n):
+        for e in range(b, n + 1):
+            assert plan.prefix_flop(b, e) == cost.prefix_flop(onet, p, sl, b, e), (b, e)
 
 
 def test_greedy_plan_is_deterministic_and_valid(jet, tmp_path):
