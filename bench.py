@@ -56,8 +56,6 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--plan-seeds", type=int, default=0, help="planner seeds searched (host only; 0 = config default)")
     ap.add_argument("--width-cap", type=int, default=31)
-    ap.add_argument("--cpu-budget-s", type=float, default=20.0,
-                    help="partial-slice oracle sample length when a complete slice is too long")
     ap.add_argument("--cpu-max-slice-s", type=float, default=240.0,
                     help="time a complete oracle slice when it is predicted to finish within this")
     ap.add_argument("--replan", action="store_true", help="run the host planner instead of reading plans/<cfg>.json")
@@ -161,38 +159,30 @@ def oracle_flop_sl(onet, path, sliced):
     return sum(f for f, _ in cost.tree_info(onet, path, sliced))
 
 
-def oracle_complete_slice(onet, path, sliced, index):
-    """The oracle as it stands (oracle.contract.slice_values: complex128 numpy pairwise steps)
-    on ONE complete slice: (s_sigma, seconds)."""
-    from oracle import contract
-
-    t0 = time.perf_counter()
-    (v,) = contract.slice_values(onet, path, sliced, indices=[index])
-    return v, time.perf_counter() - t0
-
-
-def oracle_partial_slice(onet, path, sliced, budget_s):
-    """Slice 0 evaluated step by step in path order for about budget_s seconds (used only when
-    a complete slice would not finish in the bench's time; the rate is then extrapolated).
-    Returns (FLOP done, seconds, steps done)."""
+def oracle_slice_steps(onet, path, sliced, index, budget_s):
+    """The oracle as it stands on slice `index`: the sigma-restricted leaves (contract.restrict)
+    contracted pairwise along the path (contract.contract_pair), i.e. contract.contract_along
+    step by step, stopping after budget_s seconds.  Returns (s_sigma or None if it stopped
+    early, FLOP done, seconds, steps done)."""
     from oracle import contract, cost
 
     steps = cost.tree_info(onet, path, sliced)
-    assign = {l: 0 for l in sliced}
+    assign = contract.slice_assignment(onet, sliced, index)
     vals, labs = {}, {}
+    t0 = time.perf_counter()
     for t in range(onet.n_tensors):
         vals[t], labs[t] = contract.restrict(onet.tensors[t], onet.labels[t], assign)
     nid = onet.n_tensors
     done_flop, n_done = 0, 0
-    t0 = time.perf_counter()
     for (i, j), (flop, _) in zip(path, steps):
         vals[nid], labs[nid] = contract.contract_pair(vals.pop(i), labs.pop(i), vals.pop(j), labs.pop(j))
         nid += 1
         done_flop += flop
         n_done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    return done_flop, time.perf_counter() - t0, n_done
+        if n_done < len(path) and time.perf_counter() - t0 > budget_s:
+            return None, done_flop, time.perf_counter() - t0, n_done
+    (root,) = vals.keys()
+    return complex(vals[root]), done_flop, time.perf_counter() - t0, n_done
 
 
 def c2_single_thread_rate():
@@ -212,51 +202,44 @@ def c2_single_thread_rate():
         from threadpoolctl import threadpool_limits
 
         with threadpool_limits(1):
-            _, sec = oracle_complete_slice(onet, path, sl, 0)
+            _, _, sec, _ = oracle_slice_steps(onet, path, sl, 0, 1e9)
     except ImportError:
         return None
     return {"seconds": round(sec, 3), "gflops": fl / sec / 1e9, "threads": 1, "flop_sl": fl}
 
 
-def oracle_run(circ, bits, path, sliced, indices, goldens, max_slice_s, partial_budget_s):
+def oracle_run(circ, bits, path, sliced, indices, goldens, max_slice_s):
     """Time the oracle on complete slices `indices` of the plan (each compared with its golden
-    value when one is stored).  When a complete slice is predicted to exceed max_slice_s (from
-    a bounded partial-slice rate), fall back to that partial sample, extrapolated by FLOP_sl.
+    value when one is stored).  A slice still running after max_slice_s ends the run: the rate
+    of that partial slice is extrapolated by FLOP_sl and the result is labelled so.
     Returns a dict with slices/s and the sample description."""
     from oracle.network import build_network
 
     onet = build_network(circ, bits)
     fl_sl = oracle_flop_sl(onet, path, sliced)
-    # predict: a short partial sample (small early steps run slower than the big ones, so the
-    # prediction is conservative)
-    pf, ps, pn = oracle_partial_slice(onet, path, sliced, min(partial_budget_s, 5.0))
-    pred = fl_sl / (pf / ps) if pf > 0 else float("inf")
-    if pn >= len(path):
-        pred = ps
-    if pred > max_slice_s:
-        fl, sec, n = oracle_partial_slice(onet, path, sliced, partial_budget_s)
-        rate = fl / sec
-        return {"value": rate / fl_sl, "complete": False, "seconds": [sec], "flop_sl": fl_sl,
-                "sample": (f"slice 0, first {n} of {len(path)} path steps ({fl:.3g} of FLOP_sl {fl_sl:.3g}) in "
-                           f"{sec:.1f} s = {rate / 1e9:.2f} GFLOP/s, extrapolated: slices/s = rate / FLOP_sl "
-                           f"(a complete slice was predicted to take {pred:.0f} s)")}
     secs, errs = [], []
     for i in indices:
-        v, sec = oracle_complete_slice(onet, path, sliced, i)
+        v, fl, sec, n = oracle_slice_steps(onet, path, sliced, i, max_slice_s)
+        if v is None:
+            rate = fl / sec
+            return {"value": rate / fl_sl, "complete": False, "seconds": [round(sec, 2)], "flop_sl": fl_sl,
+                    "sample": (f"slice {i}, first {n} of {len(path)} path steps ({fl:.3g} of FLOP_sl {fl_sl:.3g}) "
+                               f"in {sec:.1f} s = {rate / 1e9:.2f} GFLOP/s, EXTRAPOLATED: slices/s = rate / FLOP_sl "
+                               f"(a complete slice did not finish within {max_slice_s:.0f} s)")}
         secs.append(sec)
         if i in goldens:
             errs.append(abs(v - goldens[i]) / abs(goldens[i]))
     tot = sum(secs)
     return {"value": len(indices) / tot, "complete": True, "seconds": [round(x, 2) for x in secs], "flop_sl": fl_sl,
             "golden_max_rel_diff": max(errs) if errs else None,
-            "sample": (f"{len(indices)} complete slice(s) {list(indices)} of the benched plan, {tot:.1f} s "
-                       f"({len(indices) * fl_sl / tot / 1e9:.2f} GFLOP/s at FLOP_sl {fl_sl:.3g}); no prefix cache "
-                       f"(the oracle recomputes every node per slice)")}
+            "sample": (f"{len(indices)} complete slice(s) {list(indices)} of the benched plan in {tot:.1f} s "
+                       f"({len(indices) * fl_sl / tot / 1e9:.2f} GFLOP/s at FLOP_sl {fl_sl:.3g}); the oracle "
+                       f"recomputes every node of every slice (no prefix cache)")}
 
 
 def cpu_baseline_entry(circ, bits, plan_path, plan_sliced, goldens, args):
     idx = [min(goldens)] if goldens else [0]
-    r = oracle_run(circ, bits, plan_path, plan_sliced, idx, goldens, args.cpu_max_slice_s, args.cpu_budget_s)
+    r = oracle_run(circ, bits, plan_path, plan_sliced, idx, goldens, args.cpu_max_slice_s)
     return {
         "value": r["value"], "unit": "slices/s", "cores": blas_threads(), "kind": "oracle",
         "sample": r["sample"], "complete_slices": r["complete"], "slice_seconds": r["seconds"],
@@ -400,11 +383,11 @@ def run_reference(args, cfg):
     goldens = load_goldens(args.config, rec)
     onet = build_network(circ, bits)
     n_sl = rec["cost"]["n_sl"]
-    for _ in range(args.warmup):
-        oracle_partial_slice(onet, path, sl, 2.0)
+    for _ in range(args.warmup):   # untimed, bounded: the first path steps of slice 0
+        oracle_slice_steps(onet, path, sl, 0, 2.0)
     idx = sorted(goldens) or [0]
     picks = [idx[s % len(idx)] for s in range(args.steps)]
-    r = oracle_run(circ, bits, path, sl, picks, goldens, args.cpu_max_slice_s, args.cpu_budget_s)
+    r = oracle_run(circ, bits, path, sl, picks, goldens, args.cpu_max_slice_s)
     value = r["value"]
     cores = blas_threads()
     sps = args.slices_per_step or cfg["sps"]

@@ -1,5 +1,5 @@
 """Print the key metrics of an ncu report (one line per metric) for profiles/ summaries."""
-import csv, subprocess, sys
+import csv, re, subprocess, sys
 
 WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
         'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
@@ -20,6 +20,11 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'smsp__average_warps_issue_stalled_drain_per_issue_active.ratio',
         'smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio',
         'smsp__issue_active.avg.pct_of_peak_sustained_active']
+# tensor / FP64 pipe evidence (names differ between ncu sections: every raw metric matching these)
+PIPE = re.compile(r'^(sm__pipe_tensor.*pct_of_peak_sustained_active|sm__pipe_fp64.*pct_of_peak_sustained_active|'
+                  r'smsp__pipe_tensor.*pct_of_peak_sustained_active|sm__inst_executed_pipe_(tc|tensor|tmem|uniform).*sum|'
+                  r'sm__ops_path_tensor_op_(utchmma_src_tf32|dmma).*\.sum$|sm__pipe_shared_cycles_active.*pct.*active|'
+                  r'l1tex__data_pipe_tc_wavefronts.*sum$|sm__mem_tensor_(reads|writes).*sum$)')
 
 def summary(path):
     out = subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
@@ -27,7 +32,8 @@ def summary(path):
     h, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
-        res.append((r[h.index('Kernel Name')], [(w, r[h.index(w)], units[h.index(w)]) for w in WANT if w in h]))
+        extra = [w for w in h if PIPE.match(w) and w not in WANT]
+        res.append((r[h.index('Kernel Name')], [(w, r[h.index(w)], units[h.index(w)]) for w in WANT + extra if w in h]))
     return res
 
 if __name__ == "__main__":

@@ -1,18 +1,20 @@
-"""Time the heaviest nodes of a bench plan one by one (kernel tuning on real shapes)."""
+"""Time the heaviest nodes of a benched plan (plans/<cfg>.json) one by one, back to back
+(kernel tuning on real shapes), with the clocks seen during the run.
+
+  python scripts/node_bench.py C3 [n_nodes]"""
 import json, os, sys
 sys.path.insert(0, '.')
 import torch
 from circuits import workload
 from paper_2107_09793_b200 import jet
-from paper_2107_09793_b200.runtime import plan_best
+import bench
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
-k, dt, cap = {"C3": (10, "c64", 0), "C2": (6, "c64", 0), "C5": (-1, "c64", 30), "C4": (-1, "c128", 28),
-              "G88d8": (-1, "c128", 30)}[cfg]
-circ, bits = workload(cfg)
+rec = bench.load_plan_file(cfg)   # the committed benched plan
+dt = rec["dtype"]
+circ, bits = workload(rec["circuit"], rec["circuit_seed"])
 net = jet.Network.from_circuit(circ, bits)
-plan, info = plan_best(net, k, dtype=dt, seeds=(1,) if dt == "c64" else (1, 2), trials=1024 if dt == "c64" else 4096,
-                       width_cap=cap)
+plan = jet.Plan.create(net, [tuple(x) for x in rec["ssa_path"]], rec["sliced_labels"])
 d = plan.describe_exec(dt)
 order = d["nodes"]
 stream = torch.cuda.Stream()
@@ -24,6 +26,8 @@ torch.cuda.synchronize()
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
 wkey = "bytes" if dt == "c64" else "flop"
 cands = sorted(range(len(order)), key=lambda i: -order[i][wkey] * (circ.d ** (order[i]["maxpos"] + 1)))[:int(sys.argv[2]) if len(sys.argv) > 2 else 8]
+clk = bench.ClockSampler(0)
+clk.start()
 for i in cands:
     n = order[i]
     r = ex.time_node(i, reps=5)
@@ -32,3 +36,4 @@ for i in cands:
     print(json.dumps({"idx": i, "kind": r["kind"], "ms": round(r["ms"], 4), "GBps": round(gbs), "frac_hbm": round(gbs / peak, 3),
                       "TFs": round(tfs, 1), "tm": n.get("tc_tm"), "tk": n.get("tc_tk"), "outer": n.get("tc_outer"),
                       "k2": [n["tm"], n["tn"], n["tk"], n["n_outer"], n["n_ok"], n["splits"], n["RM"], n["RN"]]}), flush=True)
+print(json.dumps({"clocks": clk.stop()}), flush=True)
