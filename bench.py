@@ -99,8 +99,11 @@ def load_goldens(name, rec):
     if rec is None or not os.path.exists(p):
         return {}
     g = json.load(open(p))
-    if g.get("plan_sha") != plan_sha(rec):
-        log(f"warning: {p} was written for another plan; parity not checked")
+    from circuits import workload
+
+    _, bits = workload(rec["circuit"], rec["circuit_seed"])
+    if g.get("plan_sha") != plan_sha(rec) or g.get("bitstring", [int(b) for b in bits]) != [int(b) for b in bits]:
+        log(f"warning: {p} was written for another plan or bitstring; parity not checked")
         return {}
     return {int(k): complex(v["re"], v["im"]) for k, v in g["slices"].items()}
 

@@ -3,6 +3,7 @@
 // the one-copy prefix cache -- the paper's shared-work reuse: a node
 // v depends only on the slice digits of S(v); with slices in lexicographic order, v is
 // recomputed only when a digit at a position <= maxpos(S(v)) changes.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -47,6 +48,7 @@ struct ExecNode {
   TcgArgs tcg{};
   std::vector<int64_t> tcgA_m, tcgA_k, tcgB_oN, tcgA_oM;  // K3g host strides (emulator)
   std::vector<int64_t> tcB_n, tcB_k;  // K3: B strides of the 7 row bits and the K bits (emulator)
+  std::vector<std::pair<int64_t, int>> tma_dims;  // K3 TMA box dims: (stride in elements, log2 size)
   int64_t v = -1;
   int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
   std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
@@ -100,11 +102,14 @@ TcgFn pick_tcg(int tmt) {
   fail(JT_EINTERNAL, "no tcg instance");
 }
 
-TcFn pick_tc(int tkc) {
-  switch (tkc) {
-    case 2: return gett_tc_kernel<2>;
-    case 3: return gett_tc_kernel<3>;
-    case 4: return gett_tc_kernel<4>;
+TcFn pick_tc(int tkc, bool tma) {
+  switch (tkc * 2 + (tma ? 1 : 0)) {
+    case 4: return gett_tc_kernel<2, false>;
+    case 5: return gett_tc_kernel<2, true>;
+    case 6: return gett_tc_kernel<3, false>;
+    case 7: return gett_tc_kernel<3, true>;
+    case 8: return gett_tc_kernel<4, false>;
+    case 9: return gett_tc_kernel<4, true>;
   }
   fail(JT_EINTERNAL, "no tc instance");
 }
@@ -149,9 +154,8 @@ void set_smem_attrs() {
       set(reinterpret_cast<const void*>(pick_gett<double>(a, b)), 200 * 1024);
       set(reinterpret_cast<const void*>(pick_dmma(a, b)), 200 * 1024);
     }
-  const void* tcs[3] = {reinterpret_cast<const void*>(gett_tc_kernel<2>), reinterpret_cast<const void*>(gett_tc_kernel<3>),
-                        reinterpret_cast<const void*>(gett_tc_kernel<4>)};
-  for (const void* f : tcs) set(f, 222 * 1024);
+  for (int tkc = 2; tkc <= 4; ++tkc)
+    for (int tma = 0; tma < 2; ++tma) set(reinterpret_cast<const void*>(pick_tc(tkc, tma != 0)), 222 * 1024);
   const void* tcgs[4] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
                          reinterpret_cast<const void*>(gett_tcg_kernel<6>), reinterpret_cast<const void*>(gett_tcg_kernel<7>)};
   for (const void* f : tcgs) set(f, 222 * 1024);
@@ -160,6 +164,18 @@ void set_smem_attrs() {
   set(reinterpret_cast<const void*>(permute_kernel<float2, 2>), 200 * 1024);
   set(reinterpret_cast<const void*>(permute_kernel<double2, 0>), 200 * 1024);
   done[dev] = 1;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+EncodeTiledFn get_encode_tiled() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  JT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) fail(JT_ECUDA, "exec: cuTensorMapEncodeTiled unavailable");
+  return reinterpret_cast<EncodeTiledFn>(fn);
 }
 
 int ilog2_exact(int d) {
@@ -202,8 +218,8 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   const int rbytes = 128 * (8 << tkc);
   const int64_t ybytes = 2LL * n_kc * yplane;
   const int64_t budget = 220 * 1024 - 1024 - ybytes;
-  int rs_cap = 6;  // JETB200_K3_RS: sweep knob for the raw gather ring depth
-  if (const char* e = std::getenv("JETB200_K3_RS")) rs_cap = std::max(2, std::min(6, atoi(e)));
+  int rs_cap = 6;  // JETB200_K3_RS: sweep knob for the raw ring depth (TMA path: up to 8)
+  if (const char* e = std::getenv("JETB200_K3_RS")) rs_cap = std::max(2, std::min(8, atoi(e)));
   const int rstages = (int)std::min<int64_t>(rs_cap, budget / rbytes);
   if (rstages < 2) return false;
   const int64_t smem = ybytes + (int64_t)rstages * rbytes + 1024;
@@ -266,6 +282,40 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
     t.vecB = (tb[0].first == 1 && tb[0].second == 8 && e && e[0] == '1') ? 1 : 0;
   }
   en.args.vecB = t.vecB;  // (reported by jt_exec_describe)
+  // TMA item load (default; JETB200_K3_TMA=0 keeps the cp.async gathers): the item's 7 + tkc bits
+  // sorted by B stride are split into runs of consecutive strides, each at most 8 bits (256
+  // elements, the TMA box limit); <= 5 runs -> one 5-D box per item, packed in stride order, so
+  // bit b lands at byte 8 << rank(b).  The item base offset is the dim-0 coordinate (int32).
+  {
+    const char* e = getenv("JETB200_K3_TMA");
+    const bool want = !(e && e[0] == '0');
+    std::vector<std::pair<int64_t, int>> bits;  // (stride, tag: row bit i = i, K bit j = 7 + j)
+    for (int i = 0; i < 7; ++i) bits.push_back({sb[tN[i]], i});
+    for (int j = 0; j < tkc; ++j) bits.push_back({sb[K[j].second], 7 + j});
+    std::sort(bits.begin(), bits.end());
+    std::vector<std::pair<int64_t, int>> dims;
+    for (size_t r = 0; r < bits.size(); ++r) {
+      if (!dims.empty() && bits[r].first == dims.back().first << dims.back().second && dims.back().second < 8)
+        ++dims.back().second;
+      else
+        dims.push_back({bits[r].first, 1});
+    }
+    int64_t reach = 1 << 11;  // highest element offset an item can touch (+ box), int32 coordinate
+    for (auto& x : vb.bits) reach += x.second;
+    for (auto& x : en.sliceB) reach += x.second * 3;  // digits < d <= 4
+    t.tma = (want && dims.size() <= 5 && bits[0].first == 1 && reach < (int64_t(1) << 31)) ? 1 : 0;
+    en.tma_dims.clear();
+    if (t.tma) {
+      en.tma_dims = dims;
+      for (size_t r = 0; r < bits.size(); ++r) {
+        const int tag = bits[r].second;
+        if (tag < 7) t.rofs_row[tag] = 8 << r;
+        else t.rofs_k[tag - 7] = 8 << r;
+      }
+      t.vecB = 0;
+      en.args.vecB = 0;
+    }
+  }
   for (int j = 0; j < kt - tkc; ++j) t.o_kB[j] = sb[K[tkc + j].second];
   for (int i = 0; i < tm; ++i) t.aM[i] = sa[M[i].second];
   for (int i = 0; i < kt; ++i) t.aK[i] = sa[K[i].second];
@@ -278,7 +328,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (int i = 0; i < kt; ++i) en.tcB_k.push_back(sb[K[i].second]);
   en.kind = 1;
   en.smem = (size_t)smem;
-  en.block = 416;
+  en.block = t.tma ? 448 : 416;
   en.n_out = t.n_tiles << (7 + tm);
   en.grid_x = t.n_tiles;
   en.args.splits = 1;
@@ -993,6 +1043,33 @@ void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector
       for (int i = 0; i < p.K; ++i) if ((k >> i) & 1) ao += p.aK[i];
       a[(size_t)m * nk + k] = A[ao];
     }
+  if (p.tma) {
+    // the TMA landing: the packed box of every item (dims = en.tma_dims, base = the dim-0
+    // coordinate) read back through rofs_row / rofs_k must be the item's B elements
+    std::vector<int64_t> box;
+    for (int64_t t = 0; t < p.n_tiles; ++t)
+      for (int c = 0; c < p.n_kc; ++c) {
+        int64_t base = 0;
+        for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
+        for (int j = 0; j < p.K - p.tkc; ++j) if ((c >> j) & 1) base += p.o_kB[j];
+        box.assign((size_t)128 << p.tkc, 0);
+        for (size_t e = 0; e < box.size(); ++e) {
+          int64_t o = base, rem = (int64_t)e;
+          for (auto& dm : en.tma_dims) {
+            o += (rem & ((int64_t(1) << dm.second) - 1)) * dm.first;
+            rem >>= dm.second;
+          }
+          box[e] = o;
+        }
+        for (int n = 0; n < 128; ++n)
+          for (int k = 0; k < (1 << p.tkc); ++k) {
+            int64_t want = base, ro = 0;
+            for (int i = 0; i < 7; ++i) if ((n >> i) & 1) { want += en.tcB_n[i]; ro += p.rofs_row[i]; }
+            for (int i = 0; i < p.tkc; ++i) if ((k >> i) & 1) { want += en.tcB_k[i]; ro += p.rofs_k[i]; }
+            if (box[(size_t)(ro / 8)] != want) fail(JT_EINTERNAL, "emulate: K3 TMA landing mismatch");
+          }
+      }
+  }
   for (int64_t t = 0; t < p.n_tiles; ++t) {
     int64_t base = 0;
     for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
@@ -1154,12 +1231,20 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
     const GettArgs& g = en.args;
     std::fprintf(f, "%s{\"v\": %lld, \"maxpos\": %d, \"flop\": %.17g, \"bytes\": %.17g, \"n_out\": %lld, "
                  "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
-                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld, \"parent\": %lld, \"pos\": %zu}",
+                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld, \"parent\": %lld, \"pos\": %zu",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
                  g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind,
                  en.kind == 2 ? en.tcg.tmt : en.tc.tm, en.kind == 2 ? 4 + en.tcg.lg_kc : en.tc.K,
                  en.kind == 2 ? en.tcg.n_oN + en.tcg.n_oM : en.tc.n_outer, (long long)L.node_off[en.v],
                  (long long)plan.nodes[en.v].parent, i);
+    if (en.kind == 1 || en.kind == 2) {  // big-operand strides of the tile rows and K bits
+      std::fprintf(f, ", \"Bn\": [");
+      for (size_t q = 0; q < en.tcB_n.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcB_n[q]);
+      std::fprintf(f, "], \"Bk\": [");
+      for (size_t q = 0; q < en.tcB_k.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcB_k[q]);
+      std::fprintf(f, "], \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : 0);
+    }
+    std::fprintf(f, "}");
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
@@ -1210,8 +1295,8 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
       continue;
     }
     if (en.kind == 1) {
-      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc)), 416,
-                                                            en.smem));
+      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc, en.tc.tma != 0)), en.block, en.smem));
       nb = std::min<int>(nb, 512 / (int)en.tc.tmem_cols);  // TMEM columns per SM
       if (nb < 1) fail(JT_EINTERNAL, "exec: a K3 tile does not fit on an SM");
       en.grid_x = std::min<int64_t>(en.tc.n_tiles, (int64_t)nb * n_sm);
@@ -1224,6 +1309,27 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     if (nb < 1) fail(JT_EINTERNAL, "exec: a contraction tile does not fit on an SM");
     const int64_t resident = (int64_t)nb * n_sm;
     en.grid_x = std::min<int64_t>(en.args.n_tiles, std::max<int64_t>(1, resident / en.args.splits));
+  }
+  // K3 TMA maps: B's item box at its workspace address (dim 0 declared 2^32 long: the item
+  // base offset is the dim-0 coordinate; see plan_tc)
+  for (ExecNode& en : L.order) {
+    if (en.kind != 1 || !en.tc.tma) continue;
+    static EncodeTiledFn encode = get_encode_tiled();
+    cuuint64_t gdim[5], gstr[4];
+    cuuint32_t box[5], est[5] = {1, 1, 1, 1, 1};
+    const auto& dm = en.tma_dims;
+    for (int i = 0; i < 5; ++i) {
+      const bool on = i < (int)dm.size();
+      box[i] = on ? (cuuint32_t)1 << dm[i].second : 1;
+      gdim[i] = box[i];
+      if (i > 0) gstr[i - 1] = (cuuint64_t)(on ? dm[i].first : dm.back().first << dm.back().second) * 8;
+    }
+    gdim[0] = (cuuint64_t)1 << 32;
+    void* base = static_cast<char*>(d_ws) + L.node_off[en.opB];
+    const CUresult r = encode(&en.tc.tmapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstr, box, est,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(JT_ECUDA, "exec: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   }
   auto* ex = new jt_exec();
   ex->L = std::move(L);
@@ -1340,7 +1446,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
-    launch_pdl(pick_tc(t.tkc), dim3((unsigned)en.grid_x), dim3(416), en.smem, ex->stream, ex->pdl, t);
+    launch_pdl(pick_tc(t.tkc, t.tma != 0), dim3((unsigned)en.grid_x), dim3(en.block), en.smem, ex->stream, ex->pdl, t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else {

@@ -11,14 +11,16 @@
 // split into hi = rna_tf32(x) and lo = x - hi, and D += Xhi*Yhi + Xhi*Ylo + Xlo*Yhi with FP32
 // accumulation in TMEM (1xTF32 misses 1e-4 over a deep tree, 3xTF32 does not).
 //
-// Shared-memory operands use the UMMA K-major SWIZZLE_NONE canonical layout: core matrices of
-// 8 rows x 16 B; LBO = 128 B (next core matrix along K), SBO = (K'/4) * 128 B (next 8 rows).
-// Every tile bit contributes a fixed byte offset in that layout, so the gather into it uses
-// the same lo/hi offset tables as K2.  One CTA = 256 threads; thread 0 issues the MMAs; all
-// threads prefetch the next tile's B into registers while the current tile's epilogue
-// (tcgen05.ld -> 256-B coalesced stores) runs.
+// Y (the expanded small operand, hi and lo planes, every K chunk) stays resident in shared
+// memory in the UMMA K-major layout (SWIZZLE_128B when a chunk holds 16 complex, else the
+// SWIZZLE_NONE canonical layout: core matrices of 8 rows x 16 B, LBO 128 B, SBO (K'/4)*128 B).
+// X (the streamed big operand) is split into hi/lo by producer warps and written to tensor
+// memory, from which the MMA reads it (the "TS" form).  See gett_tc_kernel below for the
+// warp roles; B items reach shared memory either by one TMA box per item (cp.async.bulk.tensor,
+// the default when the item's address bits form <= 5 runs) or by per-element cp.async gathers.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,6 +31,8 @@ namespace jt {
 constexpr int kTcMaxTile = 12;  // 7 row bits + up to 5 K bits per chunk
 
 struct TcArgs {
+  CUtensorMap tmapB;  // TMA map of B's item (<= 5 dims = the item bits' stride runs; dim 0 is
+                      // declared 2^32 long so the item base offset is its coordinate); tma = 1
   const float2* A;  // small operand (all bits in the tile)
   const float2* B;  // big operand
   float2* C;        // output, layout [7 row (n) bits][tm bits][outer bits]
@@ -51,6 +55,9 @@ struct TcArgs {
   int8_t swz_row[3];                           // row bits (lowest B stride first) that drive the raw-row swizzle
   int32_t vecB;                                // 1: chunk-tile bit 0 is a K bit at global stride 1
                                                //    -> gather k-pairs as 16-B copies
+  int32_t tma;                                 // 1: items arrive by TMA (gett_tc_kernel<TKC, true>)
+  int32_t rofs_row[7], rofs_k[5];              // TMA landing: byte offset of row bit i / chunk K bit j
+                                               //   (the box is packed in B-stride order: 8 << rank)
   SliceView sv;
 };
 
@@ -148,14 +155,9 @@ __device__ __forceinline__ float tf32_hi(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// 3xTF32 split by truncation: hi = x with the low 13 mantissa bits cleared (exactly a TF32
-// value, so the MMA reads it exactly whatever its own rounding), lo = x - hi (exact in fp32);
-// lo is then read at TF32 precision (relative error 2^-11 of lo, ~2^-22 of x).
-// Round-to-nearest TF32 (low 13 mantissa bits zero).  The 3xTF32 split is hi = rna(x),
-// lo = rna(x - hi): both are exact TF32 inputs, so |x - hi - lo| <= 2^-22 |x| and the MMA's
-// own handling of the low mantissa bits never enters (a truncated split loses ~4x more).
-// (Integer form of cvt.rna.tf32.f32, which ptxas expands with an Inf/NaN branch; the
-// operands here are finite.)
+// Round-to-nearest TF32 (low 13 mantissa bits zero): hi = rna(x) is an exact TF32 value, so the
+// MMA reads it exactly whatever its own handling of the low mantissa bits.  (Integer form of
+// cvt.rna.tf32.f32, which ptxas expands with an Inf/NaN branch; the operands here are finite.)
 __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
@@ -165,6 +167,18 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // only by a factor of 2, and 2^-21 is ~15x below fp32-accumulate rounding over a 16-term K step).
 // Saves two integer ops per value on the producers' critical path.
 __device__ __forceinline__ float tf32_lo(float x, float hi) { return x - hi; }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// One TMA box (5-D tiled map; unused dims have size 1) into shared memory, completing on `bar`.
+__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, int c0, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %3, %3, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
 
 }  // namespace tc
 
@@ -182,10 +196,13 @@ __device__ __forceinline__ int tc_off(int r, int kk, int sbo, int swz) {
 //              hi/lo TF32 and writes both into a TMEM X stage with tcgen05.st
 //   warp 12    MMA issuer: tcgen05.mma kind::tf32 with A = X from TMEM ([a_tmem], the "TS" form)
 //              and B = Y (expanded small operand, resident in shared memory), 3xTF32
-// Barriers: xfull/xempty per TMEM X stage, tfull/tempty per accumulator.
+//   warp 13    (TMA = true) TMA issuer: one cp.async.bulk.tensor box per item into the raw ring;
+//              the producers then only read their row from shared memory, split and store
+// Barriers: xfull/xempty per TMEM X stage, tfull/tempty per accumulator, rfull/rempty per raw
+// stage (TMA = true; without TMA the producers sync on a named barrier per item instead).
 // TKC = K bits per chunk (row of the X stage = 2*2^TKC TF32 = hi or lo).
-template <int TKC>
-__global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
+template <int TKC, bool TMA>
+__global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __grid_constant__ TcArgs p) {
   constexpr int PER = (128 << TKC) / 256;  // B elements each producer thread copies per item
   constexpr int NCOL = 1 << TKC;           // fp32 columns (of hi or lo) each producer thread writes
   constexpr int KPC = 2 << TKC;            // TF32 columns of one X row (hi or lo)
@@ -193,7 +210,7 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
   __shared__ int64_t kc_off[16];  // B offset of K chunk c (n_kc <= 16)
-  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2], rfull[8], rempty[8];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < 16) {
@@ -234,8 +251,14 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 128);
     }
+    if (TMA)
+      for (int i = 0; i < p.rstages; ++i) {
+        tc::mbar_init(&rfull[i], 1);   // the issuer's expect_tx arrival + the TMA bytes
+        tc::mbar_init(&rempty[i], 8);  // one arrival per producer warp
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (TMA && warp == 13 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmapB) : "memory");
   pdl_wait();  // the operands are written by the previous kernels of the sequence
   pdl_launch_dependents();
   // ---- Y = expanded small operand (hi/lo) for every K chunk: row = 2m+s, col = 2k+t
@@ -276,7 +299,83 @@ __global__ void __launch_bounds__(416, 1) gett_tc_kernel(const __grid_constant__
   const uint32_t lbo = p.swz ? 16u : 128u;
   const uint32_t kstep = p.swz ? 32u : 256u;  // Y descriptor advance per 8-TF32 K step
 
-  if (warp >= 4 && warp < 12) {
+  if (TMA && warp >= 4 && warp < 12) {
+    // ===================== producers (TMA-fed) =====================
+    // the item landed as one box packed in B-stride order: element (row n, complex k) sits at
+    // byte rofs(n) + kofs(k); each thread reads its row's half of the chunk, splits, stores to TMEM
+    constexpr int NQ = 1 << (TKC - 1);  // complex per thread per item
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int row = quarter * 32 + lane;
+    int32_t roff = 0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) roff += ((row >> i) & 1) ? p.rofs_row[i] : 0;
+    int32_t koff[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int k = half * NQ + q;
+      int32_t o = 0;
+#pragma unroll
+      for (int j = 0; j < TKC; ++j) o += ((k >> j) & 1) ? p.rofs_k[j] : 0;
+      koff[q] = o;
+    }
+    const int RS = p.rstages, XS = p.xstages;
+    int rst = 0, xs = 0;
+    uint32_t rph = 0, xph = 0;
+    for (int64_t it = 0; it < items; ++it) {
+      tc::mbar_wait(&rfull[rst], rph);
+      const unsigned char* raw = R + rst * p.rbytes + roff;
+      float hi[NCOL], lo[NCOL];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float2 v = *reinterpret_cast<const float2*>(raw + koff[q]);
+        hi[2 * q] = tc::tf32_rna(v.x);
+        lo[2 * q] = tc::tf32_lo(v.x, hi[2 * q]);
+        hi[2 * q + 1] = tc::tf32_rna(v.y);
+        lo[2 * q + 1] = tc::tf32_lo(v.y, hi[2 * q + 1]);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&rempty[rst]);  // this warp is done with the raw stage
+      if (++rst == RS) { rst = 0; rph ^= 1; }
+      tc::mbar_wait(&xempty[xs], xph ^ 1);  // TMEM X stage free
+      tc::fence_after();
+      const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+      const uint32_t col = xcol0 + (uint32_t)(xs * 2 * KPC + half * NCOL);
+      tc::tmem_st<NCOL>(lane_addr + col, hi);
+      tc::tmem_st<NCOL>(lane_addr + col + KPC, lo);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&xfull[xs]);
+      if (++xs == XS) { xs = 0; xph ^= 1; }
+    }
+  } else if (TMA && warp == 13) {
+    // ===================== TMA issuer =====================
+    const int64_t boff = slice_off(p.sv, false);
+    const int64_t o_s = lane < p.n_outer ? p.o_sB[lane] : 0;
+    auto tile_base = [&](int64_t ct) {
+      const int64_t t = (int64_t)blockIdx.x + ct * gridDim.x;
+      int64_t tb = ((t >> lane) & 1) ? o_s : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tb += __shfl_xor_sync(0xffffffffu, tb, o);
+      return boff + tb;
+    };
+    const int RS = p.rstages;
+    int64_t ct = 0, cbase = tile_base(0);
+    int cc = 0, wst = 0;
+    uint32_t wph = 0;
+    for (int64_t it = 0; it < items; ++it) {
+      if (lane == 0) {
+        if (it >= RS) tc::mbar_wait(&rempty[wst], wph ^ 1);  // all producer warps released it
+        tc::mbar_expect_tx(&rfull[wst], (uint32_t)p.rbytes);
+        tc::tma_load5(R + wst * p.rbytes, &p.tmapB, (int)(cbase + kc_off[cc]), &rfull[wst]);
+      }
+      if (++wst == RS) { wst = 0; wph ^= 1; }
+      if (++cc == p.n_kc) {
+        cc = 0;
+        ++ct;
+        cbase = tile_base(ct);
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
     // ===================== producers =====================
     const int ptid = tid - 128;  // 0..255
     const int64_t boff = slice_off(p.sv, false);

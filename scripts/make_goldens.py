@@ -72,15 +72,33 @@ def main():
     net = build_network(circ, bits)
     path = [tuple(s) for s in plan["ssa_path"]]
     sl = list(plan["sliced_labels"])
-    rep = cost.cost_report(net, path, sl)
-    n_sl = rep["n_sl"]
+    steps = cost.tree_info(net, path, sl)       # (cost_report would enumerate all N_sl slices)
+    rep = {"flop_sl": sum(f for f, _ in steps)}
+    n_sl = 1
+    for l in sl:
+        n_sl *= net.dims[l]
     if args.indices:
         idx = sorted(int(x) for x in args.indices.split(","))
     else:
         idx = picks_for(n_sl, min(args.blocks, n_sl), args.per_block, args.seed)
     out_path = os.path.join(ROOT, "tests", "golden", f"parity_{args.config}.json")
     old = json.load(open(out_path)) if os.path.exists(out_path) else {}
-    slices = {int(k): v for k, v in old.get("slices", {}).items()} if old.get("plan_sha") == plan_sha(plan) else {}
+    same = old.get("plan_sha") == plan_sha(plan) and old.get("bitstring", list(bits)) == [int(b) for b in bits]
+    slices = {int(k): v for k, v in old.get("slices", {}).items()} if same else {}
+    def write():
+        rec = {
+            "config": args.config, "plan": f"plans/{args.config}.json", "plan_sha": plan_sha(plan),
+            "bitstring": [int(b) for b in bits],
+            "what": "oracle s_sigma (complex128 numpy, oracle/contract.py) of the sigma-restricted network "
+                    "along the plan's SSA path; PAPER.md l.95-105 (Eq. seq), l.123-128 (Eq. sliced_sum)",
+            "script": "scripts/make_goldens.py (imports only oracle/ and circuits/)",
+            "n_sl": n_sl, "flop_sl": rep["flop_sl"], "blocks": args.blocks,
+            "host": {"cpu_model": cpu_model(), "threads": blas_threads(), "nproc": os.cpu_count()},
+            "slices": {str(k): slices[k] for k in sorted(slices)},
+        }
+        with open(out_path, "w") as f:
+            json.dump(rec, f, indent=1)
+
     for i in idx:
         if i in slices:
             continue
@@ -91,17 +109,8 @@ def main():
         import resource
         rss = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6
         print(f"{args.config} slice {i}: {v!r} ({dt:.1f} s, max rss {rss:.1f} GB)", flush=True)
-        rec = {
-            "config": args.config, "plan": f"plans/{args.config}.json", "plan_sha": plan_sha(plan),
-            "what": "oracle s_sigma (complex128 numpy, oracle/contract.py) of the sigma-restricted network "
-                    "along the plan's SSA path; PAPER.md l.95-105 (Eq. seq), l.123-128 (Eq. sliced_sum)",
-            "script": "scripts/make_goldens.py (imports only oracle/ and circuits/)",
-            "n_sl": n_sl, "flop_sl": rep["flop_sl"], "blocks": args.blocks,
-            "host": {"cpu_model": cpu_model(), "threads": blas_threads(), "nproc": os.cpu_count()},
-            "slices": {str(k): slices[k] for k in sorted(slices)},
-        }
-        with open(out_path, "w") as f:
-            json.dump(rec, f, indent=1)
+        write()
+    write()
 
 
 def plan_sha(plan):

@@ -91,7 +91,7 @@ def test_describe_exec_layout(jet):
     d = plan.describe_exec("c64")
     assert d["total_bytes"] == plan.workspace_bytes("c64")
     for n in d["nodes"]:
-        assert n["block"] % 32 == 0 and n["block"] <= (416 if n["kind"] == 1 else 256)
+        assert n["block"] % 32 == 0 and n["block"] <= (448 if n["kind"] == 1 else 256)
         if n["kind"] in (1, 2):   # K3 / K3g: 128-row MMA tiles
             assert n["n_out"] == 2 ** (7 + n["tc_tm"] + n["tc_outer"])
             assert 3 <= n["tc_tm"] <= 7 and 2 <= n["tc_tk"] and n["smem"] <= 220 * 1024
@@ -104,7 +104,9 @@ def test_emulated_k3_matches_oracle_c2_slices(jet):
     circ, bits = workload("C2")
     net = jet.Network.from_circuit(circ, bits)
     plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6, bytes_weight=5.0)
-    assert sum(n["kind"] for n in plan.describe_exec("c64")["nodes"]) > 0
+    nodes = plan.describe_exec("c64")["nodes"]
+    assert sum(n["kind"] for n in nodes) > 0
+    assert any(n["kind"] == 1 and n["tma"] for n in nodes)   # the TMA landing is emulated too
     ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[5]))
     v = jet.debug_emulate_host(plan, 5, 6, "c64")
     assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4

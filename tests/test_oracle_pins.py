@@ -393,3 +393,22 @@ def test_cost_identities_bruteforce(c1):
         a = cost.prefix_flop(net, p, sl, 0, half)
         b = cost.prefix_flop(net, p, sl, half, rep["n_sl"])
         assert a + b >= rep["prefix"]
+
+
+def test_p7_slice_closed_form_matches_oracle():
+    """The P7 per-slice closed form (tests/p7_closed.py) used to pin the GPU path at C3/C5 size
+    equals the oracle's s_sigma on a 3x3 grid with fSim(0, 0) = I, for random sliced labels and
+    every slice (and so do their sums, Eq. sliced_sum)."""
+    from circuits.sycamore import grid_qubits, random_circuit
+    from p7_closed import slice_closed_form
+
+    circ = random_circuit(grid_qubits(3, 3), 8, seed=3, theta=0.0, phi=0.0)
+    rng = np.random.default_rng(4)
+    for t in range(4):
+        bits = [int(b) for b in rng.integers(0, 2, size=9)]
+        net = build_network(circ, bits)
+        p = path.greedy_path(net)
+        sl = [int(x) for x in rng.choice(sorted(net.dims), size=4, replace=False)]
+        ref = contract.slice_values(net, p, sl)
+        for i, r in enumerate(ref):
+            assert abs(slice_closed_form(circ, bits, sl, i) - r) < 1e-13
