@@ -203,7 +203,9 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   const int tm = (int)M.size(), kt = (int)K.size();
   // (1-2 free bits of A run through the padded-N path correctly but measured slower than K2 on
   // the C3 streaming nodes -- 8-KB gather items -- so K3 takes 3..7)
-  if (tm < 3 || tm > 7 || kt < 2 || kt > 8 || (int)N.size() < 7) return false;
+  int min_tm = 3;  // JETB200_K3_MINTM: sweep knob (1-2 free bits of A run on the padded-N path)
+  if (const char* e = std::getenv("JETB200_K3_MINTM")) min_tm = std::max(1, std::min(3, atoi(e)));
+  if (tm < min_tm || tm > 7 || kt < 2 || kt > 8 || (int)N.size() < 7) return false;
   const int swz = kt >= 4 ? 1 : 0;        // SWIZZLE_128B needs 32 TF32 (16 complex) per row
   const int tkc = swz ? 4 : kt;
   const int n_kc = 1 << (kt - tkc);
