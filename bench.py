@@ -318,8 +318,8 @@ def tensor_peak_alg(dtype):
     return bf16 * 0.5 / 3.0, f"measured bf16 {bf16} x 0.5 (TF32) / 3 (3xTF32)"
 
 
-KERNEL_NAMES = {"K3": "tcgen05 3xTF32, resident small operand", "K3G": "tcgen05 3xTF32, both operands streamed",
-                "K2": "CUDA-core GETT", "K4": "FP64 tensor-core DMMA GETT"}
+KERNEL_NAMES = {"K3": "tcgen05 3xTF32, resident small operand, TMA-fed", "K3G": "tcgen05 3xTF32, both operands streamed",
+                "K2": "CUDA-core GETT", "K4": "FP64 tensor-core DMMA GETT", "K2S": "TMA-fed streaming GETT (skinny)"}
 
 
 def roofline_entry(args, dom, gbs, tfs, dom_bytes, dom_n, dom_ms, peak, peak_kind, ms_max, prof_steps, kern, dtype):
@@ -584,18 +584,19 @@ def run_ours(args, cfg):
     # (the K2 counters hold every timed contraction launch; K3 and K4 are subsets)
     # (K3 counters include K3g; split them: K3 = resident small operand, K3g = both streamed)
     cls = {}
-    for key in ("k3", "k4", "k3g"):
+    for key in ("k3", "k4", "k3g", "k2s"):
         cls[key.upper()] = (pst[f"{key}_time_ms"], pst[f"{key}_timed_bytes"], pst[f"{key}_timed_launches"],
                             pst[f"{key}_timed_flop"])
     cls["K3"] = tuple(a - b for a, b in zip(cls["K3"], cls["K3G"]))
-    cls["K2"] = tuple(pst[f"k2_{f}"] - cls["K3"][i] - cls["K3G"][i] - cls["K4"][i]
+    cls["K2"] = tuple(pst[f"k2_{f}"] - cls["K3"][i] - cls["K3G"][i] - cls["K4"][i] - cls["K2S"][i]
                       for i, f in enumerate(("time_ms", "timed_bytes", "timed_launches", "timed_flop")))
     dom = max(cls, key=lambda q: cls[q][0])
     dom_ms, dom_bytes, dom_n, dom_flop = cls[dom]
     dom_n = int(dom_n)
     dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     dom_tfs = dom_flop / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
-    names = {"K3": "K3_tcgen05", "K3G": "K3g_tcgen05_streamed", "K2": "K2_cuda_core", "K4": "K4_dmma_fp64"}
+    names = {"K3": "K3_tcgen05", "K3G": "K3g_tcgen05_streamed", "K2": "K2_cuda_core", "K4": "K4_dmma_fp64",
+             "K2S": "K2s_tma_stream"}
     kern_info = {names[q]: {"launches": int(v[2]), "ms": v[0], "GBps": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 else None,
                             "TFLOPs_alg": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else None}
                  for q, v in cls.items()}

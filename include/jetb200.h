@@ -124,6 +124,11 @@ typedef struct {
   int64_t k3g_timed_launches;
   double k3g_timed_bytes;
   double k3g_timed_flop;
+  double k2s_time_ms;         /* ... the subset of the timed launches that ran on K2s (TMA-fed
+                                 streaming GETT for skinny c64 nodes; not counted under K3) */
+  int64_t k2s_timed_launches;
+  double k2s_timed_bytes;
+  double k2s_timed_flop;
 } jt_exec_stats;
 
 const char* jt_last_error(void);

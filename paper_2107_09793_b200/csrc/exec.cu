@@ -21,6 +21,7 @@
 #include "kernels_tc.cuh"
 #include "kernels_tcg.cuh"
 #include "kernels_dmma.cuh"
+#include "kernels_stream.cuh"
 
 #define JT_CUDA(x)                                                                        \
   do {                                                                                    \
@@ -43,7 +44,10 @@ struct View {
 };
 
 struct ExecNode {
-  int kind = 0;  // 0: K2 CUDA-core GETT, 1: K3 tcgen05 (resident A), 2: K3g tcgen05 (streamed A)
+  int kind = 0;  // 0: K2 CUDA-core GETT, 1: K3 tcgen05 (resident A), 2: K3g tcgen05 (streamed A),
+                 // 3: K4 DMMA (c128), 4: K2s TMA-fed streaming GETT (skinny c64)
+  StreamArgs st{};
+  std::vector<int64_t> stN, stK;  // K2s: B strides of the 8 tile columns and the K bits (emulator)
   TcArgs tc{};
   TcgArgs tcg{};
   std::vector<int64_t> tcgA_m, tcgA_k, tcgB_oN, tcgA_oM;  // K3g host strides (emulator)
@@ -114,6 +118,16 @@ TcFn pick_tc(int tkc, bool tma) {
   fail(JT_EINTERNAL, "no tc instance");
 }
 
+using StreamFn = void (*)(StreamArgs);
+StreamFn pick_stream(int tm, int kt) {
+#define JT_SCASE(a, b) \
+  if (tm == a && kt == b) return stream_gett_kernel<a, b>;
+  JT_SCASE(0, 1) JT_SCASE(0, 2) JT_SCASE(0, 3) JT_SCASE(1, 1) JT_SCASE(1, 2) JT_SCASE(1, 3)
+  JT_SCASE(2, 1) JT_SCASE(2, 2) JT_SCASE(2, 3) JT_SCASE(3, 1) JT_SCASE(3, 2) JT_SCASE(3, 3)
+#undef JT_SCASE
+  fail(JT_EINTERNAL, "no stream instance");
+}
+
 GettFn pick_dmma(int SMT, int SNT) {
 #define JT_DCASE(a, b) \
   if (SMT == a && SNT == b) return gett_dmma_kernel<a, b>;
@@ -159,6 +173,8 @@ void set_smem_attrs() {
   const void* tcgs[4] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
                          reinterpret_cast<const void*>(gett_tcg_kernel<6>), reinterpret_cast<const void*>(gett_tcg_kernel<7>)};
   for (const void* f : tcgs) set(f, 222 * 1024);
+  for (int tm = 0; tm <= 3; ++tm)
+    for (int kt = 1; kt <= 3; ++kt) set(reinterpret_cast<const void*>(pick_stream(tm, kt)), 200 * 1024);
   set(reinterpret_cast<const void*>(permute_kernel<float2, 0>), 200 * 1024);
   set(reinterpret_cast<const void*>(permute_kernel<float2, 1>), 200 * 1024);
   set(reinterpret_cast<const void*>(permute_kernel<float2, 2>), 200 * 1024);
@@ -340,6 +356,104 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (auto b : tN) { out.bits.push_back({b, st}); st <<= 1; }
   for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
   for (auto b : oN) { out.bits.push_back({b, st}); st <<= 1; }
+  return true;
+}
+
+// TMA box of an item whose bits have the given B strides: runs of consecutive strides, each at
+// most 8 bits (the 256-element box limit), in stride order.  Returns false when the item needs
+// more than 5 dims or does not hold B's stride-1 bit.  rank[i] = the bit's position in the
+// packed box (it lands at byte 8 << rank).
+bool tma_item_dims(const std::vector<int64_t>& strides, std::vector<std::pair<int64_t, int>>& dims,
+                   std::vector<int>& rank) {
+  std::vector<std::pair<int64_t, int>> bits;
+  for (size_t i = 0; i < strides.size(); ++i) bits.push_back({strides[i], (int)i});
+  std::sort(bits.begin(), bits.end());
+  dims.clear();
+  for (auto& b : bits) {
+    if (!dims.empty() && b.first == dims.back().first << dims.back().second && dims.back().second < 8)
+      ++dims.back().second;
+    else
+      dims.push_back({b.first, 1});
+  }
+  rank.assign(strides.size(), 0);
+  for (size_t r = 0; r < bits.size(); ++r) rank[bits[r].second] = (int)r;
+  return dims.size() <= 5 && bits[0].first == 1;
+}
+
+bool tma_enabled() {
+  const char* e = std::getenv("JETB200_K3_TMA");
+  return !(e && e[0] == '0');
+}
+
+// K2s eligibility and descriptor (c64): A tiny (<= 3 free bits, 1..3 contracted bits), B with
+// >= 8 free bits; tiles of B's 8 lowest-stride free bits x all K bits, one TMA box each.
+// Output layout [M bits][8 tile bits][outer bits].  JETB200_K2S=0 disables it, JETB200_K2S_MAXTM
+// (default 2: tm = 3 goes to K3) sets the largest tm taken.
+bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& out) {
+  if (esize != 8 || !tma_enabled()) return false;
+  {
+    const char* e = std::getenv("JETB200_K2S");
+    if (e && e[0] == '0') return false;
+  }
+  int maxtm = 2;
+  if (const char* e = std::getenv("JETB200_K2S_MAXTM")) maxtm = std::max(0, std::min(3, atoi(e)));
+  std::map<int64_t, int64_t> sa, sb;
+  for (auto& x : va.bits) sa[x.first] = x.second;
+  for (auto& x : vb.bits) sb[x.first] = x.second;
+  std::vector<std::pair<int64_t, int64_t>> M, N, K;
+  for (auto& x : va.bits) {
+    if (sb.count(x.first)) K.push_back({sb[x.first], x.first});
+    else M.push_back({x.second, x.first});
+  }
+  for (auto& x : vb.bits)
+    if (!sa.count(x.first)) N.push_back({x.second, x.first});
+  const int tm = (int)M.size(), kt = (int)K.size();
+  if (tm > maxtm || kt < 1 || kt > 3 || (int)N.size() < 8 || (int)N.size() - 8 > kMaxOuter) return false;
+  std::sort(M.begin(), M.end());
+  std::sort(N.begin(), N.end());
+  std::sort(K.begin(), K.end());
+  std::vector<int64_t> item;
+  for (int i = 0; i < 8; ++i) item.push_back(N[i].first);
+  for (int j = 0; j < kt; ++j) item.push_back(K[j].first);
+  std::vector<std::pair<int64_t, int>> dims;
+  std::vector<int> rank;
+  if (!tma_item_dims(item, dims, rank)) return false;
+  int64_t reach = 1 << 11;
+  for (auto& x : vb.bits) reach += x.second;
+  for (auto& x : en.sliceB) reach += x.second * 3;
+  if (reach >= (int64_t(1) << 31)) return false;
+  StreamArgs& t = en.st;
+  std::memset(&t, 0, sizeof(t));
+  t.rbytes = 8 << (8 + kt);
+  t.rstages = std::min(8, (200 * 1024 - 1024) / t.rbytes);
+  t.n_outer = (int)N.size() - 8;
+  for (int j = 0; j < t.n_outer; ++j) t.o_sB[j] = N[8 + j].first;
+  for (int i = 0; i < 8; ++i) t.rofs_n[i] = 8 << rank[i];
+  for (int j = 0; j < kt; ++j) t.rofs_k[j] = 8 << rank[8 + j];
+  for (int i = 0; i < tm; ++i) t.aM[i] = M[i].first;
+  for (int j = 0; j < kt; ++j) t.aK[j] = sa[K[j].second];
+  t.n_tiles = int64_t(1) << t.n_outer;
+  en.tma_dims = dims;
+  en.stN.clear();
+  en.stK.clear();
+  for (int i = 0; i < 8; ++i) en.stN.push_back(N[i].first);
+  for (int j = 0; j < kt; ++j) en.stK.push_back(K[j].first);
+  en.kind = 4;
+  en.args.tm = tm;   // (reported by jt_exec_describe)
+  en.args.tk = kt;
+  en.args.tn = 8;
+  en.args.n_outer = t.n_outer;
+  en.args.splits = 1;
+  en.args.n_tiles = t.n_tiles;
+  en.smem = (size_t)t.rstages * t.rbytes + 1024;
+  en.block = 288;
+  en.n_out = t.n_tiles << (8 + tm);
+  en.grid_x = t.n_tiles;
+  out.bits.clear();
+  int64_t st = 1;
+  for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
+  for (int i = 0; i < 8; ++i) { out.bits.push_back({N[i].second, st}); st <<= 1; }
+  for (int j = 8; j < (int)N.size(); ++j) { out.bits.push_back({N[j].second, st}); st <<= 1; }
   return true;
 }
 
@@ -877,7 +991,8 @@ Layout compile(const jt_plan& plan, int esize) {
     if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
     if (en.sliceA.size() > 4 || en.sliceB.size() > 4) fail(JT_EUSAGE, "exec: more than 4 sliced labels on one leaf");
     View tv;
-    if (use_tc && !force_tcg && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
+    if (use_tc && plan_stream(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
+    else if (use_tc && !force_tcg && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
     else if (use_tc && plan_tcg(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
     else if (esize == 16 && use_dmma && plan_dmma(en, views[en.opA], views[en.opB], tv)) views[v] = tv;
     else views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
@@ -1032,6 +1147,58 @@ void emulate_gett(const GettArgs& p, char* ws, const ExecNode& en, const std::ve
   }
 }
 
+// K2s: the TMA landing of every tile (read back through rofs_n / rofs_k) and the output layout
+// [M][8 tile bits][outer], with the kernel's FP32 complex arithmetic order
+void emulate_stream(const StreamArgs& p, const ExecNode& en, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
+  const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
+  const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
+  float2* C = reinterpret_cast<float2*>(ws + off[2].first);
+  const int tm = en.args.tm, kt = en.args.tk, nm = 1 << tm, nk = 1 << kt;
+  std::vector<float2> a((size_t)nm * nk);
+  for (int m = 0; m < nm; ++m)
+    for (int k = 0; k < nk; ++k) {
+      int64_t ao = 0;
+      for (int i = 0; i < tm; ++i) if ((m >> i) & 1) ao += p.aM[i];
+      for (int i = 0; i < kt; ++i) if ((k >> i) & 1) ao += p.aK[i];
+      a[(size_t)m * nk + k] = A[ao];
+    }
+  std::vector<int64_t> box((size_t)256 << kt);
+  for (int64_t t = 0; t < p.n_tiles; ++t) {
+    int64_t base = 0;
+    for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
+    for (size_t e = 0; e < box.size(); ++e) {
+      int64_t o = base, rem = (int64_t)e;
+      for (auto& dm : en.tma_dims) {
+        o += (rem & ((int64_t(1) << dm.second) - 1)) * dm.first;
+        rem >>= dm.second;
+      }
+      box[e] = o;
+    }
+    for (int n = 0; n < 256; ++n) {
+      int64_t noff = 0, nb = base;
+      for (int i = 0; i < 8; ++i) if ((n >> i) & 1) { noff += p.rofs_n[i]; nb += en.stN[i]; }
+      float2 b[8];
+      for (int k = 0; k < nk; ++k) {
+        int64_t ko = 0, want = nb;
+        for (int j = 0; j < kt; ++j) if ((k >> j) & 1) { ko += p.rofs_k[j]; want += en.stK[j]; }
+        if (box[(size_t)((noff + ko) / 8)] != want) fail(JT_EINTERNAL, "emulate: K2s TMA landing mismatch");
+        b[k] = B[want];
+      }
+      for (int m = 0; m < nm; ++m) {
+        float re = 0.f, im = 0.f;
+        for (int k = 0; k < nk; ++k) {
+          const float2 x = a[(size_t)m * nk + k];
+          re = std::fma(x.x, b[k].x, re);
+          re = std::fma(-x.y, b[k].y, re);
+          im = std::fma(x.x, b[k].y, im);
+          im = std::fma(x.y, b[k].x, im);
+        }
+        C[(t << (8 + tm)) + ((int64_t)n << tm) + m] = make_float2(re, im);
+      }
+    }
+  }
+}
+
 void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
   const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
   const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
@@ -1150,7 +1317,8 @@ void emulate_host(const jt_plan& plan, int esize, int64_t b, int64_t e, double* 
       for (auto& sl : en.sliceB) offB += (int64_t)dig[sl.first] * sl.second;
       std::vector<std::pair<int64_t, int64_t>> offs = {{L.node_off[en.opA], offA}, {L.node_off[en.opB], offB},
                                                        {en.out_off, 0}, {en.part_off, 0}};
-      if (en.kind == 2) emulate_tcg(en.tcg, en, ws.data(), offs);
+      if (en.kind == 4) emulate_stream(en.st, en, ws.data(), offs);
+      else if (en.kind == 2) emulate_tcg(en.tcg, en, ws.data(), offs);
       else if (en.kind == 1) emulate_tc(en.tc, en, ws.data(), offs);
       else emulate_gett<R>(en.args, ws.data(), en, offs);
     }
@@ -1296,6 +1464,13 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
       en.grid_x = std::min<int64_t>(en.tcg.n_tiles, n_sm);  // one CTA per SM (512 TMEM columns)
       continue;
     }
+    if (en.kind == 4) {
+      JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &nb, reinterpret_cast<const void*>(pick_stream(en.args.tm, en.args.tk)), en.block, en.smem));
+      if (nb < 1) fail(JT_EINTERNAL, "exec: a K2s tile does not fit on an SM");
+      en.grid_x = std::min<int64_t>(en.st.n_tiles, (int64_t)nb * n_sm);
+      continue;
+    }
     if (en.kind == 1) {
       JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc, en.tc.tma != 0)), en.block, en.smem));
@@ -1315,7 +1490,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   // K3 TMA maps: B's item box at its workspace address (dim 0 declared 2^32 long: the item
   // base offset is the dim-0 coordinate; see plan_tc)
   for (ExecNode& en : L.order) {
-    if (en.kind != 1 || !en.tc.tma) continue;
+    if (!((en.kind == 1 && en.tc.tma) || en.kind == 4)) continue;
     static EncodeTiledFn encode = get_encode_tiled();
     cuuint64_t gdim[5], gstr[4];
     cuuint32_t box[5], est[5] = {1, 1, 1, 1, 1};
@@ -1328,7 +1503,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     }
     gdim[0] = (cuuint64_t)1 << 32;
     void* base = static_cast<char*>(d_ws) + L.node_off[en.opB];
-    const CUresult r = encode(&en.tc.tmapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstr, box, est,
+    const CUresult r = encode(en.kind == 4 ? &en.st.tmapB : &en.tc.tmapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstr, box, est,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(JT_ECUDA, "exec: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -1352,6 +1527,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     for (int i = 0; i < sv.nA; ++i) { sv.posA[i] = en.sliceA[i].first; sv.strA[i] = en.sliceA[i].second; }
     for (int i = 0; i < sv.nB; ++i) { sv.posB[i] = en.sliceB[i].first; sv.strB[i] = en.sliceB[i].second; }
     en.args.sv = sv;
+    en.st.sv = sv;
     en.tc.sv = sv;
     en.tcg.sv = sv;
   }
@@ -1440,6 +1616,15 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
     launch_pdl(pick_tcg(t.tmt), dim3((unsigned)en.grid_x), dim3(416), en.smem, ex->stream, ex->pdl, t);
+    ev_end(ex, en);
+    st.kernel_launches++;
+  } else if (en.kind == 4) {
+    StreamArgs& t = en.st;
+    t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]);
+    t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
+    ev_begin(ex);
+    launch_pdl(pick_stream(en.args.tm, en.args.tk), dim3((unsigned)en.grid_x), dim3(en.block), en.smem, ex->stream,
+               ex->pdl, t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else if (en.kind == 1) {
@@ -1578,6 +1763,11 @@ void exec_contract(jt_exec* ex, int64_t b, int64_t e, double* d_acc, double* h_v
         ex->stats.k4_timed_launches++;
         ex->stats.k4_timed_bytes += ex->ev_work[i].first;
         ex->stats.k4_timed_flop += ex->ev_work[i].second;
+      } else if (ex->ev_kind[i] == 4) {
+        ex->stats.k2s_time_ms += ms;
+        ex->stats.k2s_timed_launches++;
+        ex->stats.k2s_timed_bytes += ex->ev_work[i].first;
+        ex->stats.k2s_timed_flop += ex->ev_work[i].second;
       } else if (ex->ev_kind[i] >= 1) {
         if (ex->ev_kind[i] == 2) {
           ex->stats.k3g_time_ms += ms;

@@ -53,7 +53,8 @@ class ExecStats(ctypes.Structure):
                 ("k3_timed_flop", c_dbl), ("h2d_bytes", c_i64),
                 ("k4_time_ms", c_dbl), ("k4_timed_launches", c_i64), ("k4_timed_bytes", c_dbl),
                 ("k4_timed_flop", c_dbl), ("k3g_time_ms", c_dbl), ("k3g_timed_launches", c_i64),
-                ("k3g_timed_bytes", c_dbl), ("k3g_timed_flop", c_dbl)]
+                ("k3g_timed_bytes", c_dbl), ("k3g_timed_flop", c_dbl), ("k2s_time_ms", c_dbl),
+                ("k2s_timed_launches", c_i64), ("k2s_timed_bytes", c_dbl), ("k2s_timed_flop", c_dbl)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
