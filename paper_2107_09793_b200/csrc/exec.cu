@@ -52,7 +52,8 @@ struct ExecNode {
   TcgArgs tcg{};
   std::vector<int64_t> tcgA_m, tcgA_k, tcgB_oN, tcgA_oM;  // K3g host strides (emulator)
   std::vector<int64_t> tcB_n, tcB_k;  // K3: B strides of the 7 row bits and the K bits (emulator)
-  std::vector<std::pair<int64_t, int>> tma_dims;  // K3 TMA box dims: (stride in elements, log2 size)
+  std::vector<std::pair<int64_t, int>> tma_dims;    // TMA box dims of B's item: (stride in elements, log2 size)
+  std::vector<std::pair<int64_t, int>> tma_dims_a;  // K3g: TMA box dims of A's chunk
   int64_t v = -1;
   int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
   std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
@@ -96,12 +97,16 @@ using GettFn = void (*)(GettArgs);
 using TcFn = void (*)(TcArgs);
 
 using TcgFn = void (*)(TcgArgs);
-TcgFn pick_tcg(int tmt) {
-  switch (tmt) {
-    case 4: return gett_tcg_kernel<4>;
-    case 5: return gett_tcg_kernel<5>;
-    case 6: return gett_tcg_kernel<6>;
-    case 7: return gett_tcg_kernel<7>;
+TcgFn pick_tcg(int tmt, bool tma) {
+  switch (tmt * 2 + (tma ? 1 : 0)) {
+    case 8: return gett_tcg_kernel<4, false>;
+    case 9: return gett_tcg_kernel<4, true>;
+    case 10: return gett_tcg_kernel<5, false>;
+    case 11: return gett_tcg_kernel<5, true>;
+    case 12: return gett_tcg_kernel<6, false>;
+    case 13: return gett_tcg_kernel<6, true>;
+    case 14: return gett_tcg_kernel<7, false>;
+    case 15: return gett_tcg_kernel<7, true>;
   }
   fail(JT_EINTERNAL, "no tcg instance");
 }
@@ -170,9 +175,8 @@ void set_smem_attrs() {
     }
   for (int tkc = 2; tkc <= 4; ++tkc)
     for (int tma = 0; tma < 2; ++tma) set(reinterpret_cast<const void*>(pick_tc(tkc, tma != 0)), 222 * 1024);
-  const void* tcgs[4] = {reinterpret_cast<const void*>(gett_tcg_kernel<4>), reinterpret_cast<const void*>(gett_tcg_kernel<5>),
-                         reinterpret_cast<const void*>(gett_tcg_kernel<6>), reinterpret_cast<const void*>(gett_tcg_kernel<7>)};
-  for (const void* f : tcgs) set(f, 222 * 1024);
+  for (int tmt = 4; tmt <= 7; ++tmt)
+    for (int tma = 0; tma < 2; ++tma) set(reinterpret_cast<const void*>(pick_tcg(tmt, tma != 0)), 222 * 1024);
   for (int tm = 0; tm <= 3; ++tm)
     for (int kt = 1; kt <= 3; ++kt) set(reinterpret_cast<const void*>(pick_stream(tm, kt)), 200 * 1024);
   set(reinterpret_cast<const void*>(permute_kernel<float2, 0>), 200 * 1024);
@@ -199,6 +203,50 @@ int ilog2_exact(int d) {
   while ((1 << b) < d) ++b;
   if ((1 << b) != d) fail(JT_EUSAGE, "exec: the GPU path needs a power-of-two qudit dimension d");
   return b;
+}
+
+// TMA boxes of an item whose bits have the given strides: runs of consecutive strides, each at
+// most 8 bits (the 256-element box limit), in stride order.  The first 5 runs form the box;
+// further runs (at most 3 bits in all) are issued as separate boxes, box j at coordinate offset
+// xoff[j] (the item still lands packed in stride order).  Returns false when the item does not
+// hold the operand's stride-1 bit or needs more than 8 boxes.  rank[i] = the bit's position in
+// the packed landing (it lands at byte 8 << rank).
+bool tma_item_dims(const std::vector<int64_t>& strides, std::vector<std::pair<int64_t, int>>& dims,
+                   std::vector<int>& rank, int* nbox = nullptr, int64_t* xoff = nullptr) {
+  std::vector<std::pair<int64_t, int>> bits;
+  for (size_t i = 0; i < strides.size(); ++i) bits.push_back({strides[i], (int)i});
+  std::sort(bits.begin(), bits.end());
+  dims.clear();
+  for (auto& b : bits) {
+    if (!dims.empty() && b.first == dims.back().first << dims.back().second && dims.back().second < 8)
+      ++dims.back().second;
+    else
+      dims.push_back({b.first, 1});
+  }
+  rank.assign(strides.size(), 0);
+  for (size_t r = 0; r < bits.size(); ++r) rank[bits[r].second] = (int)r;
+  if (bits[0].first != 1) return false;
+  int extra = 0;
+  for (size_t i = 5; i < dims.size(); ++i) extra += dims[i].second;
+  if (extra > 3) return false;
+  if (nbox) {
+    *nbox = 1 << extra;
+    for (int j = 0; j < *nbox; ++j) {  // digits of j over the extra runs, lowest run first
+      int64_t o = 0;
+      int rem = j;
+      for (size_t i = 5; i < dims.size(); ++i) {
+        o += (int64_t)(rem & ((1 << dims[i].second) - 1)) * dims[i].first;
+        rem >>= dims[i].second;
+      }
+      xoff[j] = o;
+    }
+  }
+  return true;
+}
+
+bool tma_enabled() {
+  const char* e = std::getenv("JETB200_K3_TMA");
+  return !(e && e[0] == '0');
 }
 
 // K3 eligibility and descriptor (c64 only): small A fully inside the tile with 3..7 free
@@ -301,35 +349,24 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   }
   en.args.vecB = t.vecB;  // (reported by jt_exec_describe)
   // TMA item load (default; JETB200_K3_TMA=0 keeps the cp.async gathers): the item's 7 + tkc bits
-  // sorted by B stride are split into runs of consecutive strides, each at most 8 bits (256
-  // elements, the TMA box limit); <= 5 runs -> one 5-D box per item, packed in stride order, so
-  // bit b lands at byte 8 << rank(b).  The item base offset is the dim-0 coordinate (int32).
+  // sorted by B stride land packed, bit b at byte 8 << rank(b), by one box of <= 5 stride runs
+  // (plus up to 8 boxes for further runs, tma_item_dims); the item base offset is the dim-0
+  // coordinate (int32)
   {
-    const char* e = getenv("JETB200_K3_TMA");
-    const bool want = !(e && e[0] == '0');
-    std::vector<std::pair<int64_t, int>> bits;  // (stride, tag: row bit i = i, K bit j = 7 + j)
-    for (int i = 0; i < 7; ++i) bits.push_back({sb[tN[i]], i});
-    for (int j = 0; j < tkc; ++j) bits.push_back({sb[K[j].second], 7 + j});
-    std::sort(bits.begin(), bits.end());
+    std::vector<int64_t> item;
+    for (int i = 0; i < 7; ++i) item.push_back(sb[tN[i]]);
+    for (int j = 0; j < tkc; ++j) item.push_back(sb[K[j].second]);
     std::vector<std::pair<int64_t, int>> dims;
-    for (size_t r = 0; r < bits.size(); ++r) {
-      if (!dims.empty() && bits[r].first == dims.back().first << dims.back().second && dims.back().second < 8)
-        ++dims.back().second;
-      else
-        dims.push_back({bits[r].first, 1});
-    }
+    std::vector<int> rank;
     int64_t reach = 1 << 11;  // highest element offset an item can touch (+ box), int32 coordinate
     for (auto& x : vb.bits) reach += x.second;
     for (auto& x : en.sliceB) reach += x.second * 3;  // digits < d <= 4
-    t.tma = (want && dims.size() <= 5 && bits[0].first == 1 && reach < (int64_t(1) << 31)) ? 1 : 0;
+    t.tma = (tma_enabled() && tma_item_dims(item, dims, rank, &t.nbox, t.xoff) && reach < (int64_t(1) << 31)) ? 1 : 0;
     en.tma_dims.clear();
     if (t.tma) {
       en.tma_dims = dims;
-      for (size_t r = 0; r < bits.size(); ++r) {
-        const int tag = bits[r].second;
-        if (tag < 7) t.rofs_row[tag] = 8 << r;
-        else t.rofs_k[tag - 7] = 8 << r;
-      }
+      for (int i = 0; i < 7; ++i) t.rofs_row[i] = 8 << rank[i];
+      for (int j = 0; j < tkc; ++j) t.rofs_k[j] = 8 << rank[7 + j];
       t.vecB = 0;
       en.args.vecB = 0;
     }
@@ -357,32 +394,6 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
   for (auto b : oN) { out.bits.push_back({b, st}); st <<= 1; }
   return true;
-}
-
-// TMA box of an item whose bits have the given B strides: runs of consecutive strides, each at
-// most 8 bits (the 256-element box limit), in stride order.  Returns false when the item needs
-// more than 5 dims or does not hold B's stride-1 bit.  rank[i] = the bit's position in the
-// packed box (it lands at byte 8 << rank).
-bool tma_item_dims(const std::vector<int64_t>& strides, std::vector<std::pair<int64_t, int>>& dims,
-                   std::vector<int>& rank) {
-  std::vector<std::pair<int64_t, int>> bits;
-  for (size_t i = 0; i < strides.size(); ++i) bits.push_back({strides[i], (int)i});
-  std::sort(bits.begin(), bits.end());
-  dims.clear();
-  for (auto& b : bits) {
-    if (!dims.empty() && b.first == dims.back().first << dims.back().second && dims.back().second < 8)
-      ++dims.back().second;
-    else
-      dims.push_back({b.first, 1});
-  }
-  rank.assign(strides.size(), 0);
-  for (size_t r = 0; r < bits.size(); ++r) rank[bits[r].second] = (int)r;
-  return dims.size() <= 5 && bits[0].first == 1;
-}
-
-bool tma_enabled() {
-  const char* e = std::getenv("JETB200_K3_TMA");
-  return !(e && e[0] == '0');
 }
 
 // K2s eligibility and descriptor (c64): A tiny (<= 3 free bits, 1..3 contracted bits), B with
@@ -417,7 +428,9 @@ bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& 
   for (int j = 0; j < kt; ++j) item.push_back(K[j].first);
   std::vector<std::pair<int64_t, int>> dims;
   std::vector<int> rank;
-  if (!tma_item_dims(item, dims, rank)) return false;
+  int nbox = 1;
+  int64_t xoff[8];
+  if (!tma_item_dims(item, dims, rank, &nbox, xoff)) return false;
   int64_t reach = 1 << 11;
   for (auto& x : vb.bits) reach += x.second;
   for (auto& x : en.sliceB) reach += x.second * 3;
@@ -426,6 +439,8 @@ bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& 
   std::memset(&t, 0, sizeof(t));
   t.rbytes = 8 << (8 + kt);
   t.rstages = std::min(8, (200 * 1024 - 1024) / t.rbytes);
+  t.nbox = nbox;
+  for (int j = 0; j < nbox; ++j) t.xoff[j] = xoff[j];
   t.n_outer = (int)N.size() - 8;
   for (int j = 0; j < t.n_outer; ++j) t.o_sB[j] = N[8 + j].first;
   for (int i = 0; i < 8; ++i) t.rofs_n[i] = 8 << rank[i];
@@ -487,14 +502,41 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   std::sort(KA.begin(), KA.end());
   std::sort(K.begin(), K.end());
   std::vector<int64_t> kc, ko;
-  for (int i = 0; i < 2; ++i) kc.push_back(KA[i].second);
-  for (auto& k : K)
-    if ((int)kc.size() < 4 && std::find(kc.begin(), kc.end(), k.second) == kc.end()) kc.push_back(k.second);
-  for (auto& k : K)
-    if (std::find(kc.begin(), kc.end(), k.second) == kc.end()) ko.push_back(k.second);
   std::vector<int64_t> tN, oN, tM, oM;
   for (size_t i = 0; i < N.size(); ++i) (i < 7 ? tN : oN).push_back(N[i].second);
   for (size_t i = 0; i < M.size(); ++i) ((int)i < tmt ? tM : oM).push_back(M[i].second);
+  // candidate K chunks, in order of preference: (gather path) the 2 lowest-A-stride K bits then
+  // the lowest-B-stride ones; (TMA) the 4 lowest-B-stride, the 4 lowest-A-stride K bits.  With
+  // TMA on, the first candidate whose B and A chunks are both <= 5-run boxes wins.
+  auto chunk_from = [&](int na) {
+    std::vector<int64_t> c;
+    for (int i = 0; i < na; ++i) c.push_back(KA[i].second);
+    for (auto& k : K)
+      if ((int)c.size() < 4 && std::find(c.begin(), c.end(), k.second) == c.end()) c.push_back(k.second);
+    return c;
+  };
+  auto chunk_boxes = [&](const std::vector<int64_t>& c) {  // TMA boxes per item, 1 << 20 if none
+    std::vector<int64_t> ib, ia;
+    for (int i = 0; i < 7; ++i) ib.push_back(sb[tN[i]]);
+    for (int i = 0; i < tmt; ++i) ia.push_back(sa[tM[i]]);
+    for (auto b : c) { ib.push_back(sb[b]); ia.push_back(sa[b]); }
+    std::vector<std::pair<int64_t, int>> d;
+    std::vector<int> r;
+    int nb = 1, na = 1;
+    int64_t xo[8];
+    if (!tma_item_dims(ib, d, r, &nb, xo) || !tma_item_dims(ia, d, r, &na, xo)) return 1 << 20;
+    return nb + na;
+  };
+  kc = chunk_from(2);
+  if (tma_enabled()) {
+    int best = chunk_boxes(kc);
+    for (int na : {0, 4, 1, 3}) {
+      const int nb = chunk_boxes(chunk_from(na));
+      if (nb < best) { best = nb; kc = chunk_from(na); }
+    }
+  }
+  for (auto& k : K)
+    if (std::find(kc.begin(), kc.end(), k.second) == kc.end()) ko.push_back(k.second);
   if (oN.size() + oM.size() > 31 || ko.size() > 32 || oN.size() > 32 || oM.size() > 32) return false;
   // Y (expanded A, hi|lo planes) ring depth: the producers run ystages-1 items ahead of the MMAs
   // (2, 3 and 4 measured within 3% of each other on the C5 nodes: not the bound; 2 keeps the
@@ -548,6 +590,32 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   for (size_t j = 0; j < bb.size(); ++j) { t.gB[j] = bb[j].first; t.sB[j] = bb[j].second; }
   for (size_t j = 0; j < aa.size(); ++j) { t.gA[j] = aa[j].first; t.sA[j] = aa[j].second; }
   t.n_tiles = int64_t(1) << (t.n_oN + t.n_oM);
+  // TMA chunk loads (default; JETB200_K3_TMA=0 keeps the cp.async gathers): B chunk = 7 row + 4
+  // K bits, A chunk = tmt M + 4 K bits, each <= 5 stride runs holding the operand's stride-1 bit
+  {
+    std::vector<int64_t> ib, ia;
+    for (int i = 0; i < 7; ++i) ib.push_back(sb[tN[i]]);
+    for (int j = 0; j < 4; ++j) ib.push_back(sb[kc[j]]);
+    for (int i = 0; i < tmt; ++i) ia.push_back(sa[tM[i]]);
+    for (int j = 0; j < 4; ++j) ia.push_back(sa[kc[j]]);
+    std::vector<std::pair<int64_t, int>> db, da;
+    std::vector<int> rb_, ra_;
+    int64_t reachB = 1 << 11, reachA = 1 << 11;
+    for (auto& x : vb.bits) reachB += x.second;
+    for (auto& x : va.bits) reachA += x.second;
+    for (auto& x : en.sliceB) reachB += x.second * 3;
+    for (auto& x : en.sliceA) reachA += x.second * 3;
+    t.tma = (tma_enabled() && tma_item_dims(ib, db, rb_, &t.nboxB, t.xoffB) && tma_item_dims(ia, da, ra_, &t.nboxA, t.xoffA) &&
+             reachB < (int64_t(1) << 31) && reachA < (int64_t(1) << 31)) ? 1 : 0;
+    if (t.tma) {
+      en.tma_dims = db;
+      en.tma_dims_a = da;
+      for (int i = 0; i < 7; ++i) t.rofsB_n[i] = 8 << rb_[i];
+      for (int j = 0; j < 4; ++j) t.rofsB_k[j] = 8 << rb_[7 + j];
+      for (int i = 0; i < tmt; ++i) t.rofsA_m[i] = 8 << ra_[i];
+      for (int j = 0; j < 4; ++j) t.rofsA_k[j] = 8 << ra_[tmt + j];
+    }
+  }
   // host copies for the emulator
   en.tcB_n.clear(); en.tcB_k.clear(); en.tcgA_m.clear(); en.tcgA_k.clear(); en.tcgB_oN.clear(); en.tcgA_oM.clear();
   for (int i = 0; i < 7; ++i) en.tcB_n.push_back(sb[tN[i]]);
@@ -558,7 +626,7 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   for (auto b : oM) en.tcgA_oM.push_back(sa[b]);
   en.kind = 2;
   en.smem = (size_t)(ybytes + (int64_t)rstages * (rb_b + rb_a) + 1024);
-  en.block = 416;
+  en.block = t.tma ? 448 : 416;
   en.n_out = t.n_tiles << (7 + tmt);
   en.grid_x = t.n_tiles;
   en.args.splits = 1;
@@ -1271,6 +1339,42 @@ void emulate_tcg(const TcgArgs& p, const ExecNode& en, char* ws, const std::vect
     for (size_t j = 0; j < st.size(); ++j) if ((v >> j) & 1) o += st[j];
     return o;
   };
+  if (p.tma) {
+    // TMA landings: the packed boxes of every (tile, chunk) read back through the rofs tables
+    auto box_of = [](int64_t base, const std::vector<std::pair<int64_t, int>>& dims, size_t n) {
+      std::vector<int64_t> b(n);
+      for (size_t e = 0; e < n; ++e) {
+        int64_t o = base, rem = (int64_t)e;
+        for (auto& dm : dims) {
+          o += (rem & ((int64_t(1) << dm.second) - 1)) * dm.first;
+          rem >>= dm.second;
+        }
+        b[e] = o;
+      }
+      return b;
+    };
+    const std::vector<int64_t> kcB(en.tcB_k.begin(), en.tcB_k.begin() + 4), koB(en.tcB_k.begin() + 4, en.tcB_k.end());
+    const std::vector<int64_t> kcA(en.tcgA_k.begin(), en.tcgA_k.begin() + 4), koA(en.tcgA_k.begin() + 4, en.tcgA_k.end());
+    for (int64_t t = 0; t < p.n_tiles; ++t)
+      for (int64_t c = 0; c < (int64_t(1) << p.lg_kc); ++c) {
+        const int64_t bo = bits(t, en.tcgB_oN) + bits(c, koB), ao = bits(t >> p.n_oN, en.tcgA_oM) + bits(c, koA);
+        const auto bb = box_of(bo, en.tma_dims, 2048), ab = box_of(ao, en.tma_dims_a, (size_t)MT * 16);
+        for (int k = 0; k < 16; ++k) {
+          int32_t kb = 0, ka = 0;
+          for (int j = 0; j < 4; ++j) if ((k >> j) & 1) { kb += p.rofsB_k[j]; ka += p.rofsA_k[j]; }
+          for (int n = 0; n < 128; ++n) {
+            int32_t r = kb;
+            for (int i = 0; i < 7; ++i) if ((n >> i) & 1) r += p.rofsB_n[i];
+            if (bb[r / 8] != bo + bits(n, en.tcB_n) + bits(k, kcB)) fail(JT_EINTERNAL, "emulate: K3g B landing mismatch");
+          }
+          for (int m = 0; m < MT; ++m) {
+            int32_t r = ka;
+            for (int i = 0; i < p.tmt; ++i) if ((m >> i) & 1) r += p.rofsA_m[i];
+            if (ab[r / 8] != ao + bits(m, en.tcgA_m) + bits(k, kcA)) fail(JT_EINTERNAL, "emulate: K3g A landing mismatch");
+          }
+        }
+      }
+  }
   for (int64_t t = 0; t < p.n_tiles; ++t) {
     const int64_t bo = bits(t, en.tcgB_oN), ao = bits(t >> p.n_oN, en.tcgA_oM);
     for (int n = 0; n < 128; ++n)
@@ -1412,7 +1516,7 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
       for (size_t q = 0; q < en.tcB_n.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcB_n[q]);
       std::fprintf(f, "], \"Bk\": [");
       for (size_t q = 0; q < en.tcB_k.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcB_k[q]);
-      std::fprintf(f, "], \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : 0);
+      std::fprintf(f, "], \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : en.tcg.tma);
     }
     std::fprintf(f, "}");
   }
@@ -1489,12 +1593,10 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   }
   // K3 TMA maps: B's item box at its workspace address (dim 0 declared 2^32 long: the item
   // base offset is the dim-0 coordinate; see plan_tc)
-  for (ExecNode& en : L.order) {
-    if (!((en.kind == 1 && en.tc.tma) || en.kind == 4)) continue;
+  auto encode_item = [&](CUtensorMap* map, const std::vector<std::pair<int64_t, int>>& dm, int64_t op) {
     static EncodeTiledFn encode = get_encode_tiled();
     cuuint64_t gdim[5], gstr[4];
     cuuint32_t box[5], est[5] = {1, 1, 1, 1, 1};
-    const auto& dm = en.tma_dims;
     for (int i = 0; i < 5; ++i) {
       const bool on = i < (int)dm.size();
       box[i] = on ? (cuuint32_t)1 << dm[i].second : 1;
@@ -1502,11 +1604,19 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
       if (i > 0) gstr[i - 1] = (cuuint64_t)(on ? dm[i].first : dm.back().first << dm.back().second) * 8;
     }
     gdim[0] = (cuuint64_t)1 << 32;
-    void* base = static_cast<char*>(d_ws) + L.node_off[en.opB];
-    const CUresult r = encode(en.kind == 4 ? &en.st.tmapB : &en.tc.tmapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstr, box, est,
+    void* base = static_cast<char*>(d_ws) + L.node_off[op];
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstr, box, est,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(JT_ECUDA, "exec: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  };
+  for (ExecNode& en : L.order) {
+    if (en.kind == 1 && en.tc.tma) encode_item(&en.tc.tmapB, en.tma_dims, en.opB);
+    if (en.kind == 4) encode_item(&en.st.tmapB, en.tma_dims, en.opB);
+    if (en.kind == 2 && en.tcg.tma) {
+      encode_item(&en.tcg.tmapB, en.tma_dims, en.opB);
+      encode_item(&en.tcg.tmapA, en.tma_dims_a, en.opA);
+    }
   }
   auto* ex = new jt_exec();
   ex->L = std::move(L);
@@ -1615,7 +1725,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
-    launch_pdl(pick_tcg(t.tmt), dim3((unsigned)en.grid_x), dim3(416), en.smem, ex->stream, ex->pdl, t);
+    launch_pdl(pick_tcg(t.tmt, t.tma != 0), dim3((unsigned)en.grid_x), dim3(en.block), en.smem, ex->stream, ex->pdl, t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else if (en.kind == 4) {

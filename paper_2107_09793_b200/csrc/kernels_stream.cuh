@@ -29,6 +29,8 @@ struct StreamArgs {
   int32_t n_outer, rstages, rbytes;
   int64_t o_sB[kMaxOuter];    // B stride of outer (tile-index) bit j
   int32_t rofs_n[8], rofs_k[3];  // landing byte offset of tile column bit i / K bit j
+  int32_t nbox;               // TMA boxes per tile (runs beyond the 5th), box j at xoff[j]
+  int64_t xoff[8];
   int64_t aM[3], aK[3];       // A strides of its M / K bits
   SliceView sv;
 };
@@ -78,7 +80,9 @@ __global__ void __launch_bounds__(288, 1) stream_gett_kernel(const __grid_consta
       if (lane == 0) {
         if (it >= RS) tc::mbar_wait(&empty[st], ph ^ 1);
         tc::mbar_expect_tx(&full[st], (uint32_t)p.rbytes);
-        tc::tma_load5(R + st * p.rbytes, &p.tmapB, (int)(boff + tb), &full[st]);
+        const int bb = p.rbytes / p.nbox;
+        for (int j = 0; j < p.nbox; ++j)
+          tc::tma_load5(R + st * p.rbytes + j * bb, &p.tmapB, (int)(boff + tb + p.xoff[j]), &full[st]);
       }
       if (++st == RS) { st = 0; ph ^= 1; }
     }

@@ -56,6 +56,8 @@ struct TcArgs {
   int32_t vecB;                                // 1: chunk-tile bit 0 is a K bit at global stride 1
                                                //    -> gather k-pairs as 16-B copies
   int32_t tma;                                 // 1: items arrive by TMA (gett_tc_kernel<TKC, true>)
+  int32_t nbox;                                // TMA boxes per item (runs beyond the 5th)
+  int64_t xoff[8];                             //   ... box j at dim-0 coordinate offset xoff[j]
   int32_t rofs_row[7], rofs_k[5];              // TMA landing: byte offset of row bit i / chunk K bit j
                                                //   (the box is packed in B-stride order: 8 << rank)
   SliceView sv;
@@ -366,7 +368,9 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
       if (lane == 0) {
         if (it >= RS) tc::mbar_wait(&rempty[wst], wph ^ 1);  // all producer warps released it
         tc::mbar_expect_tx(&rfull[wst], (uint32_t)p.rbytes);
-        tc::tma_load5(R + wst * p.rbytes, &p.tmapB, (int)(cbase + kc_off[cc]), &rfull[wst]);
+        const int bb = p.rbytes / p.nbox;
+        for (int j = 0; j < p.nbox; ++j)
+          tc::tma_load5(R + wst * p.rbytes + j * bb, &p.tmapB, (int)(cbase + kc_off[cc] + p.xoff[j]), &rfull[wst]);
       }
       if (++wst == RS) { wst = 0; wph ^= 1; }
       if (++cc == p.n_kc) {

@@ -17,6 +17,8 @@
 namespace jt {
 
 struct TcgArgs {
+  CUtensorMap tmapB, tmapA;  // TMA maps of the B chunk (7 row + 4 K bits) and the A chunk (tmt M + 4
+                             // K bits), as TcArgs::tmapB; tma = 1
   const float2* A;
   const float2* B;
   float2* C;                // layout [7 n bits][tmt m bits][outer N bits][outer M bits]
@@ -33,6 +35,10 @@ struct TcgArgs {
   int64_t k_B[32], k_A[32]; // chunk-index bit strides in B / in A
   int64_t gB[12], gA[12];   // chunk-tile bits (stride order): global strides
   int32_t sB[12], sA[12];   //   ... and raw byte offsets (XOR-combinable)
+  int32_t tma;              // 1: chunks arrive by TMA (gett_tcg_kernel<TMT, true>)
+  int32_t nboxB, nboxA;     // TMA boxes per chunk (runs beyond the 5th), box j at xoffB/A[j]
+  int64_t xoffB[8], xoffA[8];
+  int32_t rofsB_n[7], rofsB_k[4], rofsA_m[7], rofsA_k[4];  // TMA landing byte offsets per bit
   SliceView sv;
 };
 
@@ -59,8 +65,10 @@ __device__ __forceinline__ int64_t raster(int64_t t, const TcgArgs& p) {
 }
 }  // namespace tcg
 
-template <int TMT>
-__global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant__ TcgArgs p) {
+// TMA = true: warp 13 issues the B and A chunk boxes of each item into the raw rings (rfull /
+// rempty mbarriers); the producers only split X and expand Y (no gathers, no named barrier).
+template <int TMT, bool TMA>
+__global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __grid_constant__ TcgArgs p) {
   constexpr int MT = 1 << TMT;       // complex columns of the tile
   constexpr int NP = 2 * MT;         // MMA N
   constexpr int PERB = 2048 / 256;   // B chunk elements per producer thread
@@ -71,7 +79,7 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
   __shared__ int64_t tgb[2][64], tga[2][64];
   __shared__ int32_t tsb[2][64], tsa[2][64];
   __shared__ int64_t dkB[32], dkA[32];  // chunk c -> c+1 offset steps, by trailing ones of c
-  __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[4], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[4], tfull[2], tempty[2], rfull[8], rempty[8];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
@@ -114,7 +122,16 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 128);
     }
+    if (TMA)
+      for (int i = 0; i < p.rstages; ++i) {
+        tc::mbar_init(&rfull[i], 1);
+        tc::mbar_init(&rempty[i], 8);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (TMA && warp == 13 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmapB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmapA) : "memory");
   }
   tc::fence_before();
   __syncthreads();
@@ -127,7 +144,141 @@ __global__ void __launch_bounds__(416, 1) gett_tcg_kernel(const __grid_constant_
   const int64_t items = my_tiles << p.lg_kc;
   const int64_t kc_mask = ((int64_t)1 << p.lg_kc) - 1;
 
-  if (warp >= 4 && warp < 12) {
+  if (TMA && warp >= 4 && warp < 12) {
+    // ===================== producers (TMA-fed) =====================
+    const int ptid = tid - 128;
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int row = quarter * 32 + lane;
+    const int RS = p.rstages;
+    int32_t rB = 0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) rB += ((row >> i) & 1) ? p.rofsB_n[i] : 0;
+    int32_t kB[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = half * 8 + q;
+      int32_t o = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o += ((k >> j) & 1) ? p.rofsB_k[j] : 0;
+      kB[q] = o;
+    }
+    int32_t a0[PAIRS], a1[PAIRS];
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) {
+      const int u = (ptid + q * 256) & (MT * 8 - 1);
+      const int m = u >> 3, kp = u & 7;
+      int32_t o = 0;
+#pragma unroll
+      for (int i = 0; i < TMT; ++i) o += ((m >> i) & 1) ? p.rofsA_m[i] : 0;
+#pragma unroll
+      for (int j = 1; j < 4; ++j) o += ((kp >> (j - 1)) & 1) ? p.rofsA_k[j] : 0;
+      a0[q] = o;
+      a1[q] = o + p.rofsA_k[0];
+    }
+    int rst = 0, ys = 0;
+    uint32_t rph = 0, yph = 0;
+    for (int64_t it = 0; it < items; ++it) {
+      const int xs = (int)(it & 3);
+      tc::mbar_wait(&rfull[rst], rph);
+      tc::mbar_wait(&xempty[xs], (uint32_t)(((it >> 2) & 1) ^ 1));
+      tc::mbar_wait(&yempty[ys], yph ^ 1u);
+      tc::fence_after();
+      // ---- X: this thread's row, half of the chunk -> hi/lo TF32 in TMEM
+      {
+        const unsigned char* raw = RB + rst * p.rbytes_b + rB;
+        float hi[16], lo[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float2 v = *reinterpret_cast<const float2*>(raw + kB[q]);
+          hi[2 * q] = tc::tf32_rna(v.x);
+          lo[2 * q] = tc::tf32_lo(v.x, hi[2 * q]);
+          hi[2 * q + 1] = tc::tf32_rna(v.y);
+          lo[2 * q + 1] = tc::tf32_lo(v.y, hi[2 * q + 1]);
+        }
+        const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t col = xcol0 + (uint32_t)(xs * 2 * KPC + half * 16);
+        tc::tmem_st<16>(lane_addr + col, hi);
+        tc::tmem_st<16>(lane_addr + col + KPC, lo);
+      }
+      // ---- Y: expand the A chunk into [[Re,-Im],[Im,Re]] hi/lo (SWIZZLE_128B, K-major)
+      {
+        const unsigned char* raw = RA + rst * p.rbytes_a;
+        unsigned char* yhi = Y + ys * 2 * NP * 128;
+        unsigned char* ylo = yhi + NP * 128;
+#pragma unroll
+        for (int q = 0; q < PAIRS; ++q) {
+          const int u = ptid + q * 256;
+          if (u < MT * 8) {
+            const int m = u >> 3, kp = u & 7;
+            const float2 e0 = *reinterpret_cast<const float2*>(raw + a0[q]);
+            const float2 e1 = *reinterpret_cast<const float2*>(raw + a1[q]);
+            const float hx = tc::tf32_rna(e0.x), hy = tc::tf32_rna(e0.y), hz = tc::tf32_rna(e1.x), hw = tc::tf32_rna(e1.y);
+            const float lx = tc::tf32_lo(e0.x, hx), ly = tc::tf32_lo(e0.y, hy), lz = tc::tf32_lo(e1.x, hz),
+                        lw = tc::tf32_lo(e1.y, hw);
+            const int ra0 = 2 * m, ra1 = 2 * m + 1;
+            const int b0 = (ra0 & 7) * 128 + (ra0 >> 3) * 1024 + ((kp ^ (ra0 & 7)) << 4);
+            const int b1 = (ra1 & 7) * 128 + (ra1 >> 3) * 1024 + ((kp ^ (ra1 & 7)) << 4);
+            *reinterpret_cast<float4*>(yhi + b0) = make_float4(hx, -hy, hz, -hw);
+            *reinterpret_cast<float4*>(ylo + b0) = make_float4(lx, -ly, lz, -lw);
+            *reinterpret_cast<float4*>(yhi + b1) = make_float4(hy, hx, hw, hz);
+            *reinterpret_cast<float4*>(ylo + b1) = make_float4(ly, lx, lw, lz);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&rempty[rst]);
+      if (++rst == RS) { rst = 0; rph ^= 1; }
+      tc::fence_proxy_async();
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&full[xs]);
+      if (++ys == p.ystages) { ys = 0; yph ^= 1u; }
+    }
+  } else if (TMA && warp == 13) {
+    // ===================== TMA issuer =====================
+    const int64_t boff = slice_off(p.sv, false), aoff = slice_off(p.sv, true);
+    const int64_t ob = lane < p.n_oN ? p.o_B[lane] : 0, oa = lane < p.n_oM ? p.o_A[lane] : 0;
+    const int RS = p.rstages;
+    int64_t ct = 0, cc = 0, tileB = 0, tileA = 0, kBo = 0, kAo = 0;
+    auto tile_bases = [&]() {
+      const int64_t t = tcg::raster((int64_t)blockIdx.x + ct * gridDim.x, p);
+      int64_t b = ((t >> lane) & 1) ? ob : 0;
+      int64_t a = (((t >> p.n_oN) >> lane) & 1) ? oa : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+      }
+      tileB = boff + b;
+      tileA = aoff + a;
+    };
+    tile_bases();
+    int wst = 0;
+    uint32_t wph = 0;
+    for (int64_t it = 0; it < items; ++it) {
+      if (lane == 0) {
+        if (it >= RS) tc::mbar_wait(&rempty[wst], wph ^ 1);
+        tc::mbar_expect_tx(&rfull[wst], (uint32_t)(p.rbytes_b + p.rbytes_a));
+        const int bb = p.rbytes_b / p.nboxB, ba = p.rbytes_a / p.nboxA;
+        for (int j = 0; j < p.nboxB; ++j)
+          tc::tma_load5(RB + wst * p.rbytes_b + j * bb, &p.tmapB, (int)(tileB + kBo + p.xoffB[j]), &rfull[wst]);
+        for (int j = 0; j < p.nboxA; ++j)
+          tc::tma_load5(RA + wst * p.rbytes_a + j * ba, &p.tmapA, (int)(tileA + kAo + p.xoffA[j]), &rfull[wst]);
+      }
+      if (++wst == RS) { wst = 0; wph ^= 1; }
+      if (cc == kc_mask) {
+        cc = 0;
+        kBo = kAo = 0;
+        ++ct;
+        tile_bases();
+      } else {
+        const int tz = __ffsll(~cc) - 1;
+        kBo += dkB[tz];
+        kAo += dkA[tz];
+        ++cc;
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
     // ===================== producers =====================
     const int ptid = tid - 128;
     const int quarter = warp & 3, half = (warp - 4) >> 2;

@@ -27,8 +27,12 @@ def perms(n, rng):
 def main():
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))["hbm_gbs"]
+    import bench
+
     rng = np.random.default_rng(1)
     out = []
+    clk = bench.ClockSampler(torch.cuda.current_device())
+    clk.start()
     for dt, tdt in (("c64", torch.complex64), ("c128", torch.complex128)):
         for n in (26, 28):
             src = torch.randn(1 << n, dtype=tdt, device="cuda")
@@ -48,7 +52,8 @@ def main():
                 gbs = 2 * (1 << n) * src.element_size() / (ms / 1e3) / 1e9
                 out.append({"dtype": dt, "n_bits": n, "perm": name, "ms": ms, "GBps": gbs, "frac_of_measured_hbm": gbs / peak})
                 print(json.dumps(out[-1]), flush=True)
-    print(json.dumps({"summary": "K1 permute", "peak_gbs_measured": peak,
+    clocks = clk.stop()
+    print(json.dumps({"summary": "K1 permute", "peak_gbs_measured": peak, "clocks": clocks,
                       "min_frac": min(o["frac_of_measured_hbm"] for o in out if o["perm"] != "identity"),
                       "median_frac": float(np.median([o["frac_of_measured_hbm"] for o in out]))}))
 

@@ -21,7 +21,7 @@ print(g.index(t))
 PY
 )
 echo "top ${KREGEX} index $SKIP" > gpurun_out/prof_${CFG}_${TAG}.txt
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"${KREGEX}" -s $SKIP -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"${KREGEX}" -s $SKIP -c 1 \
   -o gpurun_out/prof_${CFG}_${TAG} -f $BENCH >> gpurun_out/prof_${CFG}_${TAG}.txt 2>&1
 python scripts/ncu_summary.py gpurun_out/prof_${CFG}_${TAG}.ncu-rep >> gpurun_out/prof_${CFG}_${TAG}.txt 2>&1
 python scripts/launches.py gpurun_out/launches_${CFG}_${TAG}.csv > gpurun_out/launches_${CFG}_${TAG}_summary.txt 2>&1
