@@ -52,8 +52,6 @@ struct ExecNode {
   TcgArgs tcg{};
   std::vector<int64_t> tcgA_m, tcgA_k, tcgB_oN, tcgA_oM;  // K3g host strides (emulator)
   std::vector<int64_t> tcB_n, tcB_k;  // K3: B strides of the 7 row bits and the K bits (emulator)
-  std::vector<std::pair<int64_t, int>> tma_dims;    // TMA box dims of B's item: (stride in elements, log2 size)
-  std::vector<std::pair<int64_t, int>> tma_dims_a;  // K3g: TMA box dims of A's chunk
   int64_t v = -1;
   int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
   std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
@@ -186,18 +184,6 @@ void set_smem_attrs() {
   done[dev] = 1;
 }
 
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
-EncodeTiledFn get_encode_tiled() {
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q{};
-  JT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-  if (!fn || q != cudaDriverEntryPointSuccess) fail(JT_ECUDA, "exec: cuTensorMapEncodeTiled unavailable");
-  return reinterpret_cast<EncodeTiledFn>(fn);
-}
-
 int ilog2_exact(int d) {
   int b = 0;
   while ((1 << b) < d) ++b;
@@ -205,42 +191,35 @@ int ilog2_exact(int d) {
   return b;
 }
 
-// TMA boxes of an item whose bits have the given strides: runs of consecutive strides, each at
-// most 8 bits (the 256-element box limit), in stride order.  The first 5 runs form the box;
-// further runs (at most 3 bits in all) are issued as separate boxes, box j at coordinate offset
-// xoff[j] (the item still lands packed in stride order).  Returns false when the item does not
-// hold the operand's stride-1 bit or needs more than 8 boxes.  rank[i] = the bit's position in
-// the packed landing (it lands at byte 8 << rank).
-bool tma_item_dims(const std::vector<int64_t>& strides, std::vector<std::pair<int64_t, int>>& dims,
-                   std::vector<int>& rank, int* nbox = nullptr, int64_t* xoff = nullptr) {
+// Bulk-copy (TMA engine, cp.async.bulk) landing of an item whose address bits have the given
+// element strides: the bits sorted by stride land packed, bit b at byte 8 << rank(b).  The run of
+// consecutive strides that starts at stride 1 is contiguous in global memory and moves as one
+// copy; the item's remaining h bits (h <= 5) enumerate 2^h copies, copy j at element offset
+// xoff[j] (the digits of j over those bits, in rank order) landing at j * copy bytes.  (A tensor
+// map cannot take the item base as a coordinate: a dim-0 extent overlapping the higher strides
+// faults with an illegal instruction on B200, profiles/r02_tma_probe.txt.)  Returns false when
+// the item does not hold the operand's stride-1 bit or needs more than 32 copies.
+bool tma_item_dims(const std::vector<int64_t>& strides, int* ncopy, int* copy_log2, int64_t* xoff,
+                   std::vector<int>& rank) {
   std::vector<std::pair<int64_t, int>> bits;
   for (size_t i = 0; i < strides.size(); ++i) bits.push_back({strides[i], (int)i});
   std::sort(bits.begin(), bits.end());
-  dims.clear();
-  for (auto& b : bits) {
-    if (!dims.empty() && b.first == dims.back().first << dims.back().second && dims.back().second < 8)
-      ++dims.back().second;
-    else
-      dims.push_back({b.first, 1});
-  }
   rank.assign(strides.size(), 0);
   for (size_t r = 0; r < bits.size(); ++r) rank[bits[r].second] = (int)r;
   if (bits[0].first != 1) return false;
-  int extra = 0;
-  for (size_t i = 5; i < dims.size(); ++i) extra += dims[i].second;
-  if (extra > 3) return false;
-  if (nbox) {
-    *nbox = 1 << extra;
-    for (int j = 0; j < *nbox; ++j) {  // digits of j over the extra runs, lowest run first
+  size_t low = 1;
+  while (low < bits.size() && bits[low].first == bits[low - 1].first * 2) ++low;
+  const int h = (int)(bits.size() - low);
+  if (h > 5) return false;
+  *ncopy = 1 << h;
+  *copy_log2 = (int)low;
+  if (xoff)
+    for (int j = 0; j < *ncopy; ++j) {
       int64_t o = 0;
-      int rem = j;
-      for (size_t i = 5; i < dims.size(); ++i) {
-        o += (int64_t)(rem & ((1 << dims[i].second) - 1)) * dims[i].first;
-        rem >>= dims[i].second;
-      }
+      for (int i = 0; i < h; ++i)
+        if ((j >> i) & 1) o += bits[low + i].first;
       xoff[j] = o;
     }
-  }
   return true;
 }
 
@@ -348,23 +327,21 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
     t.vecB = (tb[0].first == 1 && tb[0].second == 8 && e && e[0] == '1') ? 1 : 0;
   }
   en.args.vecB = t.vecB;  // (reported by jt_exec_describe)
-  // TMA item load (default; JETB200_K3_TMA=0 keeps the cp.async gathers): the item's 7 + tkc bits
-  // sorted by B stride land packed, bit b at byte 8 << rank(b), by one box of <= 5 stride runs
-  // (plus up to 8 boxes for further runs, tma_item_dims); the item base offset is the dim-0
-  // coordinate (int32)
+  // TMA-engine item load (default; JETB200_K3_TMA=0 keeps the cp.async gathers): the item's
+  // 7 + tkc bits land packed in B-stride order, bit b at byte 8 << rank(b), moved as bulk copies
+  // of the item's stride-1 run (tma_item_dims)
   {
     std::vector<int64_t> item;
     for (int i = 0; i < 7; ++i) item.push_back(sb[tN[i]]);
     for (int j = 0; j < tkc; ++j) item.push_back(sb[K[j].second]);
-    std::vector<std::pair<int64_t, int>> dims;
     std::vector<int> rank;
-    int64_t reach = 1 << 11;  // highest element offset an item can touch (+ box), int32 coordinate
-    for (auto& x : vb.bits) reach += x.second;
-    for (auto& x : en.sliceB) reach += x.second * 3;  // digits < d <= 4
-    t.tma = (tma_enabled() && tma_item_dims(item, dims, rank, &t.nbox, t.xoff) && reach < (int64_t(1) << 31)) ? 1 : 0;
-    en.tma_dims.clear();
+    int ncopy = 0, clog = 0;
+    bool even = true;  // 16-B aligned copies: a sliced leaf's digit strides must be even
+    for (auto& x : en.sliceB) even &= (x.second % 2) == 0;
+    t.tma = (tma_enabled() && even && tma_item_dims(item, &ncopy, &clog, t.xoff, rank)) ? 1 : 0;
     if (t.tma) {
-      en.tma_dims = dims;
+      t.ncopy = ncopy;
+      t.copy_bytes = 8 << clog;
       for (int i = 0; i < 7; ++i) t.rofs_row[i] = 8 << rank[i];
       for (int j = 0; j < tkc; ++j) t.rofs_k[j] = 8 << rank[7 + j];
       t.vecB = 0;
@@ -426,21 +403,19 @@ bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& 
   std::vector<int64_t> item;
   for (int i = 0; i < 8; ++i) item.push_back(N[i].first);
   for (int j = 0; j < kt; ++j) item.push_back(K[j].first);
-  std::vector<std::pair<int64_t, int>> dims;
   std::vector<int> rank;
-  int nbox = 1;
-  int64_t xoff[8];
-  if (!tma_item_dims(item, dims, rank, &nbox, xoff)) return false;
-  int64_t reach = 1 << 11;
-  for (auto& x : vb.bits) reach += x.second;
-  for (auto& x : en.sliceB) reach += x.second * 3;
-  if (reach >= (int64_t(1) << 31)) return false;
+  int ncopy = 0, clog = 0;
+  int64_t xoff[32];
+  for (auto& x : en.sliceB)
+    if (x.second % 2) return false;
+  if (!tma_item_dims(item, &ncopy, &clog, xoff, rank)) return false;
   StreamArgs& t = en.st;
   std::memset(&t, 0, sizeof(t));
   t.rbytes = 8 << (8 + kt);
   t.rstages = std::min(8, (200 * 1024 - 1024) / t.rbytes);
-  t.nbox = nbox;
-  for (int j = 0; j < nbox; ++j) t.xoff[j] = xoff[j];
+  t.ncopy = ncopy;
+  t.copy_bytes = 8 << clog;
+  for (int j = 0; j < ncopy; ++j) t.xoff[j] = xoff[j];
   t.n_outer = (int)N.size() - 8;
   for (int j = 0; j < t.n_outer; ++j) t.o_sB[j] = N[8 + j].first;
   for (int i = 0; i < 8; ++i) t.rofs_n[i] = 8 << rank[i];
@@ -448,7 +423,6 @@ bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& 
   for (int i = 0; i < tm; ++i) t.aM[i] = M[i].first;
   for (int j = 0; j < kt; ++j) t.aK[j] = sa[K[j].second];
   t.n_tiles = int64_t(1) << t.n_outer;
-  en.tma_dims = dims;
   en.stN.clear();
   en.stK.clear();
   for (int i = 0; i < 8; ++i) en.stN.push_back(N[i].first);
@@ -520,11 +494,9 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
     for (int i = 0; i < 7; ++i) ib.push_back(sb[tN[i]]);
     for (int i = 0; i < tmt; ++i) ia.push_back(sa[tM[i]]);
     for (auto b : c) { ib.push_back(sb[b]); ia.push_back(sa[b]); }
-    std::vector<std::pair<int64_t, int>> d;
     std::vector<int> r;
-    int nb = 1, na = 1;
-    int64_t xo[8];
-    if (!tma_item_dims(ib, d, r, &nb, xo) || !tma_item_dims(ia, d, r, &na, xo)) return 1 << 20;
+    int nb = 0, na = 0, cl = 0;
+    if (!tma_item_dims(ib, &nb, &cl, nullptr, r) || !tma_item_dims(ia, &na, &cl, nullptr, r)) return 1 << 20;
     return nb + na;
   };
   kc = chunk_from(2);
@@ -598,18 +570,18 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
     for (int j = 0; j < 4; ++j) ib.push_back(sb[kc[j]]);
     for (int i = 0; i < tmt; ++i) ia.push_back(sa[tM[i]]);
     for (int j = 0; j < 4; ++j) ia.push_back(sa[kc[j]]);
-    std::vector<std::pair<int64_t, int>> db, da;
     std::vector<int> rb_, ra_;
-    int64_t reachB = 1 << 11, reachA = 1 << 11;
-    for (auto& x : vb.bits) reachB += x.second;
-    for (auto& x : va.bits) reachA += x.second;
-    for (auto& x : en.sliceB) reachB += x.second * 3;
-    for (auto& x : en.sliceA) reachA += x.second * 3;
-    t.tma = (tma_enabled() && tma_item_dims(ib, db, rb_, &t.nboxB, t.xoffB) && tma_item_dims(ia, da, ra_, &t.nboxA, t.xoffA) &&
-             reachB < (int64_t(1) << 31) && reachA < (int64_t(1) << 31)) ? 1 : 0;
+    int nb = 0, na = 0, cb = 0, ca = 0;
+    bool even = true;
+    for (auto& x : en.sliceB) even &= (x.second % 2) == 0;
+    for (auto& x : en.sliceA) even &= (x.second % 2) == 0;
+    t.tma = (tma_enabled() && even && tma_item_dims(ib, &nb, &cb, t.xoffB, rb_) &&
+             tma_item_dims(ia, &na, &ca, t.xoffA, ra_)) ? 1 : 0;
     if (t.tma) {
-      en.tma_dims = db;
-      en.tma_dims_a = da;
+      t.ncopyB = nb;
+      t.copyB_bytes = 8 << cb;
+      t.ncopyA = na;
+      t.copyA_bytes = 8 << ca;
       for (int i = 0; i < 7; ++i) t.rofsB_n[i] = 8 << rb_[i];
       for (int j = 0; j < 4; ++j) t.rofsB_k[j] = 8 << rb_[7 + j];
       for (int i = 0; i < tmt; ++i) t.rofsA_m[i] = 8 << ra_[i];
@@ -1215,6 +1187,16 @@ void emulate_gett(const GettArgs& p, char* ws, const ExecNode& en, const std::ve
   }
 }
 
+// The packed landing of a bulk-copied item: element e sits at global base + xoff[e >> log2 copy
+// elements] + (e & (copy elements - 1)).
+std::vector<int64_t> landing(int64_t base, int ncopy, int copy_bytes, const int64_t* xoff, size_t n) {
+  std::vector<int64_t> b(n);
+  const int64_t ce = copy_bytes / 8;
+  if ((int64_t)ncopy * ce != (int64_t)n) fail(JT_EINTERNAL, "emulate: bulk copies do not tile the item");
+  for (size_t e = 0; e < n; ++e) b[e] = base + xoff[(int64_t)e / ce] + (int64_t)e % ce;
+  return b;
+}
+
 // K2s: the TMA landing of every tile (read back through rofs_n / rofs_k) and the output layout
 // [M][8 tile bits][outer], with the kernel's FP32 complex arithmetic order
 void emulate_stream(const StreamArgs& p, const ExecNode& en, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
@@ -1230,18 +1212,10 @@ void emulate_stream(const StreamArgs& p, const ExecNode& en, char* ws, const std
       for (int i = 0; i < kt; ++i) if ((k >> i) & 1) ao += p.aK[i];
       a[(size_t)m * nk + k] = A[ao];
     }
-  std::vector<int64_t> box((size_t)256 << kt);
   for (int64_t t = 0; t < p.n_tiles; ++t) {
     int64_t base = 0;
     for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
-    for (size_t e = 0; e < box.size(); ++e) {
-      int64_t o = base, rem = (int64_t)e;
-      for (auto& dm : en.tma_dims) {
-        o += (rem & ((int64_t(1) << dm.second) - 1)) * dm.first;
-        rem >>= dm.second;
-      }
-      box[e] = o;
-    }
+    const std::vector<int64_t> box = landing(base, p.ncopy, p.copy_bytes, p.xoff, (size_t)256 << kt);
     for (int n = 0; n < 256; ++n) {
       int64_t noff = 0, nb = base;
       for (int i = 0; i < 8; ++i) if ((n >> i) & 1) { noff += p.rofs_n[i]; nb += en.stN[i]; }
@@ -1281,23 +1255,14 @@ void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector
       a[(size_t)m * nk + k] = A[ao];
     }
   if (p.tma) {
-    // the TMA landing: the packed box of every item (dims = en.tma_dims, base = the dim-0
-    // coordinate) read back through rofs_row / rofs_k must be the item's B elements
-    std::vector<int64_t> box;
+    // the TMA-engine landing of every item, read back through rofs_row / rofs_k, must be the
+    // item's B elements
     for (int64_t t = 0; t < p.n_tiles; ++t)
       for (int c = 0; c < p.n_kc; ++c) {
         int64_t base = 0;
         for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
         for (int j = 0; j < p.K - p.tkc; ++j) if ((c >> j) & 1) base += p.o_kB[j];
-        box.assign((size_t)128 << p.tkc, 0);
-        for (size_t e = 0; e < box.size(); ++e) {
-          int64_t o = base, rem = (int64_t)e;
-          for (auto& dm : en.tma_dims) {
-            o += (rem & ((int64_t(1) << dm.second) - 1)) * dm.first;
-            rem >>= dm.second;
-          }
-          box[e] = o;
-        }
+        const std::vector<int64_t> box = landing(base, p.ncopy, p.copy_bytes, p.xoff, (size_t)128 << p.tkc);
         for (int n = 0; n < 128; ++n)
           for (int k = 0; k < (1 << p.tkc); ++k) {
             int64_t want = base, ro = 0;
@@ -1340,25 +1305,14 @@ void emulate_tcg(const TcgArgs& p, const ExecNode& en, char* ws, const std::vect
     return o;
   };
   if (p.tma) {
-    // TMA landings: the packed boxes of every (tile, chunk) read back through the rofs tables
-    auto box_of = [](int64_t base, const std::vector<std::pair<int64_t, int>>& dims, size_t n) {
-      std::vector<int64_t> b(n);
-      for (size_t e = 0; e < n; ++e) {
-        int64_t o = base, rem = (int64_t)e;
-        for (auto& dm : dims) {
-          o += (rem & ((int64_t(1) << dm.second) - 1)) * dm.first;
-          rem >>= dm.second;
-        }
-        b[e] = o;
-      }
-      return b;
-    };
+    // TMA-engine landings of every (tile, chunk), read back through the rofs tables
     const std::vector<int64_t> kcB(en.tcB_k.begin(), en.tcB_k.begin() + 4), koB(en.tcB_k.begin() + 4, en.tcB_k.end());
     const std::vector<int64_t> kcA(en.tcgA_k.begin(), en.tcgA_k.begin() + 4), koA(en.tcgA_k.begin() + 4, en.tcgA_k.end());
     for (int64_t t = 0; t < p.n_tiles; ++t)
       for (int64_t c = 0; c < (int64_t(1) << p.lg_kc); ++c) {
         const int64_t bo = bits(t, en.tcgB_oN) + bits(c, koB), ao = bits(t >> p.n_oN, en.tcgA_oM) + bits(c, koA);
-        const auto bb = box_of(bo, en.tma_dims, 2048), ab = box_of(ao, en.tma_dims_a, (size_t)MT * 16);
+        const auto bb = landing(bo, p.ncopyB, p.copyB_bytes, p.xoffB, 2048);
+        const auto ab = landing(ao, p.ncopyA, p.copyA_bytes, p.xoffA, (size_t)MT * 16);
         for (int k = 0; k < 16; ++k) {
           int32_t kb = 0, ka = 0;
           for (int j = 0; j < 4; ++j) if ((k >> j) & 1) { kb += p.rofsB_k[j]; ka += p.rofsA_k[j]; }
@@ -1516,6 +1470,10 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
       for (size_t q = 0; q < en.tcB_n.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcB_n[q]);
       std::fprintf(f, "], \"Bk\": [");
       for (size_t q = 0; q < en.tcB_k.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcB_k[q]);
+      std::fprintf(f, "], \"Am\": [");
+      for (size_t q = 0; q < en.tcgA_m.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcgA_m[q]);
+      std::fprintf(f, "], \"Ak\": [");
+      for (size_t q = 0; q < en.tcgA_k.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcgA_k[q]);
       std::fprintf(f, "], \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : en.tcg.tma);
     }
     std::fprintf(f, "}");
@@ -1593,31 +1551,6 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   }
   // K3 TMA maps: B's item box at its workspace address (dim 0 declared 2^32 long: the item
   // base offset is the dim-0 coordinate; see plan_tc)
-  auto encode_item = [&](CUtensorMap* map, const std::vector<std::pair<int64_t, int>>& dm, int64_t op) {
-    static EncodeTiledFn encode = get_encode_tiled();
-    cuuint64_t gdim[5], gstr[4];
-    cuuint32_t box[5], est[5] = {1, 1, 1, 1, 1};
-    for (int i = 0; i < 5; ++i) {
-      const bool on = i < (int)dm.size();
-      box[i] = on ? (cuuint32_t)1 << dm[i].second : 1;
-      gdim[i] = box[i];
-      if (i > 0) gstr[i - 1] = (cuuint64_t)(on ? dm[i].first : dm.back().first << dm.back().second) * 8;
-    }
-    gdim[0] = (cuuint64_t)1 << 32;
-    void* base = static_cast<char*>(d_ws) + L.node_off[op];
-    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstr, box, est,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(JT_ECUDA, "exec: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  };
-  for (ExecNode& en : L.order) {
-    if (en.kind == 1 && en.tc.tma) encode_item(&en.tc.tmapB, en.tma_dims, en.opB);
-    if (en.kind == 4) encode_item(&en.st.tmapB, en.tma_dims, en.opB);
-    if (en.kind == 2 && en.tcg.tma) {
-      encode_item(&en.tcg.tmapB, en.tma_dims, en.opB);
-      encode_item(&en.tcg.tmapA, en.tma_dims_a, en.opA);
-    }
-  }
   auto* ex = new jt_exec();
   ex->L = std::move(L);
   ex->cur_stats = &ex->stats;
@@ -1731,6 +1664,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
   } else if (en.kind == 4) {
     StreamArgs& t = en.st;
     t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]);
+    t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
     launch_pdl(pick_stream(en.args.tm, en.args.tk), dim3((unsigned)en.grid_x), dim3(en.block), en.smem, ex->stream,

@@ -5,9 +5,10 @@
 // Sycamore m=14 path.  Arithmetic intensity is ~2-3 FLOP/B, so the node is a pure HBM stream:
 // every B byte is read once and every C byte written once (algorithmic bytes 8(|A|+|B|+|C|)).
 //
-//   tile  = 256 columns n (B's 8 lowest-stride free bits) x all 2^KT k: one TMA box of
-//           2^(8+KT) elements (<= 16 KB), packed in B-stride order (bit b at byte 8 << rank b)
-//   warp 8     lane 0 issues the boxes into a ring of RS stages (full/empty mbarriers)
+//   tile  = 256 columns n (B's 8 lowest-stride free bits) x all 2^KT k: 2^(8+KT) elements
+//           (<= 16 KB) moved by TMA-engine bulk copies of its contiguous runs, landing packed in
+//           B-stride order (bit b at byte 8 << rank b)
+//   warp 8     issues the copies (one per lane) into a ring of RS stages (full/empty mbarriers)
 //   warps 0-7  one thread per column n: read its 2^KT values, multiply by A (registers),
 //              write its 2^TM outputs as one contiguous run: C is laid out
 //              [M bits][tile n bits][outer bits], so a warp stores 32 x 2^TM x 8 B contiguous
@@ -22,15 +23,15 @@
 namespace jt {
 
 struct StreamArgs {
-  CUtensorMap tmapB;          // B tile box (see TcArgs::tmapB); dim-0 coordinate = tile base offset
   const float2* A;
+  const float2* B;
   float2* C;
   int64_t n_tiles;
   int32_t n_outer, rstages, rbytes;
   int64_t o_sB[kMaxOuter];    // B stride of outer (tile-index) bit j
   int32_t rofs_n[8], rofs_k[3];  // landing byte offset of tile column bit i / K bit j
-  int32_t nbox;               // TMA boxes per tile (runs beyond the 5th), box j at xoff[j]
-  int64_t xoff[8];
+  int32_t ncopy, copy_bytes;  // bulk copies per tile (its stride-1 run each), copy j at xoff[j]
+  int64_t xoff[32];
   int64_t aM[3], aK[3];       // A strides of its M / K bits
   SliceView sv;
 };
@@ -50,7 +51,6 @@ __global__ void __launch_bounds__(288, 1) stream_gett_kernel(const __grid_consta
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmapB) : "memory");
   pdl_wait();
   pdl_launch_dependents();
   if (tid < NM * NK) {
@@ -80,10 +80,11 @@ __global__ void __launch_bounds__(288, 1) stream_gett_kernel(const __grid_consta
       if (lane == 0) {
         if (it >= RS) tc::mbar_wait(&empty[st], ph ^ 1);
         tc::mbar_expect_tx(&full[st], (uint32_t)p.rbytes);
-        const int bb = p.rbytes / p.nbox;
-        for (int j = 0; j < p.nbox; ++j)
-          tc::tma_load5(R + st * p.rbytes + j * bb, &p.tmapB, (int)(boff + tb + p.xoff[j]), &full[st]);
       }
+      __syncwarp();
+      if (lane < p.ncopy)
+        tc::bulk_g2s(R + st * p.rbytes + lane * p.copy_bytes, p.B + (boff + tb + p.xoff[lane]), (uint32_t)p.copy_bytes,
+                     &full[st]);
       if (++st == RS) { st = 0; ph ^= 1; }
     }
   } else {

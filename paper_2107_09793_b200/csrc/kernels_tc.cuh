@@ -16,8 +16,8 @@
 // SWIZZLE_NONE canonical layout: core matrices of 8 rows x 16 B, LBO 128 B, SBO (K'/4)*128 B).
 // X (the streamed big operand) is split into hi/lo by producer warps and written to tensor
 // memory, from which the MMA reads it (the "TS" form).  See gett_tc_kernel below for the
-// warp roles; B items reach shared memory either by one TMA box per item (cp.async.bulk.tensor,
-// the default when the item's address bits form <= 5 runs) or by per-element cp.async gathers.
+// warp roles; B items reach shared memory either on the TMA engine (cp.async.bulk copies of the
+// item's contiguous runs, the default) or by per-element cp.async gathers.
 #pragma once
 
 #include <cuda.h>
@@ -31,8 +31,6 @@ namespace jt {
 constexpr int kTcMaxTile = 12;  // 7 row bits + up to 5 K bits per chunk
 
 struct TcArgs {
-  CUtensorMap tmapB;  // TMA map of B's item (<= 5 dims = the item bits' stride runs; dim 0 is
-                      // declared 2^32 long so the item base offset is its coordinate); tma = 1
   const float2* A;  // small operand (all bits in the tile)
   const float2* B;  // big operand
   float2* C;        // output, layout [7 row (n) bits][tm bits][outer bits]
@@ -55,9 +53,9 @@ struct TcArgs {
   int8_t swz_row[3];                           // row bits (lowest B stride first) that drive the raw-row swizzle
   int32_t vecB;                                // 1: chunk-tile bit 0 is a K bit at global stride 1
                                                //    -> gather k-pairs as 16-B copies
-  int32_t tma;                                 // 1: items arrive by TMA (gett_tc_kernel<TKC, true>)
-  int32_t nbox;                                // TMA boxes per item (runs beyond the 5th)
-  int64_t xoff[8];                             //   ... box j at dim-0 coordinate offset xoff[j]
+  int32_t tma;                                 // 1: items arrive by TMA bulk copies (gett_tc_kernel<TKC, true>)
+  int32_t ncopy, copy_bytes;                   // bulk copies per item (the stride-1 run each) and their size
+  int64_t xoff[32];                            //   ... copy j reads at item base + xoff[j], lands at j * copy_bytes
   int32_t rofs_row[7], rofs_k[5];              // TMA landing: byte offset of row bit i / chunk K bit j
                                                //   (the box is packed in B-stride order: 8 << rank)
   SliceView sv;
@@ -173,13 +171,13 @@ __device__ __forceinline__ float tf32_lo(float x, float hi) { return x - hi; }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// One TMA box (5-D tiled map; unused dims have size 1) into shared memory, completing on `bar`.
-__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, int c0, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %3, %3, "
-      "%3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(0), "r"(smem_u32(bar))
-      : "memory");
+// One bulk copy global -> shared on the TMA engine (16-B aligned, size a multiple of 16 B),
+// completing its bytes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 }  // namespace tc
@@ -198,7 +196,8 @@ __device__ __forceinline__ int tc_off(int r, int kk, int sbo, int swz) {
 //              hi/lo TF32 and writes both into a TMEM X stage with tcgen05.st
 //   warp 12    MMA issuer: tcgen05.mma kind::tf32 with A = X from TMEM ([a_tmem], the "TS" form)
 //              and B = Y (expanded small operand, resident in shared memory), 3xTF32
-//   warp 13    (TMA = true) TMA issuer: one cp.async.bulk.tensor box per item into the raw ring;
+//   warp 13    (TMA = true) TMA issuer: each item's contiguous runs as cp.async.bulk copies (one
+//              per lane) into the raw ring, landing packed in B-stride order;
 //              the producers then only read their row from shared memory, split and store
 // Barriers: xfull/xempty per TMEM X stage, tfull/tempty per accumulator, rfull/rempty per raw
 // stage (TMA = true; without TMA the producers sync on a named barrier per item instead).
@@ -260,7 +259,6 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (TMA && warp == 13 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmapB) : "memory");
   pdl_wait();  // the operands are written by the previous kernels of the sequence
   pdl_launch_dependents();
   // ---- Y = expanded small operand (hi/lo) for every K chunk: row = 2m+s, col = 2k+t
@@ -368,10 +366,11 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
       if (lane == 0) {
         if (it >= RS) tc::mbar_wait(&rempty[wst], wph ^ 1);  // all producer warps released it
         tc::mbar_expect_tx(&rfull[wst], (uint32_t)p.rbytes);
-        const int bb = p.rbytes / p.nbox;
-        for (int j = 0; j < p.nbox; ++j)
-          tc::tma_load5(R + wst * p.rbytes + j * bb, &p.tmapB, (int)(cbase + kc_off[cc] + p.xoff[j]), &rfull[wst]);
       }
+      __syncwarp();
+      if (lane < p.ncopy)
+        tc::bulk_g2s(R + wst * p.rbytes + lane * p.copy_bytes, p.B + (cbase + kc_off[cc] + p.xoff[lane]),
+                     (uint32_t)p.copy_bytes, &rfull[wst]);
       if (++wst == RS) { wst = 0; wph ^= 1; }
       if (++cc == p.n_kc) {
         cc = 0;

@@ -17,8 +17,6 @@
 namespace jt {
 
 struct TcgArgs {
-  CUtensorMap tmapB, tmapA;  // TMA maps of the B chunk (7 row + 4 K bits) and the A chunk (tmt M + 4
-                             // K bits), as TcArgs::tmapB; tma = 1
   const float2* A;
   const float2* B;
   float2* C;                // layout [7 n bits][tmt m bits][outer N bits][outer M bits]
@@ -36,8 +34,8 @@ struct TcgArgs {
   int64_t gB[12], gA[12];   // chunk-tile bits (stride order): global strides
   int32_t sB[12], sA[12];   //   ... and raw byte offsets (XOR-combinable)
   int32_t tma;              // 1: chunks arrive by TMA (gett_tcg_kernel<TMT, true>)
-  int32_t nboxB, nboxA;     // TMA boxes per chunk (runs beyond the 5th), box j at xoffB/A[j]
-  int64_t xoffB[8], xoffA[8];
+  int32_t ncopyB, copyB_bytes, ncopyA, copyA_bytes;  // bulk copies per chunk (TcArgs::ncopy)
+  int64_t xoffB[32], xoffA[32];
   int32_t rofsB_n[7], rofsB_k[4], rofsA_m[7], rofsA_k[4];  // TMA landing byte offsets per bit
   SliceView sv;
 };
@@ -65,7 +63,8 @@ __device__ __forceinline__ int64_t raster(int64_t t, const TcgArgs& p) {
 }
 }  // namespace tcg
 
-// TMA = true: warp 13 issues the B and A chunk boxes of each item into the raw rings (rfull /
+// TMA = true: warp 13 issues the B and A chunks of each item as TMA-engine bulk copies of their
+// contiguous runs (one per lane) into the raw rings (rfull /
 // rempty mbarriers); the producers only split X and expand Y (no gathers, no named barrier).
 template <int TMT, bool TMA>
 __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __grid_constant__ TcgArgs p) {
@@ -128,10 +127,6 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
         tc::mbar_init(&rempty[i], 8);
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (TMA && warp == 13 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmapB) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmapA) : "memory");
   }
   tc::fence_before();
   __syncthreads();
@@ -259,12 +254,14 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
       if (lane == 0) {
         if (it >= RS) tc::mbar_wait(&rempty[wst], wph ^ 1);
         tc::mbar_expect_tx(&rfull[wst], (uint32_t)(p.rbytes_b + p.rbytes_a));
-        const int bb = p.rbytes_b / p.nboxB, ba = p.rbytes_a / p.nboxA;
-        for (int j = 0; j < p.nboxB; ++j)
-          tc::tma_load5(RB + wst * p.rbytes_b + j * bb, &p.tmapB, (int)(tileB + kBo + p.xoffB[j]), &rfull[wst]);
-        for (int j = 0; j < p.nboxA; ++j)
-          tc::tma_load5(RA + wst * p.rbytes_a + j * ba, &p.tmapA, (int)(tileA + kAo + p.xoffA[j]), &rfull[wst]);
       }
+      __syncwarp();
+      if (lane < p.ncopyB)
+        tc::bulk_g2s(RB + wst * p.rbytes_b + lane * p.copyB_bytes, p.B + (tileB + kBo + p.xoffB[lane]),
+                     (uint32_t)p.copyB_bytes, &rfull[wst]);
+      if (lane < p.ncopyA)
+        tc::bulk_g2s(RA + wst * p.rbytes_a + lane * p.copyA_bytes, p.A + (tileA + kAo + p.xoffA[lane]),
+                     (uint32_t)p.copyA_bytes, &rfull[wst]);
       if (++wst == RS) { wst = 0; wph ^= 1; }
       if (cc == kc_mask) {
         cc = 0;

@@ -4,8 +4,6 @@
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/tma_probe scripts/tma_probe.cu > gpurun_out/tma_probe_build.log 2>&1
-timeout 300 /tmp/tma_probe > gpurun_out/tma_probe.txt 2>&1; echo "rc=$?" >> gpurun_out/tma_probe.txt
 timeout 1500 python -m pytest tests/test_gpu_benched.py tests/test_gpu_parity.py -q -rA -k "benched or k2s or k3g or c2_full or c3 or reuse or graph or golden or partition" > gpurun_out/pytest_tma.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_tma.log
 timeout 600 python scripts/node_bench.py C3 14 > gpurun_out/nodes_C3_tma.txt 2>&1
 JETB200_K3_TMA=0 timeout 600 python scripts/node_bench.py C3 14 > gpurun_out/nodes_C3_gather.txt 2>&1
