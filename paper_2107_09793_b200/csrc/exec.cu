@@ -211,6 +211,12 @@ bool tma_item_dims(const std::vector<int64_t>& strides, int* ncopy, int* copy_lo
   while (low < bits.size() && bits[low].first == bits[low - 1].first * 2) ++low;
   const int h = (int)(bits.size() - low);
   if (h > 5) return false;
+  // copies below JETB200_TMA_MINCOPY bytes (default 4 KB) lose to the cp.async gathers: measured
+  // on the C3 K3 nodes, 16 x 1 KB copies per item ran at 57-73% of HBM vs 70-91% gathered, while
+  // 2-4 copies of 4-8 KB reached 100-103% (profiles/r02_nodes_C3_tma.txt)
+  int64_t min_copy = 4096;
+  if (const char* e = std::getenv("JETB200_TMA_MINCOPY")) min_copy = std::max<int64_t>(16, atoll(e));
+  if ((int64_t(8) << low) < min_copy) return false;
   *ncopy = 1 << h;
   *copy_log2 = (int)low;
   if (xoff)
@@ -379,9 +385,10 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
 // (default 2: tm = 3 goes to K3) sets the largest tm taken.
 bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& out) {
   if (esize != 8 || !tma_enabled()) return false;
-  {
+  {  // opt-in (JETB200_K2S=1): measured 2.0 TB/s on the C3 skinny nodes vs 3.4-5.0 TB/s for K2
+     // (shared-memory bank conflicts of the column-per-thread reads, profiles/r02_nodes_C3_tma.txt)
     const char* e = std::getenv("JETB200_K2S");
-    if (e && e[0] == '0') return false;
+    if (!(e && e[0] == '1')) return false;
   }
   int maxtm = 2;
   if (const char* e = std::getenv("JETB200_K2S_MAXTM")) maxtm = std::max(0, std::min(3, atoi(e)));
@@ -1474,8 +1481,16 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
       for (size_t q = 0; q < en.tcgA_m.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcgA_m[q]);
       std::fprintf(f, "], \"Ak\": [");
       for (size_t q = 0; q < en.tcgA_k.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.tcgA_k[q]);
-      std::fprintf(f, "], \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : en.tcg.tma);
+      std::fprintf(f, "], \"ncopy\": %d, \"copy_bytes\": %d, \"rofs_row\": [%d, %d, %d, %d, %d, %d, %d]", en.kind == 1 ? en.tc.ncopy : en.tcg.ncopyB,
+                   en.kind == 1 ? en.tc.copy_bytes : en.tcg.copyB_bytes, en.tc.rofs_row[0], en.tc.rofs_row[1],
+                   en.tc.rofs_row[2], en.tc.rofs_row[3], en.tc.rofs_row[4], en.tc.rofs_row[5], en.tc.rofs_row[6]);
+      std::fprintf(f, ", \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : en.tcg.tma);
     }
+    if (en.kind == 4)
+      std::fprintf(f, ", \"ncopy\": %d, \"copy_bytes\": %d, \"rofs_n\": [%d, %d, %d, %d, %d, %d, %d, %d], \"rofs_k\": [%d, %d, %d]",
+                   en.st.ncopy, en.st.copy_bytes, en.st.rofs_n[0], en.st.rofs_n[1], en.st.rofs_n[2], en.st.rofs_n[3],
+                   en.st.rofs_n[4], en.st.rofs_n[5], en.st.rofs_n[6], en.st.rofs_n[7], en.st.rofs_k[0], en.st.rofs_k[1],
+                   en.st.rofs_k[2]);
     std::fprintf(f, "}");
   }
   std::fprintf(f, "]}\n");

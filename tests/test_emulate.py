@@ -100,13 +100,14 @@ def test_describe_exec_layout(jet):
             assert n["n_out"] == 2 ** (n["tm"] + n["tn"] + n["n_outer"])
 
 
-def test_emulated_k3_matches_oracle_c2_slices(jet):
+def test_emulated_k3_matches_oracle_c2_slices(jet, monkeypatch):
+    monkeypatch.setenv("JETB200_TMA_MINCOPY", "16")   # every K3 item on the TMA engine: emulate its landing
     circ, bits = workload("C2")
     net = jet.Network.from_circuit(circ, bits)
     plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6, bytes_weight=5.0)
     nodes = plan.describe_exec("c64")["nodes"]
     assert sum(n["kind"] for n in nodes) > 0
-    assert any(n["kind"] == 1 and n["tma"] for n in nodes)   # the TMA landing is emulated too
+    assert any(n["kind"] == 1 and n["tma"] for n in nodes)
     ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[5]))
     v = jet.debug_emulate_host(plan, 5, 6, "c64")
     assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4
@@ -115,6 +116,7 @@ def test_emulated_k3_matches_oracle_c2_slices(jet):
 def test_emulated_k3g_matches_oracle_c2_slice(jet, monkeypatch):
     """K3g (both operands streamed) descriptors: force the K3-eligible C2 nodes onto K3g."""
     monkeypatch.setenv("JETB200_TCG_FORCE", "1")
+    monkeypatch.setenv("JETB200_TMA_MINCOPY", "16")
     circ, bits = workload("C2")
     net = jet.Network.from_circuit(circ, bits)
     plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6, bytes_weight=5.0)
@@ -150,13 +152,15 @@ def test_emulated_k4_descriptors_match_oracle_gbs(jet, dim, width, d):
     assert n_k4 > 0, "no node was routed to K4"
 
 
-def test_emulated_k2s_and_k3_tma_match_oracle_grid():
+def test_emulated_k2s_and_k3_tma_match_oracle_grid(monkeypatch):
     """K2s (TMA-fed streaming GETT) and K3-TMA descriptors on a 4x5 m=10 grid circuit with 4
     sliced labels: the emulated TMA landings (every tile) and the emulated contraction match the
     oracle's s_sigma on every slice (c64 arithmetic, 1e-4)."""
     import paper_2107_09793_b200.jet as jet
     from circuits import grid_rqc, random_bitstring
 
+    monkeypatch.setenv("JETB200_K2S", "1")
+    monkeypatch.setenv("JETB200_TMA_MINCOPY", "16")
     circ = grid_rqc(4, 5, 10, 1)
     bits = random_bitstring(20, 2, 1)
     net = jet.Network.from_circuit(circ, bits)

@@ -60,9 +60,15 @@ def record(name, data):
     """Error evidence for profiles/ (the achieved errors, not just pass/fail)."""
     if os.path.isdir(OUT):
         p = os.path.join(OUT, "parity_errors.json")
-        d = json.load(open(p)) if os.path.exists(p) else {}
+        try:
+            d = json.load(open(p))
+        except (OSError, ValueError):
+            d = {}
         d[name] = data
-        json.dump(d, open(p, "w"), indent=1)
+        tmp = p + ".tmp"
+        with open(tmp, "w") as f:
+            json.dump(d, f, indent=1, default=lambda x: x.item() if hasattr(x, "item") else str(x))
+        os.replace(tmp, p)
 
 
 def exec_on_stream(jet, plan, dtype):
@@ -382,7 +388,9 @@ def test_k2s_and_k3_tma_grid_parity(jet, monkeypatch):
     plan = jet.Plan.greedy(net, seed=1, trials=32, n_sliced=4)
     ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
     out = {}
-    for tag, env in (("default", {}), ("no_k2s", {"JETB200_K2S": "0"}), ("no_tma", {"JETB200_K3_TMA": "0"})):
+    monkeypatch.setenv("JETB200_TMA_MINCOPY", "16")   # every item on the TMA engine, however small
+    for tag, env in (("default", {"JETB200_K2S": "1"}), ("no_k2s", {"JETB200_K2S": "0"}),
+                     ("no_tma", {"JETB200_K3_TMA": "0"})):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         p = jet.Plan.create(net, plan.ssa_path, plan.sliced_labels)

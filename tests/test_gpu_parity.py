@@ -399,15 +399,18 @@ def test_c3_fsim_identity_closed_form_full_amplitude(jet):
     assert rel(amp, want) < 1e-4
 
 
-@pytest.mark.parametrize("tmt_max", ["6", "7"])
-def test_k3g_streamed_operands_parity(jet, c2_plan, monkeypatch, tmt_max):
+@pytest.mark.parametrize("tmt_max,mincopy", [("6", "4096"), ("7", "4096"), ("7", "16")])
+def test_k3g_streamed_operands_parity(jet, c2_plan, monkeypatch, tmt_max, mincopy):
     """K3g (tcgen05 with both operands streamed, K in 16-complex chunks): force the C2 nodes
     K3 would take onto K3g and compare 8 slices with the oracle (tile columns up to 64 complex
     with two accumulators, or up to 128 with one)."""
     circ, bits, net, plan = c2_plan
     monkeypatch.setenv("JETB200_TCG_FORCE", "1")
     monkeypatch.setenv("JETB200_TCG_TMT", tmt_max)
+    monkeypatch.setenv("JETB200_TMA_MINCOPY", mincopy)   # 16: every chunk on the TMA engine
     nodes = plan.describe_exec("c64")["nodes"]
+    if mincopy == "16":
+        assert any(n["kind"] == 2 and n["tma"] for n in nodes)
     assert [n["kind"] for n in nodes].count(2) >= 10
     assert max(n["tc_tm"] for n in nodes if n["kind"] == 2) == int(tmt_max)
     idx = list(range(0, 64, 8))
