@@ -262,18 +262,28 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   // rows are zero and the padded accumulator columns are never stored)
   const int Kpc = 2 << tkc, Np = std::max(16, 2 << tm);
   const int yplane = Np * Kpc * 4;
-  // TMEM: accumulators (2 when they fit beside >= 2 X stages) + X stages of 2*Kpc columns
+  // TMEM: accumulators (2 when they fit beside >= 2 X stages) + X stages of 2*Kpc columns.
+  // CTAs per SM: TMEM (512 columns) is per SM and the block scheduler does not see it, so the
+  // shared-memory footprint enforces the CTA count the TMEM budget allows -- two CTAs of <= 256
+  // columns each, or one CTA whose shared memory is padded past half of the SM.  (Two CTAs of
+  // one grid sized for one per SM co-resided through shared memory, the second blocking in
+  // tcgen05.alloc until the first finished: +2.2 s per C3 amplitude under PDL.)
   int acc_bufs = (2 * Np + 2 * 2 * Kpc <= 512) ? 2 : 1;
-  int xstages = std::min(4, (512 - acc_bufs * Np) / (2 * Kpc));
+  int ctas = 2;  // JETB200_K3_CTAS: 1 forces one CTA per SM (deeper raw ring)
+  if (const char* e = std::getenv("JETB200_K3_CTAS")) ctas = std::max(1, std::min(2, atoi(e)));
+  const bool two = ctas == 2 && acc_bufs * Np + 2 * 2 * Kpc <= 256;
+  const int cols_budget = two ? 256 : 512;
+  int xstages = std::min(4, (cols_budget - acc_bufs * Np) / (2 * Kpc));
   if (xstages < 2) return false;
   const int rbytes = 128 * (8 << tkc);
   const int64_t ybytes = 2LL * n_kc * yplane;
-  const int64_t budget = 220 * 1024 - 1024 - ybytes;
-  int rs_cap = 6;  // JETB200_K3_RS: sweep knob for the raw ring depth (TMA path: up to 8)
-  if (const char* e = std::getenv("JETB200_K3_RS")) rs_cap = std::max(2, std::min(8, atoi(e)));
+  const int64_t budget = (two ? 112 : 220) * 1024 - 1024 - ybytes;
+  int rs_cap = two ? 6 : 12;  // JETB200_K3_RS: sweep knob for the raw ring depth (<= 16)
+  if (const char* e = std::getenv("JETB200_K3_RS")) rs_cap = std::max(2, std::min(16, atoi(e)));
   const int rstages = (int)std::min<int64_t>(rs_cap, budget / rbytes);
   if (rstages < 2) return false;
-  const int64_t smem = ybytes + (int64_t)rstages * rbytes + 1024;
+  int64_t smem = ybytes + (int64_t)rstages * rbytes + 1024;
+  if (!two) smem = std::max<int64_t>(smem, 116 * 1024);
   std::sort(M.begin(), M.end());
   std::sort(N.begin(), N.end());
   std::sort(K.begin(), K.end());
@@ -301,6 +311,7 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t cols = 32;
   while ((int)cols < acc_bufs * Np + xstages * 2 * Kpc) cols <<= 1;
+  if (!two) cols = 512;
   t.tmem_cols = cols;
   // chunk-tile bits in B-stride order with their byte offsets in the raw landing stage:
   // row n, complex k at n*rb + ((k>>1) ^ (n & (chunks-1)))*16 + (k&1)*8 (XOR-combinable)

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
   __shared__ int64_t kc_off[16];  // B offset of K chunk c (n_kc <= 16)
-  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2], rfull[8], rempty[8];
+  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2], rfull[16], rempty[16];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < 16) {

@@ -91,7 +91,7 @@ def test_describe_exec_layout(jet):
     d = plan.describe_exec("c64")
     assert d["total_bytes"] == plan.workspace_bytes("c64")
     for n in d["nodes"]:
-        assert n["block"] % 32 == 0 and n["block"] <= {1: 448, 4: 288}.get(n["kind"], 256)
+        assert n["block"] % 32 == 0 and n["block"] <= {1: 448, 2: 448, 4: 288}.get(n["kind"], 256)
         if n["kind"] in (1, 2):   # K3 / K3g: 128-row MMA tiles
             assert n["n_out"] == 2 ** (7 + n["tc_tm"] + n["tc_outer"])
             assert 3 <= n["tc_tm"] <= 7 and 2 <= n["tc_tk"] and n["smem"] <= 220 * 1024
