@@ -211,10 +211,11 @@ bool tma_item_dims(const std::vector<int64_t>& strides, int* ncopy, int* copy_lo
   while (low < bits.size() && bits[low].first == bits[low - 1].first * 2) ++low;
   const int h = (int)(bits.size() - low);
   if (h > 5) return false;
-  // copies below JETB200_TMA_MINCOPY bytes (default 4 KB) lose to the cp.async gathers: measured
+  // copies below JETB200_TMA_MINCOPY bytes (default 2 KB) lose to the cp.async gathers: measured
   // on the C3 K3 nodes, 16 x 1 KB copies per item ran at 57-73% of HBM vs 70-91% gathered, while
-  // 2-4 copies of 4-8 KB reached 100-103% (profiles/r02_nodes_C3_tma.txt)
-  int64_t min_copy = 4096;
+  // 2-4 copies of 4-8 KB reached 100-103% (profiles/r02_nodes_C3_tma.txt); in the amplitude step
+  // a 2-KB floor beat a 4-KB one (9.17 vs 9.27 s, profiles/r02_variants_pdl.txt)
+  int64_t min_copy = 2048;
   if (const char* e = std::getenv("JETB200_TMA_MINCOPY")) min_copy = std::max<int64_t>(16, atoll(e));
   if ((int64_t(8) << low) < min_copy) return false;
   *ncopy = 1 << h;
@@ -1583,8 +1584,12 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
   {
     const char* e = std::getenv("JETB200_GRAPHS");
     ex->use_graphs = !(e && e[0] == '0') && stream != nullptr;  // no capture on the legacy stream
+    // programmatic dependent launch: opt-in (JETB200_PDL=1).  Measured on the C3 amplitude with
+    // the TMA-fed K3: 10.22 s with PDL vs 9.28 s without (gather K3: 10.08 vs 9.72 s), i.e. the
+    // early-launched dependents cost more than the prologue overlap saves
+    // (profiles/r02_variants_pdl.txt)
     const char* q = std::getenv("JETB200_PDL");
-    ex->pdl = !(q && q[0] == '0');
+    ex->pdl = q && q[0] == '1';
   }
   const int32_t* dptr = reinterpret_cast<const int32_t*>(static_cast<char*>(d_ws) + ex->L.state_base +
                                                          offsetof(SliceState, digits));

@@ -18,16 +18,10 @@ ks = {k: (v["launches"], round(v["ms"], 1), v["GBps"] and round(v["GBps"])) for 
 print(t, "ms/step %.1f" % d["ms_per_step"], "frac %.3f" % r["frac"], "clk", d["clocks"]["sm_mhz"], d["clocks"]["reasons"], ks)
 PY
 }
+# each argument: tag or tag:ENV=VAL,ENV=VAL (e.g. nopdl_gather:JETB200_PDL=0,JETB200_K3_TMA=0)
 for v in "$@"; do
-  case $v in
-    default) run default X=1 ;;
-    nopdl) run nopdl JETB200_PDL=0 ;;
-    nographs) run nographs JETB200_GRAPHS=0 ;;
-    gather) run gather JETB200_K3_TMA=0 ;;
-    rs8) run rs8 JETB200_K3_RS=8 ;;
-    rs4) run rs4 JETB200_K3_RS=4 ;;
-    mincopy2k) run mincopy2k JETB200_TMA_MINCOPY=2048 ;;
-    mincopy8k) run mincopy8k JETB200_TMA_MINCOPY=8192 ;;
-    k2s) run k2s JETB200_K2S=1 ;;
-  esac
+  tag=${v%%:*}
+  envs="X=1"
+  if [[ "$v" == *:* ]]; then envs=$(echo "${v#*:}" | tr ',' ' '); fi
+  run "$tag" $envs
 done
