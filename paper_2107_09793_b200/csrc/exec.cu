@@ -383,10 +383,22 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   en.grid_x = t.n_tiles;
   en.args.splits = 1;
   en.args.n_tiles = t.n_tiles;
+  // output layout: [M][7 rows][outer] (JETB200_K3_MLOW=1, tm >= 3 so a row's m values are
+  // whole 16-B pairs) puts the small operand's new legs -- which the next absorption contracts --
+  // lowest, next to the rows; default [rows][M][outer]
+  {
+    const char* e = std::getenv("JETB200_K3_MLOW");
+    t.mlow = (e && e[0] == '1' && tm >= 3 && Np == 2 << tm) ? 1 : 0;
+  }
   out.bits.clear();
   int64_t st = 1;
-  for (auto b : tN) { out.bits.push_back({b, st}); st <<= 1; }
-  for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
+  if (t.mlow) {
+    for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
+    for (auto b : tN) { out.bits.push_back({b, st}); st <<= 1; }
+  } else {
+    for (auto b : tN) { out.bits.push_back({b, st}); st <<= 1; }
+    for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
+  }
   for (auto b : oN) { out.bits.push_back({b, st}); st <<= 1; }
   return true;
 }
@@ -1306,7 +1318,8 @@ void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector
           re += (double)x.x * y.x - (double)x.y * y.y;
           im += (double)x.x * y.y + (double)x.y * y.x;
         }
-        C[(t << (7 + p.tm)) + ((int64_t)m << 7) + n] = make_float2((float)re, (float)im);
+        C[(t << (7 + p.tm)) + (p.mlow ? ((int64_t)n << p.tm) + m : ((int64_t)m << 7) + n)] =
+            make_float2((float)re, (float)im);
       }
     }
   }

@@ -33,7 +33,7 @@ constexpr int kTcMaxTile = 12;  // 7 row bits + up to 5 K bits per chunk
 struct TcArgs {
   const float2* A;  // small operand (all bits in the tile)
   const float2* B;  // big operand
-  float2* C;        // output, layout [7 row (n) bits][tm bits][outer bits]
+  float2* C;        // output, layout [7 row (n) bits][tm bits][outer bits], or [tm][7 rows][outer] (mlow)
   int64_t n_tiles;
   int32_t n_outer, tm, K, tkc, n_kc, nX, swz;  // K contracted bits, tkc per chunk, n_kc = 2^(K-tkc)
   int32_t Np, Kpc;                             // MMA N (2*2^tm); TF32 per row per chunk (2*2^tkc)
@@ -54,6 +54,7 @@ struct TcArgs {
   int32_t vecB;                                // 1: chunk-tile bit 0 is a K bit at global stride 1
                                                //    -> gather k-pairs as 16-B copies
   int32_t tma;                                 // 1: items arrive by TMA bulk copies (gett_tc_kernel<TKC, true>)
+  int32_t mlow;                                // output layout [M bits][7 row bits][outer] (else [rows][M][outer])
   int32_t ncopy, copy_bytes;                   // bulk copies per item (the stride-1 run each) and their size
   int64_t xoff[32];                            //   ... copy j reads at item base + xoff[j], lands at j * copy_bytes
   int32_t rofs_row[7], rofs_k[5];              // TMA landing: byte offset of row bit i / chunk K bit j
@@ -523,7 +524,12 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int m = c0 / 2 + j;
-          if (m < nm) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+          if (!p.mlow && m < nm) out[row + ((int64_t)m << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+        }
+        if (p.mlow && c0 / 2 < nm) {  // [M][rows] layout: this row's m values are contiguous
+          float4* o4 = reinterpret_cast<float4*>(out + ((int64_t)row << p.tm) + c0 / 2);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
       }
       tc::fence_before();

@@ -170,3 +170,15 @@ def test_emulated_k2s_and_k3_tma_match_oracle_grid(monkeypatch):
     ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
     v = jet.debug_emulate_host(plan, 0, 16, "c64")
     assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4
+
+
+def test_emulated_k3_mlow_layout_matches_oracle(jet, monkeypatch):
+    """K3 with the [M][rows][outer] output layout (JETB200_K3_MLOW=1) on C2: emulated descriptors
+    (the layout propagates into every consumer's strides) match the oracle."""
+    monkeypatch.setenv("JETB200_K3_MLOW", "1")
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6, bytes_weight=5.0)
+    ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[7]))
+    v = jet.debug_emulate_host(plan, 7, 8, "c64")
+    assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4

@@ -403,3 +403,18 @@ def test_k2s_and_k3_tma_grid_parity(jet, monkeypatch):
     for tag, v in out.items():
         assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4, tag
     assert np.max(np.abs(out["default"] - out["no_k2s"]) / np.abs(ref)) < 2e-5
+
+
+@pytest.mark.parametrize("env", [{"JETB200_K3_MLOW": "1"}, {"JETB200_TMA_MINCOPY": "16"},
+                                 {"JETB200_K3_TMA": "0"}, {"JETB200_PDL": "1"}])
+def test_c2_benched_variants_vs_oracle(jet, monkeypatch, env):
+    """The opt-in layout / item-path / launch-mode variants on the benched C2 plan: all 64 slices
+    against the oracle goldens (1e-4)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rec, gold = load("C2")
+    _, _, _, plan = benched_plan(jet, rec)
+    ex, _ = exec_on_stream(jet, plan, "c64")
+    vals = block_values(jet, ex, 0, 64)
+    ref = np.array([gold[i] for i in range(64)])
+    assert np.max(np.abs(vals - ref) / np.abs(ref)) < 1e-4
