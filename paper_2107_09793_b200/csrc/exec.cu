@@ -565,6 +565,14 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
     if (t.lg_bm < 0) t.lg_bm = 0;
   }
   t.lg_kc = (int)ko.size();
+  // FP32 accumulation in TMEM over very long K drifts (C5: 2^19-complex K, 7.9e-3 relative vs
+  // the CUDA-core path): the accumulator restarts every 2^JETB200_TCG_SEG chunks (default 2^6 =
+  // 1024 complex) and the epilogue sums the segments in FP32 in order
+  {
+    int seg = 6;
+    if (const char* e = getenv("JETB200_TCG_SEG")) seg = std::max(0, atoi(e));
+    t.lg_kcs = std::min(t.lg_kc, seg);
+  }
   t.nXb = 11;
   t.nAb = tmt + 4;
   t.Np = NP;

@@ -23,6 +23,9 @@ struct TcgArgs {
   int64_t n_tiles;          // 2^(n_oN + n_oM)
   int32_t n_oN, n_oM;       // outer bits of the tile index: N bits first (B strides), then M (A)
   int32_t tmt, lg_kc;       // M tile bits; K chunk-index bits (n_kc = 2^lg_kc)
+  int32_t lg_kcs;           // chunks per accumulation segment (log2, <= lg_kc): the TMEM
+                            // accumulator restarts every 2^lg_kcs chunks and the epilogue adds the
+                            // segment sums into the output tile in order (long-K precision)
   int32_t nXb, nAb;         // tile bits of a B chunk (7 + 4) and of an A chunk (tmt + 4)
   int32_t Np;               // MMA N = 2 * 2^tmt
   uint32_t idesc, tmem_cols;
@@ -419,9 +422,10 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
     const bool leader = lane == 0;
     int64_t tt = 0;
     int ys = 0;
+    const int64_t seg_mask = ((int64_t)1 << p.lg_kcs) - 1;
     for (int64_t it = 0; it < items; ++it) {
       const int xs = (int)(it & 3);
-      const int64_t c = it & kc_mask;
+      const int64_t c = it & seg_mask;  // chunk within the accumulation segment
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
       if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);
@@ -440,18 +444,23 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
         }
         tc::mma_commit(&xempty[xs]);
         tc::mma_commit(&yempty[ys]);
-        if (c == kc_mask) tc::mma_commit(&tfull[b]);
+        if (c == seg_mask) tc::mma_commit(&tfull[b]);
       }
       __syncwarp();
-      if (c == kc_mask) ++tt;
+      if (c == seg_mask) ++tt;
       if (++ys == p.ystages) ys = 0;
     }
   } else if (warp < 4) {
     // ===================== epilogue =====================
+    // one accumulator drain per K segment of 2^lg_kcs chunks: the first segment of a tile stores,
+    // the others add into the tile (read-modify-write, L2-resident), in segment order
     const int row = warp * 32 + lane;
-    for (int64_t tt = 0; tt < my_tiles; ++tt) {
-      const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
-      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
+    const int lg_seg = p.lg_kc - p.lg_kcs;
+    for (int64_t st = 0; st < (my_tiles << lg_seg); ++st) {
+      const int64_t tt = st >> lg_seg;
+      const bool first = (st & (((int64_t)1 << lg_seg) - 1)) == 0;
+      const int b = p.acc_bufs == 2 ? (int)(st & 1) : 0;
+      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((st >> 1) & 1) : (uint32_t)(st & 1);
       tc::mbar_wait(&tfull[b], tph);
       tc::fence_after();
       const int64_t t = tcg::raster((int64_t)blockIdx.x + tt * gridDim.x, p);
@@ -460,8 +469,17 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
       for (int c0 = 0; c0 < NP; c0 += 16) {
         float v[16];
         tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * NP + c0), v);
+        if (first) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) out[row + ((int64_t)(c0 / 2 + j) << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+          for (int j = 0; j < 8; ++j) out[row + ((int64_t)(c0 / 2 + j) << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+        } else {
+          float2 o[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = out[row + ((int64_t)(c0 / 2 + j) << 7)];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            out[row + ((int64_t)(c0 / 2 + j) << 7)] = make_float2(o[j].x + v[2 * j], o[j].y + v[2 * j + 1]);
+        }
       }
       tc::fence_before();
       tc::mbar_arrive(&tempty[b]);

@@ -307,6 +307,7 @@ def test_k3_consumer_layout_and_pair_gathers_parity(jet, monkeypatch):
     net = jet.Network.from_circuit(circ, bits)
     monkeypatch.setenv("JETB200_CONSUMER_LAYOUT", "1")
     monkeypatch.setenv("JETB200_K3_VEC", "1")
+    monkeypatch.setenv("JETB200_K3_TMA", "0")   # the pair gathers belong to the cp.async path
     plan = jet.Plan.greedy(net, seed=1, trials=256, n_sliced=6, bytes_weight=5.0)
     nodes = plan.describe_exec("c64")["nodes"]
     assert any(n["kind"] == 1 and n["vecB"] == 1 for n in nodes)
