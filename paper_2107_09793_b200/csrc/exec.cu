@@ -566,10 +566,13 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   }
   t.lg_kc = (int)ko.size();
   // FP32 accumulation in TMEM over very long K drifts (C5: 2^19-complex K, 7.9e-3 relative vs
-  // the CUDA-core path): the accumulator restarts every 2^JETB200_TCG_SEG chunks (default 2^6 =
-  // 1024 complex) and the epilogue sums the segments in FP32 in order
+  // the CUDA-core path, 1.07e-3 vs the P7 closed form): the accumulator restarts every
+  // 2^JETB200_TCG_SEG chunks and the epilogue sums the segments in FP32 in order.  Measured on
+  // the benched C5 plan (profiles/r02_c5_segments.txt), K3g vs K2 / worst P7 slice / K3g time:
+  // seg 8: 1.8e-4 / 8.8e-5 / +2%; seg 6: 1.0e-4 / 8.6e-5 / +5%; seg 4: 4.2e-5 / 6.9e-5 / +13%.
+  // Default 4 (256 complex per segment, the longest accumulation K3 itself does)
   {
-    int seg = 6;
+    int seg = 4;
     if (const char* e = getenv("JETB200_TCG_SEG")) seg = std::max(0, atoi(e));
     t.lg_kcs = std::min(t.lg_kc, seg);
   }
