@@ -67,7 +67,22 @@ struct ExecNode {
   // bit keys the consumer (parent) contracts: the producer puts one of them at stride 1 in its
   // output when it can (consumer-ordered layout -> 16-B k-pair gathers in a K3 consumer)
   std::vector<int64_t> pref_low;
+  // bit keys of this node's output that its parent contracts (shared with the sibling)
+  std::vector<int64_t> consumer_k;
 };
+
+// Consumer-aware order (K3, default; JETB200_K3_CORDER=0 keeps stride order): the bits the parent
+// contracts first within the small-operand (M) bits and within the tile-index (outer) bits, so the
+// parent's K chunk sits right above the 7 row bits in this node's output and the parent's item
+// is one long contiguous run (one or a few TMA-engine copies).  Both orders are free: the epilogue
+// writes [rows][M][outer] whatever the bit order inside M and inside outer.
+template <typename T, typename Key>
+void consumer_first(std::vector<T>& v, const std::vector<int64_t>& ck, Key key) {
+  const char* e = std::getenv("JETB200_K3_CORDER");
+  if ((e && e[0] == '0') || ck.empty()) return;
+  std::stable_partition(v.begin(), v.end(),
+                        [&](const T& x) { return std::find(ck.begin(), ck.end(), key(x)) != ck.end(); });
+}
 
 // Move the first bit of `t` that the consumer contracts to the front (it gets stride 1 in the
 // output view); the others keep their order.
@@ -292,6 +307,8 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   for (size_t i = 0; i < N.size(); ++i) (i < 7 ? tN : oN).push_back(N[i].second);
   if ((int)oN.size() > 31) return false;
   prefer_low(tN, en.pref_low);
+  consumer_first(M, en.consumer_k, [](const std::pair<int64_t, int64_t>& x) { return x.second; });
+  consumer_first(oN, en.consumer_k, [](int64_t x) { return x; });
   TcArgs& t = en.tc;
   std::memset(&t, 0, sizeof(t));
   t.tm = tm;
@@ -1062,12 +1079,13 @@ Layout compile(const jt_plan& plan, int esize) {
     // consumer-ordered output layouts: opt-in (JETB200_CONSUMER_LAYOUT=1); measured neutral to
     // slightly slower on C3 without the 16-B gathers (10.34 s vs 10.03 s)
     const char* cl = std::getenv("JETB200_CONSUMER_LAYOUT");
-    if (n.parent >= 0 && cl && cl[0] == '1') {
+    if (n.parent >= 0) {
       const PlanNode& par = plan.nodes[n.parent];
       const int64_t sib = par.left == v ? par.right : par.left;
       for (int64_t l : n.labels)
         if (std::find(plan.nodes[sib].labels.begin(), plan.nodes[sib].labels.end(), l) != plan.nodes[sib].labels.end())
-          for (int j = 0; j < lb; ++j) en.pref_low.push_back(l * lb + j);
+          for (int j = 0; j < lb; ++j) en.consumer_k.push_back(l * lb + j);
+      if (cl && cl[0] == '1') en.pref_low = en.consumer_k;
     }
     if (en.opA < nt) en.sliceA = leaf_slices[en.opA];
     if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
