@@ -468,6 +468,34 @@ bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& 
   for (int j = 0; j < t.n_outer; ++j) t.o_sB[j] = N[8 + j].first;
   for (int i = 0; i < 8; ++i) t.rofs_n[i] = 8 << rank[i];
   for (int j = 0; j < kt; ++j) t.rofs_k[j] = 8 << rank[8 + j];
+  {  // lane-linear read map: ranks 0-4 -> lanes, the 3 lowest-rank column bits above -> warp,
+     // the remaining kt ranks -> iterations
+    std::vector<int> who(8 + kt);   // rank -> item bit (0..7 column bit, 8.. K bit)
+    for (int b = 0; b < 8 + kt; ++b) who[rank[b]] = b;
+    auto kidx = [&](int b) { return b >= 8 ? 1 << (b - 8) : 0; };
+    auto nidx = [&](int b) { return b < 8 ? 1 << b : 0; };
+    for (int r = 0; r < 5; ++r) {
+      t.lane_kidx[r] = kidx(who[r]);
+      t.lane_nidx[r] = nidx(who[r]);
+      if (who[r] >= 8) t.lane_kmask |= 1 << r;
+    }
+    int nwb = 0, nib = 0;
+    for (int r = 5; r < 8 + kt; ++r) {
+      const int b = who[r];
+      if (b < 8 && nwb < 3) {
+        t.warp_rank[nwb] = r;
+        t.warp_nidx[nwb] = nidx(b);
+        ++nwb;
+      } else {
+        t.it_rank[nib] = r;
+        t.it_kidx[nib] = kidx(b);
+        t.it_nidx[nib] = nidx(b);
+        if (b >= 8) t.it_kmask |= 1 << nib;
+        ++nib;
+      }
+    }
+    if (nwb != 3 || nib != kt) return false;
+  }
   for (int i = 0; i < tm; ++i) t.aM[i] = M[i].first;
   for (int j = 0; j < kt; ++j) t.aK[j] = sa[K[j].second];
   t.n_tiles = int64_t(1) << t.n_outer;
@@ -1276,6 +1304,23 @@ void emulate_stream(const StreamArgs& p, const ExecNode& en, char* ws, const std
     int64_t base = 0;
     for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
     const std::vector<int64_t> box = landing(base, p.ncopy, p.copy_bytes, p.xoff, (size_t)256 << kt);
+    // the kernel's lane-linear read map: thread (warp w, lane l), iteration it reads packed
+    // position l + wpos + itpos and takes it as column n = nl | nw | itn, k = kl | itk
+    for (int w = 0; w < 8; ++w)
+      for (int l = 0; l < 32; ++l)
+        for (int it = 0; it < (1 << kt); ++it) {
+          int pos = l, n = 0, k = 0;
+          for (int i = 0; i < 5; ++i)
+            if ((l >> i) & 1) { n |= p.lane_nidx[i]; k |= p.lane_kidx[i]; }
+          for (int j = 0; j < 3; ++j)
+            if ((w >> j) & 1) { pos += 1 << p.warp_rank[j]; n |= p.warp_nidx[j]; }
+          for (int b = 0; b < kt; ++b)
+            if ((it >> b) & 1) { pos += 1 << p.it_rank[b]; n |= p.it_nidx[b]; k |= p.it_kidx[b]; }
+          int64_t want = base;
+          for (int i = 0; i < 8; ++i) if ((n >> i) & 1) want += en.stN[i];
+          for (int j = 0; j < kt; ++j) if ((k >> j) & 1) want += en.stK[j];
+          if (box[(size_t)pos] != want) fail(JT_EINTERNAL, "emulate: K2s read map mismatch");
+        }
     for (int n = 0; n < 256; ++n) {
       int64_t noff = 0, nb = base;
       for (int i = 0; i < 8; ++i) if ((n >> i) & 1) { noff += p.rofs_n[i]; nb += en.stN[i]; }
