@@ -307,7 +307,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def tensor_peak_alg(dtype):
+def tensor_peak_alg(dtype, gauss=False):
     """Algorithmic complex-FLOP peak of the tensor path: TF32 = measured bf16 burst x 1/2 (the
     guide's nominal TF32:BF16 ratio), divided by 3 for the 3xTF32 split (the 4M real expansion
     does exactly the complex work: 4 real MACs = 8 real FLOP per complex MAC).  c128 runs on
@@ -316,16 +316,20 @@ def tensor_peak_alg(dtype):
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     bf16 = json.load(open(p)).get("bf16_tflops", 1590.0) if os.path.exists(p) else 1590.0
     if dtype == "c128":
+        if gauss:   # K4 in the 3M form: 3 real MACs per complex MAC, so the algorithmic peak is 4/3x
+            return 37.0 * 4 / 3, ("measured FP64 DMMA peak 37.0 TFLOP/s x 4/3 (K4 3M form: 6 real FLOP "
+                                  "per complex MAC on the pipe; scripts/fp64_probe.cu, profiles/r01_fp64_probe.txt)")
         return 37.0, "measured FP64 DMMA peak 37.0 TFLOP/s (scripts/fp64_probe.cu, profiles/r01_fp64_probe.txt)"
     return bf16 * 0.5 / 3.0, f"measured bf16 {bf16} x 0.5 (TF32) / 3 (3xTF32)"
 
 
 KERNEL_NAMES = {"K3": "tcgen05 3xTF32, resident small operand, TMA-fed", "K3G": "tcgen05 3xTF32, both operands streamed",
-                "K2": "CUDA-core GETT", "K4": "FP64 tensor-core DMMA GETT", "K2S": "TMA-fed streaming GETT (skinny)"}
+                "K2": "CUDA-core GETT", "K4": "FP64 tensor-core DMMA GETT", "K2S": "streaming GETT, small operand in registers (skinny)"}
 
 
-def roofline_entry(args, dom, gbs, tfs, dom_bytes, dom_n, dom_ms, peak, peak_kind, ms_max, prof_steps, kern, dtype):
-    tpeak, tkind = tensor_peak_alg(dtype)
+def roofline_entry(args, dom, gbs, tfs, dom_bytes, dom_n, dom_ms, peak, peak_kind, ms_max, prof_steps, kern, dtype,
+                   gauss=False):
+    tpeak, tkind = tensor_peak_alg(dtype, gauss and dom == "K4")
     fh = (gbs / peak) if gbs else None
     ft = (tfs / tpeak) if tfs else None
     bound = "tensor" if (ft or 0) > (fh or 0) else "hbm"
@@ -598,7 +602,7 @@ def run_ours(args, cfg):
     dom_gbs = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     dom_tfs = dom_flop / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
     names = {"K3": "K3_tcgen05", "K3G": "K3g_tcgen05_streamed", "K2": "K2_cuda_core", "K4": "K4_dmma_fp64",
-             "K2S": "K2s_tma_stream"}
+             "K2S": "K2s_stream"}
     kern_info = {names[q]: {"launches": int(v[2]), "ms": v[0], "GBps": (v[1] / (v[0] / 1e3) / 1e9) if v[0] > 0 else None,
                             "TFLOPs_alg": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else None}
                  for q, v in cls.items()}
@@ -696,7 +700,9 @@ def run_ours(args, cfg):
             "gpu_launches": int(tot_launch),
             "clocks": clk,
             "roofline": roofline_entry(args, dom, dom_gbs, dom_tfs, dom_bytes, dom_n, dom_ms, peak, peak_kind,
-                                       ms_max, prof_steps, kern_info, cfg["dtype"]),
+                                       ms_max, prof_steps, kern_info, cfg["dtype"],
+                                       gauss=any(n.get("gauss") for n in plan.describe_exec(cfg["dtype"])["nodes"]
+                                                 if n["kind"] == 3)),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "algorithmic_gbs_step": tot_bytes / (ms_max / 1e3) / 1e9,

@@ -124,8 +124,9 @@ typedef struct {
   int64_t k3g_timed_launches;
   double k3g_timed_bytes;
   double k3g_timed_flop;
-  double k2s_time_ms;         /* ... the subset of the timed launches that ran on K2s (TMA-fed
-                                 streaming GETT for skinny c64 nodes; not counted under K3) */
+  double k2s_time_ms;         /* ... the subset of the timed launches that ran on K2s (streaming
+                                 GETT for skinny c64 nodes, small operand in registers; not
+                                 counted under K3) */
   int64_t k2s_timed_launches;
   double k2s_timed_bytes;
   double k2s_timed_flop;

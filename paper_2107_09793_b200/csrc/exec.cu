@@ -45,9 +45,9 @@ struct View {
 
 struct ExecNode {
   int kind = 0;  // 0: K2 CUDA-core GETT, 1: K3 tcgen05 (resident A), 2: K3g tcgen05 (streamed A),
-                 // 3: K4 DMMA (c128), 4: K2s TMA-fed streaming GETT (skinny c64)
+                 // 3: K4 DMMA (c128), 4: K2s streaming GETT (skinny c64, A in registers)
   StreamArgs st{};
-  std::vector<int64_t> stN, stK;  // K2s: B strides of the 8 tile columns and the K bits (emulator)
+  std::vector<int64_t> stN, stK;  // K2s: B strides of the column bits and the K bits (emulator)
   TcArgs tc{};
   TcgArgs tcg{};
   std::vector<int64_t> tcgA_m, tcgA_k, tcgB_oN, tcgA_oM;  // K3g host strides (emulator)
@@ -141,17 +141,18 @@ StreamFn pick_stream(int tm, int kt) {
 #define JT_SCASE(a, b) \
   if (tm == a && kt == b) return stream_gett_kernel<a, b>;
   JT_SCASE(0, 1) JT_SCASE(0, 2) JT_SCASE(0, 3) JT_SCASE(1, 1) JT_SCASE(1, 2) JT_SCASE(1, 3)
-  JT_SCASE(2, 1) JT_SCASE(2, 2) JT_SCASE(2, 3) JT_SCASE(3, 1) JT_SCASE(3, 2) JT_SCASE(3, 3)
+  JT_SCASE(2, 1) JT_SCASE(2, 2) JT_SCASE(2, 3)
 #undef JT_SCASE
   fail(JT_EINTERNAL, "no stream instance");
 }
 
-GettFn pick_dmma(int SMT, int SNT) {
+GettFn pick_dmma(int SMT, int SNT, bool gauss) {
 #define JT_DCASE(a, b) \
-  if (SMT == a && SNT == b) return gett_dmma_kernel<a, b>;
+  if (SMT == a && SNT == b) return gauss ? gett_dmma_kernel<a, b, true> : gett_dmma_kernel<a, b, false>;
   JT_DCASE(1, 1) JT_DCASE(1, 2) JT_DCASE(1, 4) JT_DCASE(2, 1) JT_DCASE(2, 2) JT_DCASE(2, 4)
-  JT_DCASE(4, 1) JT_DCASE(4, 2) JT_DCASE(4, 4)
+  JT_DCASE(4, 1) JT_DCASE(4, 2)
 #undef JT_DCASE
+  if (SMT == 4 && SNT == 4 && !gauss) return gett_dmma_kernel<4, 4, false>;
   fail(JT_EINTERNAL, "no dmma instance");
 }
 
@@ -184,14 +185,14 @@ void set_smem_attrs() {
     for (int b : rms) {
       set(reinterpret_cast<const void*>(pick_gett<float>(a, b)), 200 * 1024);
       set(reinterpret_cast<const void*>(pick_gett<double>(a, b)), 200 * 1024);
-      set(reinterpret_cast<const void*>(pick_dmma(a, b)), 200 * 1024);
+      set(reinterpret_cast<const void*>(pick_dmma(a, b, false)), 200 * 1024);
+      if (a * b <= 8) set(reinterpret_cast<const void*>(pick_dmma(a, b, true)), 200 * 1024);
     }
   for (int tkc = 2; tkc <= 4; ++tkc)
     for (int tma = 0; tma < 2; ++tma) set(reinterpret_cast<const void*>(pick_tc(tkc, tma != 0)), 222 * 1024);
   for (int tmt = 4; tmt <= 7; ++tmt)
     for (int tma = 0; tma < 2; ++tma) set(reinterpret_cast<const void*>(pick_tcg(tmt, tma != 0)), 222 * 1024);
-  for (int tm = 0; tm <= 3; ++tm)
-    for (int kt = 1; kt <= 3; ++kt) set(reinterpret_cast<const void*>(pick_stream(tm, kt)), 200 * 1024);
+
   set(reinterpret_cast<const void*>(permute_kernel<float2, 0>), 200 * 1024);
   set(reinterpret_cast<const void*>(permute_kernel<float2, 1>), 200 * 1024);
   set(reinterpret_cast<const void*>(permute_kernel<float2, 2>), 200 * 1024);
@@ -420,105 +421,80 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   return true;
 }
 
-// K2s eligibility and descriptor (c64): A tiny (<= 3 free bits, 1..3 contracted bits), B with
-// >= 8 free bits; tiles of B's 8 lowest-stride free bits x all K bits, one TMA box each.
-// Output layout [M bits][8 tile bits][outer bits].  JETB200_K2S=0 disables it, JETB200_K2S_MAXTM
-// (default 2: tm = 3 goes to K3) sets the largest tm taken.
-bool plan_stream(ExecNode& en, const View& va, const View& vb, int esize, View& out) {
-  if (esize != 8 || !tma_enabled()) return false;
-  {  // opt-in (JETB200_K2S=1): measured 2.0 TB/s on the C3 skinny nodes vs 3.4-5.0 TB/s for K2
-     // (shared-memory bank conflicts of the column-per-thread reads, profiles/r02_nodes_C3_tma.txt)
-    const char* e = std::getenv("JETB200_K2S");
-    if (!(e && e[0] == '1')) return false;
-  }
-  int maxtm = 2;
-  if (const char* e = std::getenv("JETB200_K2S_MAXTM")) maxtm = std::max(0, std::min(3, atoi(e)));
+// K2s eligibility and descriptor (c64): A tiny (<= 2 free bits, 1..3 contracted bits), B with
+// >= 10 free bits.  `kv` is the K2 output view of the same node ([tile-N][tile-M][outer], from
+// plan_gett): K2s writes exactly that layout when the M bits are adjacent in it, so the consumer
+// sees what K2 would have produced.  JETB200_K2S=0 keeps such nodes on K2.
+bool plan_stream(ExecNode& en, const View& va, const View& vb, const View& kv, int esize) {
+  if (esize != 8) return false;
+  if (const char* e = std::getenv("JETB200_K2S"))
+    if (e[0] == '0') return false;
   std::map<int64_t, int64_t> sa, sb;
   for (auto& x : va.bits) sa[x.first] = x.second;
   for (auto& x : vb.bits) sb[x.first] = x.second;
-  std::vector<std::pair<int64_t, int64_t>> M, N, K;
+  std::vector<std::pair<int64_t, int64_t>> M, K;  // (stride in A / in B, bit)
   for (auto& x : va.bits) {
     if (sb.count(x.first)) K.push_back({sb[x.first], x.first});
     else M.push_back({x.second, x.first});
   }
-  for (auto& x : vb.bits)
-    if (!sa.count(x.first)) N.push_back({x.second, x.first});
   const int tm = (int)M.size(), kt = (int)K.size();
-  if (tm > maxtm || kt < 1 || kt > 3 || (int)N.size() < 8 || (int)N.size() - 8 > kMaxOuter) return false;
-  std::sort(M.begin(), M.end());
-  std::sort(N.begin(), N.end());
-  std::sort(K.begin(), K.end());
-  std::vector<int64_t> item;
-  for (int i = 0; i < 8; ++i) item.push_back(N[i].first);
-  for (int j = 0; j < kt; ++j) item.push_back(K[j].first);
-  std::vector<int> rank;
-  int ncopy = 0, clog = 0;
-  int64_t xoff[32];
-  for (auto& x : en.sliceB)
-    if (x.second % 2) return false;
-  if (!tma_item_dims(item, &ncopy, &clog, xoff, rank)) return false;
+  const int ncols = (int)vb.bits.size() - kt;
+  if (tm > 2 || kt < 1 || kt > 3 || ncols < 10 || ncols > kStreamMaxCols) return false;
+  // the K2 layout: column bits (B free) in output order, the M bits adjacent at n_lo
+  std::vector<int64_t> cols, mo;
+  int n_lo = -1;
+  for (size_t i = 0; i < kv.bits.size(); ++i) {
+    const int64_t b = kv.bits[i].first;
+    if (sa.count(b)) {
+      if (n_lo < 0) n_lo = (int)i;
+      else if ((int)i != n_lo + (int)mo.size()) return false;
+      mo.push_back(b);
+    } else {
+      cols.push_back(b);
+    }
+  }
+  if (tm == 0) n_lo = ncols;
+  if ((int)cols.size() != ncols || (int)mo.size() != tm) return false;
+  std::sort(K.begin(), K.end());  // lowest B stride first: K bit 0 is the pair bit when stride 1
   StreamArgs& t = en.st;
   std::memset(&t, 0, sizeof(t));
-  t.rbytes = 8 << (8 + kt);
-  t.rstages = std::min(8, (200 * 1024 - 1024) / t.rbytes);
-  t.ncopy = ncopy;
-  t.copy_bytes = 8 << clog;
-  for (int j = 0; j < ncopy; ++j) t.xoff[j] = xoff[j];
-  t.n_outer = (int)N.size() - 8;
-  for (int j = 0; j < t.n_outer; ++j) t.o_sB[j] = N[8 + j].first;
-  for (int i = 0; i < 8; ++i) t.rofs_n[i] = 8 << rank[i];
-  for (int j = 0; j < kt; ++j) t.rofs_k[j] = 8 << rank[8 + j];
-  {  // lane-linear read map: ranks 0-4 -> lanes, the 3 lowest-rank column bits above -> warp,
-     // the remaining kt ranks -> iterations
-    std::vector<int> who(8 + kt);   // rank -> item bit (0..7 column bit, 8.. K bit)
-    for (int b = 0; b < 8 + kt; ++b) who[rank[b]] = b;
-    auto kidx = [&](int b) { return b >= 8 ? 1 << (b - 8) : 0; };
-    auto nidx = [&](int b) { return b < 8 ? 1 << b : 0; };
-    for (int r = 0; r < 5; ++r) {
-      t.lane_kidx[r] = kidx(who[r]);
-      t.lane_nidx[r] = nidx(who[r]);
-      if (who[r] >= 8) t.lane_kmask |= 1 << r;
-    }
-    int nwb = 0, nib = 0;
-    for (int r = 5; r < 8 + kt; ++r) {
-      const int b = who[r];
-      if (b < 8 && nwb < 3) {
-        t.warp_rank[nwb] = r;
-        t.warp_nidx[nwb] = nidx(b);
-        ++nwb;
-      } else {
-        t.it_rank[nib] = r;
-        t.it_kidx[nib] = kidx(b);
-        t.it_nidx[nib] = nidx(b);
-        if (b >= 8) t.it_kmask |= 1 << nib;
-        ++nib;
-      }
-    }
-    if (nwb != 3 || nib != kt) return false;
+  t.n_cols = ncols;
+  t.n_lo = n_lo;
+  bool even = K[0].first == 1;
+  for (int j = 0; j < ncols; ++j) {
+    t.sN[j] = sb[cols[j]];
+    even &= t.sN[j] % 2 == 0;
   }
-  for (int i = 0; i < tm; ++i) t.aM[i] = M[i].first;
-  for (int j = 0; j < kt; ++j) t.aK[j] = sa[K[j].second];
-  t.n_tiles = int64_t(1) << t.n_outer;
+  for (int j = 1; j < kt; ++j) even &= K[j].first % 2 == 0;
+  for (auto& x : en.sliceB) even &= (x.second % 2) == 0;
+  t.vec = even ? 1 : 0;
+  for (int k = 0; k < (1 << kt); ++k) {
+    int64_t o = 0;
+    for (int j = 0; j < kt; ++j) if ((k >> j) & 1) o += K[j].first;
+    t.kofs[k] = o;
+  }
+  for (int m = 0; m < (1 << tm); ++m)
+    for (int k = 0; k < (1 << kt); ++k) {
+      int64_t o = 0;
+      for (int i = 0; i < tm; ++i) if ((m >> i) & 1) o += sa[mo[i]];
+      for (int j = 0; j < kt; ++j) if ((k >> j) & 1) o += sa[K[j].second];
+      t.aofs[m * (1 << kt) + k] = o;
+    }
   en.stN.clear();
   en.stK.clear();
-  for (int i = 0; i < 8; ++i) en.stN.push_back(N[i].first);
+  for (int j = 0; j < ncols; ++j) en.stN.push_back(t.sN[j]);
   for (int j = 0; j < kt; ++j) en.stK.push_back(K[j].first);
   en.kind = 4;
   en.args.tm = tm;   // (reported by jt_exec_describe)
   en.args.tk = kt;
-  en.args.tn = 8;
-  en.args.n_outer = t.n_outer;
+  en.args.tn = n_lo;
+  en.args.n_outer = ncols - n_lo;
   en.args.splits = 1;
-  en.args.n_tiles = t.n_tiles;
-  en.smem = (size_t)t.rstages * t.rbytes + 1024;
-  en.block = 288;
-  en.n_out = t.n_tiles << (8 + tm);
-  en.grid_x = t.n_tiles;
-  out.bits.clear();
-  int64_t st = 1;
-  for (auto& b : M) { out.bits.push_back({b.second, st}); st <<= 1; }
-  for (int i = 0; i < 8; ++i) { out.bits.push_back({N[i].second, st}); st <<= 1; }
-  for (int j = 8; j < (int)N.size(); ++j) { out.bits.push_back({N[j].second, st}); st <<= 1; }
+  en.args.n_tiles = int64_t(1) << ncols;
+  en.smem = 0;
+  en.block = 256;
+  en.n_out = int64_t(1) << (ncols + tm);
+  en.grid_x = 1;
   return true;
 }
 
@@ -708,6 +684,16 @@ View fill_gett(ExecNode& en, std::map<int64_t, int64_t>& sa, std::map<int64_t, i
                const std::vector<std::pair<int64_t, int64_t>>& M, const std::vector<std::pair<int64_t, int64_t>>& N,
                const std::vector<std::pair<int64_t, int64_t>>& K, const std::vector<char>& inM,
                const std::vector<char>& inN, const std::vector<char>& inK, int esize, bool dmma);
+
+// K4 3M (Gauss) form: opt-in (JETB200_K4_3M=1).  Measured on the C4 nodes (one B200,
+// profiles/r02_nodes_C4_k4_3m.txt): 26.7-30.6 TFLOP/s algorithmic in the 3M form (4x2 warp tiles,
+// one 256-thread CTA per SM) vs 28.8-32.1 in the 4M form (4x4 warp tiles, two 128-thread CTAs) --
+// the 4M kernel is already at 86% of the FP64 pipe, and the 3M form's smaller warp tiles double
+// the operand loads per DMMA.
+bool k4_gauss_enabled() {
+  const char* e = std::getenv("JETB200_K4_3M");
+  return e && e[0] == '1';
+}
 
 bool dmma_enabled() {
   const char* e = std::getenv("JETB200_DMMA");
@@ -957,6 +943,16 @@ View fill_gett(ExecNode& en, std::map<int64_t, int64_t>& sa, std::map<int64_t, i
     en.kind = 3;
     en.RM = std::min(4, 1 << (g.tm - 3));
     en.RN = std::min(4, 1 << (g.tn - 3));
+    // 3M (Gauss) form (opt-in, JETB200_K4_3M=1): three accumulators per sub-tile, so warp tiles
+    // of <= 8 sub-tiles (4x2) and CTAs of <= 8 warps
+    g.gauss = 0;
+    if (k4_gauss_enabled()) {
+      const int rn = std::min(2, 1 << (g.tn - 3));
+      if (32 * ((1 << (g.tm - 3)) / en.RM) * ((1 << (g.tn - 3)) / rn) <= 256) {
+        en.RN = rn;
+        g.gauss = 1;
+      }
+    }
     g.TY = (1 << (g.tm - 3)) / en.RM;
     g.TX = (1 << (g.tn - 3)) / en.RN;
     g.KG = 1;
@@ -1119,11 +1115,13 @@ Layout compile(const jt_plan& plan, int esize) {
     if (en.opB < nt) en.sliceB = leaf_slices[en.opB];
     if (en.sliceA.size() > 4 || en.sliceB.size() > 4) fail(JT_EUSAGE, "exec: more than 4 sliced labels on one leaf");
     View tv;
-    if (use_tc && plan_stream(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
-    else if (use_tc && !force_tcg && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
+    if (use_tc && !force_tcg && plan_tc(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
     else if (use_tc && plan_tcg(en, views[en.opA], views[en.opB], esize, tv)) views[v] = tv;
     else if (esize == 16 && use_dmma && plan_dmma(en, views[en.opA], views[en.opB], tv)) views[v] = tv;
-    else views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
+    else {
+      views[v] = plan_gett(en, views[en.opA], views[en.opB], esize);
+      if (use_tc) plan_stream(en, views[en.opA], views[en.opB], views[v], esize);  // K2 layout kept
+    }
     en.maxpos = n.maxpos;
     en.flop = n.flop;
     en.bytes = n.bytes8 / 8.0 * esize;
@@ -1285,63 +1283,44 @@ std::vector<int64_t> landing(int64_t base, int ncopy, int copy_bytes, const int6
   return b;
 }
 
-// K2s: the TMA landing of every tile (read back through rofs_n / rofs_k) and the output layout
-// [M][8 tile bits][outer], with the kernel's FP32 complex arithmetic order
+// K2s: every column's B offsets from the descriptor (the kernel's four 9-bit tables are the
+// GF(2)-linear bit -> stride map, recomputed here bit by bit), the 16-B pair alignment, and the
+// output layout [n_lo columns][M][rest], with the kernel's FP32 complex arithmetic order
 void emulate_stream(const StreamArgs& p, const ExecNode& en, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
   const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
   const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
   float2* C = reinterpret_cast<float2*>(ws + off[2].first);
   const int tm = en.args.tm, kt = en.args.tk, nm = 1 << tm, nk = 1 << kt;
-  std::vector<float2> a((size_t)nm * nk);
-  for (int m = 0; m < nm; ++m)
-    for (int k = 0; k < nk; ++k) {
-      int64_t ao = 0;
-      for (int i = 0; i < tm; ++i) if ((m >> i) & 1) ao += p.aM[i];
-      for (int i = 0; i < kt; ++i) if ((k >> i) & 1) ao += p.aK[i];
-      a[(size_t)m * nk + k] = A[ao];
+  for (int k = 0; k < nk; ++k) {
+    int64_t o = 0;
+    for (int j = 0; j < kt; ++j) if ((k >> j) & 1) o += en.stK[j];
+    if (o != p.kofs[k]) fail(JT_EINTERNAL, "emulate: K2s k offsets");
+  }
+  const int64_t ncol = int64_t(1) << p.n_cols, lo_mask = (int64_t(1) << p.n_lo) - 1;
+  for (int64_t c = 0; c < ncol; ++c) {
+    int64_t bo = 0;
+    for (int h = 0; h < 4; ++h) {
+      const int v = (int)((c >> (9 * h)) & 511);
+      for (int b = 0; b < 9; ++b)
+        if (((v >> b) & 1) && 9 * h + b < p.n_cols) bo += p.sN[9 * h + b];
     }
-  for (int64_t t = 0; t < p.n_tiles; ++t) {
-    int64_t base = 0;
-    for (int j = 0; j < p.n_outer; ++j) if ((t >> j) & 1) base += p.o_sB[j];
-    const std::vector<int64_t> box = landing(base, p.ncopy, p.copy_bytes, p.xoff, (size_t)256 << kt);
-    // the kernel's lane-linear read map: thread (warp w, lane l), iteration it reads packed
-    // position l + wpos + itpos and takes it as column n = nl | nw | itn, k = kl | itk
-    for (int w = 0; w < 8; ++w)
-      for (int l = 0; l < 32; ++l)
-        for (int it = 0; it < (1 << kt); ++it) {
-          int pos = l, n = 0, k = 0;
-          for (int i = 0; i < 5; ++i)
-            if ((l >> i) & 1) { n |= p.lane_nidx[i]; k |= p.lane_kidx[i]; }
-          for (int j = 0; j < 3; ++j)
-            if ((w >> j) & 1) { pos += 1 << p.warp_rank[j]; n |= p.warp_nidx[j]; }
-          for (int b = 0; b < kt; ++b)
-            if ((it >> b) & 1) { pos += 1 << p.it_rank[b]; n |= p.it_nidx[b]; k |= p.it_kidx[b]; }
-          int64_t want = base;
-          for (int i = 0; i < 8; ++i) if ((n >> i) & 1) want += en.stN[i];
-          for (int j = 0; j < kt; ++j) if ((k >> j) & 1) want += en.stK[j];
-          if (box[(size_t)pos] != want) fail(JT_EINTERNAL, "emulate: K2s read map mismatch");
-        }
-    for (int n = 0; n < 256; ++n) {
-      int64_t noff = 0, nb = base;
-      for (int i = 0; i < 8; ++i) if ((n >> i) & 1) { noff += p.rofs_n[i]; nb += en.stN[i]; }
-      float2 b[8];
+    float2 bv[8];
+    for (int k = 0; k < nk; ++k) {
+      if (p.vec && (k % 2) == 0 && ((off[1].second + bo + p.kofs[k]) % 2) != 0)
+        fail(JT_EINTERNAL, "emulate: K2s 16-B pair misaligned");
+      bv[k] = B[bo + p.kofs[k]];
+    }
+    float2* out = C + (c & lo_mask) + ((c >> p.n_lo) << (p.n_lo + tm));
+    for (int m = 0; m < nm; ++m) {
+      float re = 0.f, im = 0.f;
       for (int k = 0; k < nk; ++k) {
-        int64_t ko = 0, want = nb;
-        for (int j = 0; j < kt; ++j) if ((k >> j) & 1) { ko += p.rofs_k[j]; want += en.stK[j]; }
-        if (box[(size_t)((noff + ko) / 8)] != want) fail(JT_EINTERNAL, "emulate: K2s TMA landing mismatch");
-        b[k] = B[want];
+        const float2 x = A[p.aofs[m * nk + k]];
+        re = std::fma(x.x, bv[k].x, re);
+        re = std::fma(-x.y, bv[k].y, re);
+        im = std::fma(x.x, bv[k].y, im);
+        im = std::fma(x.y, bv[k].x, im);
       }
-      for (int m = 0; m < nm; ++m) {
-        float re = 0.f, im = 0.f;
-        for (int k = 0; k < nk; ++k) {
-          const float2 x = a[(size_t)m * nk + k];
-          re = std::fma(x.x, b[k].x, re);
-          re = std::fma(-x.y, b[k].y, re);
-          im = std::fma(x.x, b[k].y, im);
-          im = std::fma(x.y, b[k].x, im);
-        }
-        C[(t << (8 + tm)) + ((int64_t)n << tm) + m] = make_float2(re, im);
-      }
+      out[(int64_t)m << p.n_lo] = make_float2(re, im);
     }
   }
 }
@@ -1565,9 +1544,9 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
     const GettArgs& g = en.args;
     std::fprintf(f, "%s{\"v\": %lld, \"maxpos\": %d, \"flop\": %.17g, \"bytes\": %.17g, \"n_out\": %lld, "
                  "\"tm\": %d, \"tn\": %d, \"tk\": %d, \"n_outer\": %d, \"n_ok\": %d, \"splits\": %d, "
-                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld, \"parent\": %lld, \"pos\": %zu",
+                 "\"block\": %d, \"RM\": %d, \"RN\": %d, \"KG\": %d, \"smem\": %zu, \"vecA\": %d, \"vecB\": %d, \"dbuf\": %d, \"gauss\": %d, \"kind\": %d, \"tc_tm\": %d, \"tc_tk\": %d, \"tc_outer\": %d, \"out_off\": %lld, \"parent\": %lld, \"pos\": %zu",
                  i ? ", " : "", (long long)en.v, en.maxpos, en.flop, en.bytes, (long long)en.n_out, g.tm, g.tn, g.tk,
-                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, en.kind,
+                 g.n_outer, g.n_ok, g.splits, en.block, en.RM, en.RN, g.KG, en.smem, g.vecA, g.vecB, g.dbuf, g.gauss, en.kind,
                  en.kind == 2 ? en.tcg.tmt : en.tc.tm, en.kind == 2 ? 4 + en.tcg.lg_kc : en.tc.K,
                  en.kind == 2 ? en.tcg.n_oN + en.tcg.n_oM : en.tc.n_outer, (long long)L.node_off[en.v],
                  (long long)plan.nodes[en.v].parent, i);
@@ -1585,11 +1564,13 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
                    en.tc.rofs_row[2], en.tc.rofs_row[3], en.tc.rofs_row[4], en.tc.rofs_row[5], en.tc.rofs_row[6]);
       std::fprintf(f, ", \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : en.tcg.tma);
     }
-    if (en.kind == 4)
-      std::fprintf(f, ", \"ncopy\": %d, \"copy_bytes\": %d, \"rofs_n\": [%d, %d, %d, %d, %d, %d, %d, %d], \"rofs_k\": [%d, %d, %d]",
-                   en.st.ncopy, en.st.copy_bytes, en.st.rofs_n[0], en.st.rofs_n[1], en.st.rofs_n[2], en.st.rofs_n[3],
-                   en.st.rofs_n[4], en.st.rofs_n[5], en.st.rofs_n[6], en.st.rofs_n[7], en.st.rofs_k[0], en.st.rofs_k[1],
-                   en.st.rofs_k[2]);
+    if (en.kind == 4) {
+      std::fprintf(f, ", \"st_vec\": %d, \"st_n_lo\": %d, \"st_cols\": %d, \"stN\": [", en.st.vec, en.st.n_lo, en.st.n_cols);
+      for (size_t q = 0; q < en.stN.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.stN[q]);
+      std::fprintf(f, "], \"stK\": [");
+      for (size_t q = 0; q < en.stK.size(); ++q) std::fprintf(f, "%s%lld", q ? ", " : "", (long long)en.stK[q]);
+      std::fprintf(f, "]");
+    }
     std::fprintf(f, "}");
   }
   std::fprintf(f, "]}\n");
@@ -1643,8 +1624,8 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     if (en.kind == 4) {
       JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &nb, reinterpret_cast<const void*>(pick_stream(en.args.tm, en.args.tk)), en.block, en.smem));
-      if (nb < 1) fail(JT_EINTERNAL, "exec: a K2s tile does not fit on an SM");
-      en.grid_x = std::min<int64_t>(en.st.n_tiles, (int64_t)nb * n_sm);
+      if (nb < 1) fail(JT_EINTERNAL, "exec: a K2s block does not fit on an SM");
+      en.grid_x = std::max<int64_t>(1, std::min<int64_t>(en.args.n_tiles / 512, (int64_t)nb * n_sm));
       continue;
     }
     if (en.kind == 1) {
@@ -1655,7 +1636,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
       en.grid_x = std::min<int64_t>(en.tc.n_tiles, (int64_t)nb * n_sm);
       continue;
     }
-    const void* fn = en.kind == 3   ? reinterpret_cast<const void*>(pick_dmma(en.RM, en.RN))
+    const void* fn = en.kind == 3   ? reinterpret_cast<const void*>(pick_dmma(en.RM, en.RN, en.args.gauss != 0))
                      : dt == JT_C64 ? reinterpret_cast<const void*>(pick_gett<float>(en.RM, en.RN))
                                     : reinterpret_cast<const void*>(pick_gett<double>(en.RM, en.RN));
     JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, en.block, en.smem));
@@ -1805,7 +1786,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     g.C = ex->ws + en.out_off;
     g.P = ex->ws + en.part_off;
     dim3 grid((unsigned)en.grid_x, (unsigned)g.splits);
-    GettFn fn = en.kind == 3 ? pick_dmma(en.RM, en.RN) : pick_gett<R>(en.RM, en.RN);
+    GettFn fn = en.kind == 3 ? pick_dmma(en.RM, en.RN, g.gauss != 0) : pick_gett<R>(en.RM, en.RN);
     ev_begin(ex);
     launch_pdl(fn, grid, dim3(en.block), en.smem, ex->stream, ex->pdl, g);
     ev_end(ex, en);

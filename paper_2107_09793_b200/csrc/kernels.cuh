@@ -67,6 +67,7 @@ struct GettArgs {
   int32_t TX, TY, KG;
   int32_t vecA, vecB;  // 1: tile bit 0 has global stride 1 -> 16-B copies of element pairs (c64)
   int32_t dbuf;        // unused (kept for the descriptor dump); the kernel always double-buffers
+  int32_t gauss;       // K4: 1 = 3M (Gauss) complex product, 3 DMMAs per complex MAC (else 4M)
   int64_t o_sA[kMaxOuter], o_sB[kMaxOuter];    // outer M/N bit j: strides in A and B
   int64_t ok_sA[kMaxOuter], ok_sB[kMaxOuter];  // outer K bit j
   int64_t gA[kMaxTile], gB[kMaxTile];          // tile bit j of A (B), sorted by stride: global stride;

@@ -19,6 +19,13 @@
 // the complex product is four real MMAs on the planar parts:
 //   Cr += Ar*Br + (-Ai)*Bi,   Ci += Ar*Bi + Ai*Br.
 // The accumulators (Cr, Ci fragments: row lane/4, columns 2*(lane%4)+{0,1}) stay in registers.
+//
+// GAUSS = true (SURVEY 8a a5 "3M"): the complex product as three real MMAs (Gauss's trick),
+//   P += Ar*Br,  Q += Ai*Bi,  R += (Ar+Ai)*(Br+Bi);   Cr = P - Q,  Ci = R - P - Q
+// -- 25% fewer DMMAs for the FP64-bound GBS nodes, at 1.5x the accumulator registers (so warp
+// tiles of at most 8 sub-tiles).  Rounding: |dC| <~ 3 eps sum|a||b| per K step instead of
+// 2 eps sum|a||b| (normwise; the amplitude parity bar is normwise, A13).  Opt-in
+// (JETB200_K4_3M=1): measured slower than 4M on the C4 nodes (see k4_gauss_enabled, exec.cu).
 #pragma once
 
 #include "kernels.cuh"
@@ -51,7 +58,7 @@ __device__ __forceinline__ void load_tile_c128(double2* dst, const double2* src,
 
 // p.TY x p.TX warps (rows x columns of warp tiles), KG = 1.  2^tm = 8*SMT*TY, 2^tn = 8*SNT*TX,
 // tile-K >= 4 complex.
-template <int SMT, int SNT>
+template <int SMT, int SNT, bool GAUSS>
 __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ GettArgs p) {
   using C2 = double2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -131,11 +138,13 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
       ld_ob += dkB[t];
     }
   };
-  double cr[SMT][SNT][2], ci[SMT][SNT][2];
+  // 4M: cr, ci are Cr, Ci.  3M: cr = P, ci = Q, cs = R (cs unused by 4M; the compiler drops it)
+  double cr[SMT][SNT][2], ci[SMT][SNT][2], cs[SMT][SNT][2];
 #pragma unroll
   for (int i = 0; i < SMT; ++i)
 #pragma unroll
-    for (int j = 0; j < SNT; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < SNT; ++j)
+      cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = cs[i][j][0] = cs[i][j][1] = 0.0;
   if (total > 0) {
     tile_start();
     load_tile_c128(sA0, A + ld_oa, p.nA, tgA, tid, nthr);
@@ -165,26 +174,47 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
       for (int i = 0; i < SMT; ++i) a[i] = sA[ka ^ offM[i]];
 #pragma unroll
       for (int j = 0; j < SNT; ++j) b[j] = sB[kb ^ offN[j]];
-      // four passes over the sub-tiles, so that the two MMAs into one accumulator are
-      // 2*SMT*SNT instructions apart (DMMA latency hidden by independent accumulators)
+      if (GAUSS) {
+        // three passes (P, Q, R accumulators 2*SMT*SNT instructions apart)
+        double sa[SMT], sb[SNT];
 #pragma unroll
-      for (int i = 0; i < SMT; ++i)
+        for (int i = 0; i < SMT; ++i) sa[i] = a[i].x + a[i].y;
 #pragma unroll
-        for (int j = 0; j < SNT; ++j) dmma884(cr[i][j], a[i].x, b[j].x);
+        for (int j = 0; j < SNT; ++j) sb[j] = b[j].x + b[j].y;
 #pragma unroll
-      for (int i = 0; i < SMT; ++i)
+        for (int i = 0; i < SMT; ++i)
 #pragma unroll
-        for (int j = 0; j < SNT; ++j) dmma884(ci[i][j], a[i].x, b[j].y);
+          for (int j = 0; j < SNT; ++j) dmma884(cr[i][j], a[i].x, b[j].x);
 #pragma unroll
-      for (int i = 0; i < SMT; ++i) {
-        const double nai = -a[i].y;
+        for (int i = 0; i < SMT; ++i)
 #pragma unroll
-        for (int j = 0; j < SNT; ++j) dmma884(cr[i][j], nai, b[j].y);
+          for (int j = 0; j < SNT; ++j) dmma884(ci[i][j], a[i].y, b[j].y);
+#pragma unroll
+        for (int i = 0; i < SMT; ++i)
+#pragma unroll
+          for (int j = 0; j < SNT; ++j) dmma884(cs[i][j], sa[i], sb[j]);
+      } else {
+        // four passes over the sub-tiles, so that the two MMAs into one accumulator are
+        // 2*SMT*SNT instructions apart (DMMA latency hidden by independent accumulators)
+#pragma unroll
+        for (int i = 0; i < SMT; ++i)
+#pragma unroll
+          for (int j = 0; j < SNT; ++j) dmma884(cr[i][j], a[i].x, b[j].x);
+#pragma unroll
+        for (int i = 0; i < SMT; ++i)
+#pragma unroll
+          for (int j = 0; j < SNT; ++j) dmma884(ci[i][j], a[i].x, b[j].y);
+#pragma unroll
+        for (int i = 0; i < SMT; ++i) {
+          const double nai = -a[i].y;
+#pragma unroll
+          for (int j = 0; j < SNT; ++j) dmma884(cr[i][j], nai, b[j].y);
+        }
+#pragma unroll
+        for (int i = 0; i < SMT; ++i)
+#pragma unroll
+          for (int j = 0; j < SNT; ++j) dmma884(ci[i][j], a[i].y, b[j].x);
       }
-#pragma unroll
-      for (int i = 0; i < SMT; ++i)
-#pragma unroll
-        for (int j = 0; j < SNT; ++j) dmma884(ci[i][j], a[i].y, b[j].x);
     }
     if (w % nk != nk - 1) {
       __syncthreads();  // this stage is refilled by the prefetch two items later
@@ -201,9 +231,14 @@ __global__ void __launch_bounds__(256) gett_dmma_kernel(const __grid_constant__ 
 #pragma unroll
       for (int j = 0; j < SNT; ++j) {
         const int n = wn * 8 * SNT + 8 * j + 2 * t4;
-        row[n] = make_double2(cr[i][j][0], ci[i][j][0]);
-        row[n + 1] = make_double2(cr[i][j][1], ci[i][j][1]);
-        cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+        if (GAUSS) {
+          row[n] = make_double2(cr[i][j][0] - ci[i][j][0], cs[i][j][0] - cr[i][j][0] - ci[i][j][0]);
+          row[n + 1] = make_double2(cr[i][j][1] - ci[i][j][1], cs[i][j][1] - cr[i][j][1] - ci[i][j][1]);
+        } else {
+          row[n] = make_double2(cr[i][j][0], ci[i][j][0]);
+          row[n + 1] = make_double2(cr[i][j][1], ci[i][j][1]);
+        }
+        cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = cs[i][j][0] = cs[i][j][1] = 0.0;
       }
     }
     __syncthreads();

@@ -379,28 +379,32 @@ def test_c5_benched_slice_k3g_vs_k2(jet, monkeypatch):
     assert rel < 1e-4
 
 
-def test_k2s_and_k3_tma_grid_parity(jet, monkeypatch):
-    """K2s (TMA-fed streaming GETT) and K3-TMA on a 4x5 m=10 grid circuit: all 16 slices
-    against the oracle (1e-4), and against the same plan with K2s off (JETB200_K2S=0) and with
-    TMA off (JETB200_K3_TMA=0: K3 cp.async gathers, skinny nodes on K2)."""
+@pytest.mark.parametrize("grid", [(4, 5), (5, 5)])
+def test_k2s_and_k3_tma_grid_parity(jet, monkeypatch, grid):
+    """K2s (register-resident streaming GETT; on the 5x5 grid also with 16-B k-pair loads) and
+    K3-TMA on an m=10 grid circuit: all 16 slices against the oracle (1e-4), and against the same
+    plan with K2s off (JETB200_K2S=0: those nodes on K2) and with TMA off (JETB200_K3_TMA=0)."""
     from circuits import grid_rqc, random_bitstring
     from oracle import contract
     from oracle.network import build_network
 
-    circ = grid_rqc(4, 5, 10, 1)
-    bits = random_bitstring(20, 2, 1)
+    r, c = grid
+    circ = grid_rqc(r, c, 10, 1)
+    bits = random_bitstring(r * c, 2, 1)
     net = jet.Network.from_circuit(circ, bits)
-    plan = jet.Plan.greedy(net, seed=1, trials=32, n_sliced=4)
+    plan = jet.Plan.greedy(net, seed=1, trials=32 if grid == (4, 5) else 16, n_sliced=4)
     ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
     out = {}
     monkeypatch.setenv("JETB200_TMA_MINCOPY", "16")   # every item on the TMA engine, however small
-    for tag, env in (("default", {"JETB200_K2S": "1"}), ("no_k2s", {"JETB200_K2S": "0"}),
-                     ("no_tma", {"JETB200_K3_TMA": "0"})):
+    for tag, env in (("default", {}), ("no_k2s", {"JETB200_K2S": "0"}), ("no_tma", {"JETB200_K3_TMA": "0"})):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         p = jet.Plan.create(net, plan.ssa_path, plan.sliced_labels)
-        kinds = [n["kind"] for n in p.describe_exec("c64")["nodes"]]
-        assert (4 in kinds) == (tag == "default")
+        nodes = p.describe_exec("c64")["nodes"]
+        kinds = [n["kind"] for n in nodes]
+        assert (4 in kinds) == (tag != "no_k2s")
+        if grid == (5, 5) and tag == "default":
+            assert any(n["st_vec"] for n in nodes if n["kind"] == 4)
         ex, _ = exec_on_stream(jet, p, "c64")
         out[tag] = block_values(jet, ex, 0, 16)
         for k in env:

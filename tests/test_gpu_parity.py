@@ -177,16 +177,21 @@ def test_gbs_parity_and_closed_forms(jet, dim, width):
 
 
 # ----------------------------------------------------------------------------- K4 (c128 DMMA)
+@pytest.mark.parametrize("form", ["3M", "4M"])
 @pytest.mark.parametrize("dim,width,d,k", [(2, 3, 4, 0), (2, 4, 4, 2), (2, 2, 8, 1), (3, 2, 4, 1), (2, 4, 4, 3)])
-def test_k4_dmma_parity_vs_oracle_and_k2(jet, monkeypatch, dim, width, d, k):
-    """c128 contractions on the FP64 tensor cores (K4) against the oracle (1e-10) and against
-    the CUDA-core K2 path (JETB200_DMMA=0) on the same plan."""
+def test_k4_dmma_parity_vs_oracle_and_k2(jet, monkeypatch, dim, width, d, k, form):
+    """c128 contractions on the FP64 tensor cores (K4: the 4M form by default and the 3M Gauss
+    form with JETB200_K4_3M=1) against the oracle (1e-10) and against the CUDA-core K2 path
+    (JETB200_DMMA=0) on the same plan."""
+    monkeypatch.setenv("JETB200_K4_3M", "1" if form == "3M" else "0")
     circ = generate_gbs(dim, width, 1, 0.5, d, seed=5)
     M = circ.n_wires
     bits = random_bitstring(M, d, 11)
     net = jet.Network.from_circuit(circ, bits)
     plan = jet.Plan.greedy(net, seed=1, trials=16, n_sliced=k)
-    assert any(n["kind"] == 3 for n in plan.describe_exec("c128")["nodes"])
+    k4 = [n for n in plan.describe_exec("c128")["nodes"] if n["kind"] == 3]
+    assert k4
+    assert any(n["gauss"] for n in k4) == (form == "3M")
     ref_vals = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels))
     ref = complex(np.sum(ref_vals))
     amp, vals, _ = run(jet, plan, "c128")
