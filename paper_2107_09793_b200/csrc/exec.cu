@@ -286,6 +286,10 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   // one grid sized for one per SM co-resided through shared memory, the second blocking in
   // tcgen05.alloc until the first finished: +2.2 s per C3 amplitude under PDL.)
   int acc_bufs = (2 * Np + 2 * 2 * Kpc <= 512) ? 2 : 1;
+  // JETB200_K3_ACC=4: four accumulators when MMA N <= 16 (one-chunk tiles of tm = 3: the MMA can
+  // run up to four tiles ahead of the epilogue)
+  if (const char* e = std::getenv("JETB200_K3_ACC"))
+    if (atoi(e) == 4 && Np <= 16) acc_bufs = 4;
   int ctas = 2;  // JETB200_K3_CTAS: 1 forces one CTA per SM (deeper raw ring)
   if (const char* e = std::getenv("JETB200_K3_CTAS")) ctas = std::max(1, std::min(2, atoi(e)));
   const bool two = ctas == 2 && acc_bufs * Np + 2 * 2 * Kpc <= 256;
@@ -569,11 +573,12 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   if (const char* e = getenv("JETB200_TCG_YS")) ystages = std::max(2, std::min(4, atoi(e)));
   const int rb_b = 128 * 128, rb_a = MT * 128;
   int64_t ybytes = (int64_t)ystages * 2 * NP * 128;
-  while (ystages > 2 && (220 * 1024 - 1024 - ybytes) / (rb_b + rb_a) < 3) {
+  while (ystages > 2 && (220 * 1024 - 1024 - 16384 - ybytes) / (rb_b + rb_a) < 3) {
     --ystages;
     ybytes = (int64_t)ystages * 2 * NP * 128;
   }
-  const int rstages = (int)std::min<int64_t>(6, (220 * 1024 - 1024 - ybytes) / (rb_b + rb_a));
+  const int64_t ebytes = 16384;  // epilogue staging: two 8-KB buffers (8 complex columns x 128 rows)
+  const int rstages = (int)std::min<int64_t>(6, (220 * 1024 - 1024 - ybytes - ebytes) / (rb_b + rb_a));
   if (rstages < 2) return false;
   TcgArgs& t = en.tcg;
   std::memset(&t, 0, sizeof(t));
@@ -660,7 +665,7 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   for (auto b : oN) en.tcgB_oN.push_back(sb[b]);
   for (auto b : oM) en.tcgA_oM.push_back(sa[b]);
   en.kind = 2;
-  en.smem = (size_t)(ybytes + (int64_t)rstages * (rb_b + rb_a) + 1024);
+  en.smem = (size_t)(ybytes + (int64_t)rstages * (rb_b + rb_a) + ebytes + 1024);
   en.block = t.tma ? 448 : 416;
   en.n_out = t.n_tiles << (7 + tmt);
   en.grid_x = t.n_tiles;

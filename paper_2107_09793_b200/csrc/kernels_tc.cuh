@@ -44,7 +44,8 @@ struct TcArgs {
   int32_t xstages;                             // TMEM X stages (hi|lo, 2*Kpc columns each)
   int32_t rstages;                             // raw shared landing stages (cp.async depth rstages-1)
   int32_t rbytes;                              // bytes of one raw stage (128 rows x 8*2^tkc)
-  int32_t acc_bufs;                            // TMEM accumulators (2: epilogue overlaps next tile)
+  int32_t acc_bufs;                            // TMEM accumulators (1, 2 or 4; > 1: epilogue overlaps
+                                               // the next tiles)
   int64_t o_sB[kMaxOuter];                     // outer (row) bit j of B: stride
   int64_t o_kB[4];                             // chunk-index bit j of B: stride
   int64_t gX[kTcMaxTile];                      // B chunk-tile bit j (stride order): global stride
@@ -181,6 +182,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// Bulk (TMA-engine) shared -> global copy / element-wise FP32 add-reduction of `bytes` (16-B
+// aligned, a multiple of 16), tracked by the issuing thread's bulk async-group.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_add_f32(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+
 }  // namespace tc
 
 // Byte offset of A-operand element (row r, tf32 column kk) inside one X buffer / Y plane.
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
   __shared__ int64_t tg[2][64];
   __shared__ int32_t ts[2][64];
   __shared__ int64_t kc_off[16];  // B offset of K chunk c (n_kc <= 16)
-  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[2], tempty[2], rfull[16], rempty[16];
+  __shared__ __align__(8) uint64_t xfull[4], xempty[4], tfull[4], tempty[4], rfull[16], rempty[16];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < 16) {
@@ -249,7 +267,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
       tc::mbar_init(&xfull[i], 256);
       tc::mbar_init(&xempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 128);
     }
@@ -482,8 +500,10 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
     int xs = 0, c = 0;
     uint32_t xph = 0;
     for (int64_t it = 0; it < items; ++it) {
-      const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
-      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
+      // accumulator b = tt mod acc_bufs (1, 2 or 4), its use count tt / acc_bufs -> phase
+      const int lgb = p.acc_bufs >> 1;  // log2(acc_bufs) for 1, 2, 4
+      const int b = (int)(tt & (p.acc_bufs - 1));
+      const uint32_t tph = (uint32_t)((tt >> lgb) & 1);
       if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);  // accumulator drained (first use passes)
       tc::mbar_wait(&xfull[xs], xph);
       tc::fence_after();
@@ -512,8 +532,10 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
     const int row = warp * 32 + lane;
     const int nm = 1 << p.tm;
     for (int64_t tt = 0; tt < my_tiles; ++tt) {
-      const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
-      const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
+      // accumulator b = tt mod acc_bufs (1, 2 or 4), its use count tt / acc_bufs -> phase
+      const int lgb = p.acc_bufs >> 1;  // log2(acc_bufs) for 1, 2, 4
+      const int b = (int)(tt & (p.acc_bufs - 1));
+      const uint32_t tph = (uint32_t)((tt >> lgb) & 1);
       tc::mbar_wait(&tfull[b], tph);
       tc::fence_after();
       const int64_t t = (int64_t)blockIdx.x + tt * gridDim.x;
