@@ -177,8 +177,12 @@ void set_smem_attrs() {
   std::lock_guard<std::mutex> lk(mu);
   if ((int)done.size() <= dev) done.resize(dev + 1, 0);
   if (done[dev]) return;
+  // the largest shared-memory carveout: without it the occupancy calculator assumes the default
+  // carveout and reported ONE K3 CTA per SM for the 52-108 KB K3 CTAs that are sized to run two
+  // per SM (measured: every C3 K3 launch had 148 CTAs, sm__warps_active 21.9% = 14 of 64 warps)
   auto set = [](const void* f, int bytes) {
     JT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    JT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
   };
   const int rms[3] = {1, 2, 4};
   for (int a : rms)
@@ -290,7 +294,12 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   // run up to four tiles ahead of the epilogue)
   if (const char* e = std::getenv("JETB200_K3_ACC"))
     if (atoi(e) == 4 && Np <= 16) acc_bufs = 4;
-  int ctas = 2;  // JETB200_K3_CTAS: 1 forces one CTA per SM (deeper raw ring)
+  // CTAs per SM: two (each half the TMEM and shared memory) when the per-item MMA work is large
+  // against the item's bytes -- N <= 16 tiles (tm = 3) or tiles of several K chunks -- else one
+  // with the deeper rings.  Measured per node on C3 (profiles/r02_nodes_C3_ctas.txt): tm = 3 nodes
+  // 0.65-0.76 -> 0.86-0.93 of HBM with two CTAs, tm = 4 single-chunk nodes 0.99 -> 0.89.
+  // JETB200_K3_CTAS=1/2 forces the count.
+  int ctas = (Np <= 16 || n_kc >= 2) ? 2 : 1;
   if (const char* e = std::getenv("JETB200_K3_CTAS")) ctas = std::max(1, std::min(2, atoi(e)));
   const bool two = ctas == 2 && acc_bufs * Np + 2 * 2 * Kpc <= 256;
   const int cols_budget = two ? 256 : 512;
@@ -330,6 +339,9 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   t.xstages = xstages;
   t.rstages = rstages;
   t.rbytes = rbytes;
+  t.passes = 3;
+  if (const char* e = std::getenv("JETB200_DEBUG_K3_PASSES"))  // diagnostic only: MMA-count sweep
+    if (e[0] == '1') t.passes = 1;
   t.acc_bufs = acc_bufs;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t cols = 32;
@@ -1636,9 +1648,30 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     if (en.kind == 1) {
       JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &nb, reinterpret_cast<const void*>(pick_tc(en.tc.tkc, en.tc.tma != 0)), en.block, en.smem));
+      const int nb_occ = nb;
+      // The occupancy calculator reports 1 CTA per SM for the tcgen05 kernels whatever their
+      // shared memory and block size (it assumes the whole TMEM per CTA); K3's shared-memory
+      // footprint is sized so that exactly 512 / tmem_cols CTAs fit (plan_tc), so that count is
+      // used (JETB200_K3_OCC=api keeps the calculator's answer).
+      {
+        const char* e = std::getenv("JETB200_K3_OCC");
+        if (!(e && std::string(e) == "api")) nb = 512 / (int)en.tc.tmem_cols;
+      }
       nb = std::min<int>(nb, 512 / (int)en.tc.tmem_cols);  // TMEM columns per SM
       if (nb < 1) fail(JT_EINTERNAL, "exec: a K3 tile does not fit on an SM");
       en.grid_x = std::min<int64_t>(en.tc.n_tiles, (int64_t)nb * n_sm);
+      if (std::getenv("JETB200_DEBUG_GRID")) {
+        cudaFuncAttributes fa{};
+        const void* f = reinterpret_cast<const void*>(pick_tc(en.tc.tkc, en.tc.tma != 0));
+        JT_CUDA(cudaFuncGetAttributes(&fa, f));
+        int o0 = 0, o1 = 0;
+        JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, f, en.block, 0));
+        JT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, f, 128, 0));
+        std::fprintf(stderr, "K3 node %lld: smem %zu block %d occupancy %d tmem_cols %u -> %d CTAs/SM, grid %lld | "
+                     "regs %d static smem %zu max dyn %d maxthr %d | occ(smem 0) %d occ(128 thr) %d\n",
+                     (long long)en.v, en.smem, en.block, nb_occ, en.tc.tmem_cols, nb, (long long)en.grid_x, fa.numRegs,
+                     fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock, o0, o1);
+      }
       continue;
     }
     const void* fn = en.kind == 3   ? reinterpret_cast<const void*>(pick_dmma(en.RM, en.RN, en.args.gauss != 0))

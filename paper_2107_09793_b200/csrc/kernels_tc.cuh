@@ -56,6 +56,8 @@ struct TcArgs {
                                                //    -> gather k-pairs as 16-B copies
   int32_t tma;                                 // 1: items arrive by TMA bulk copies (gett_tc_kernel<TKC, true>)
   int32_t mlow;                                // output layout [M bits][7 row bits][outer] (else [rows][M][outer])
+  int32_t passes;                              // MMA products per K step: 3 (3xTF32); 1 only for the
+                                               // JETB200_DEBUG_K3_PASSES=1 diagnostic (hi*hi, wrong digits)
   int32_t ncopy, copy_bytes;                   // bulk copies per item (the stride-1 run each) and their size
   int64_t xoff[32];                            //   ... copy j reads at item base + xoff[j], lands at j * copy_bytes
   int32_t rofs_row[7], rofs_k[5];              // TMA landing: byte offset of row bit i / chunk K bit j
@@ -516,8 +518,10 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
           const uint64_t dyh = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
           const uint64_t dyl = tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout);
           tc::mma_tf32_ts(d, xh + ks * 8, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
-          tc::mma_tf32_ts(d, xh + ks * 8, dyl, p.idesc, 1u);
-          tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
+          if (p.passes == 3) {
+            tc::mma_tf32_ts(d, xh + ks * 8, dyl, p.idesc, 1u);
+            tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
+          }
         }
         tc::mma_commit(&xempty[xs]);                     // TMEM X stage free once these finish
         if (c == p.n_kc - 1) tc::mma_commit(&tfull[b]);  // tile accumulated

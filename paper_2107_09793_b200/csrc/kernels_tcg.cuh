@@ -9,10 +9,10 @@
 //   into raw shared rings, then split B into hi/lo TF32 in TMEM (the MMA's A operand) and expand
 //   A into the Y operand [[Re,-Im],[Im,Re]] hi/lo in shared memory (SWIZZLE_128B, K-major)
 //   MMA warp: 4 K steps x 3 (hi*hi, hi*lo, lo*hi) tcgen05.mma kind::tf32 per item
-//   epilogue warps: TMEM accumulator -> shared staging (8 complex columns x 128 rows, two
-//   buffers) -> TMA-engine bulk stores of 8-KB runs of the output tile; the later accumulation
-//   segments of a tile are added by bulk FP32 add-reductions (cp.reduce.async.bulk .add.f32), in
-//   segment order (the issuing thread waits for the previous segment's group before the next)
+//   epilogue warps: TMEM accumulator -> 256-B coalesced stores of the complex output tile (first
+//   accumulation segment); later segments -> shared staging (8 complex columns x 128 rows, two
+//   buffers) -> TMA-engine bulk FP32 add-reductions (cp.reduce.async.bulk .add.f32) of 8-KB runs,
+//   in segment order (the issuing thread waits for the previous segment's group before the next)
 #pragma once
 
 #include "kernels_tc.cuh"
@@ -456,14 +456,16 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
     }
   } else if (warp < 4) {
     // ===================== epilogue =====================
-    // one accumulator drain per K segment of 2^lg_kcs chunks, in chunks of 8 complex columns:
-    // tcgen05.ld -> shared staging [8 columns][128 rows] -> one 8-KB bulk store (first segment of
-    // a tile) or bulk FP32 add-reduction (later segments) by thread 0.  Before a tile's later
-    // segment starts, thread 0 waits for every earlier bulk group to complete (the adds into one
-    // output element happen in segment order: FP32 sums identical to a read-modify-write).
+    // one accumulator drain per K segment of 2^lg_kcs chunks.  The first segment of a tile is
+    // stored directly (tcgen05.ld -> 256-B coalesced stores, then a generic->async proxy fence);
+    // each later segment goes through shared staging ([8 columns][128 rows], two buffers) and is
+    // added by thread 0 with 8-KB bulk FP32 add-reductions (cp.reduce.async.bulk .add.f32) -- no
+    // read-modify-write round trip.  Before a later segment, thread 0 waits for every earlier
+    // bulk group to complete, so the adds into one element happen in segment order (the same
+    // FP32 sums as a read-modify-write).
     const int row = warp * 32 + lane;
     const int lg_seg = p.lg_kc - p.lg_kcs;
-    int q = 0;  // chunk counter (staging buffer q & 1)
+    int q = 0;  // staged chunk counter (staging buffer q & 1)
     for (int64_t st = 0; st < (my_tiles << lg_seg); ++st) {
       const int64_t tt = st >> lg_seg;
       const bool first = (st & (((int64_t)1 << lg_seg) - 1)) == 0;
@@ -471,18 +473,32 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((st >> 1) & 1) : (uint32_t)(st & 1);
       tc::mbar_wait(&tfull[b], tph);
       tc::fence_after();
-      if (!first && tid == 0) tc::bulk_wait<0>();  // earlier segments' adds complete
       const int64_t t = tcg::raster((int64_t)blockIdx.x + tt * gridDim.x, p);
       float2* out = p.C + (t << (7 + TMT));
+      const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * NP);
+      if (first) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < NP; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(tbase + (uint32_t)c0, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) out[row + ((int64_t)(c0 / 2 + j) << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+        }
+        tc::fence_before();
+        tc::mbar_arrive(&tempty[b]);
+        if (lg_seg > 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // stores before the bulk adds
+        continue;
+      }
+      if (tid == 0) tc::bulk_wait<0>();  // earlier segments' adds complete
       float v[16];
-      tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * NP), v);
+      tc::tmem_ld16(tbase, v);
 #pragma unroll 1
       for (int c0 = 0; c0 < NP; c0 += 16, ++q) {
         float2* sb = ES + (q & 1) * 1024;
         tc::bar_sync(2, 128);  // staging buffer q & 1 free (thread 0 waited for its last read)
 #pragma unroll
         for (int j = 0; j < 8; ++j) sb[j * 128 + row] = make_float2(v[2 * j], v[2 * j + 1]);
-        if (c0 + 16 < NP) tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * NP + c0 + 16), v);
+        if (c0 + 16 < NP) tc::tmem_ld16(tbase + (uint32_t)(c0 + 16), v);
         else {
           tc::fence_before();
           tc::mbar_arrive(&tempty[b]);  // accumulator drained into registers / staging
@@ -490,9 +506,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
         tc::fence_proxy_async();
         tc::bar_sync(2, 128);  // staging written
         if (tid == 0) {
-          float2* dst = out + ((int64_t)(c0 / 2) << 7);
-          if (first) tc::bulk_s2g(dst, sb, 8192);
-          else tc::bulk_s2g_add_f32(dst, sb, 8192);
+          tc::bulk_s2g_add_f32(out + ((int64_t)(c0 / 2) << 7), sb, 8192);
           tc::bulk_commit();
           tc::bulk_wait_read<1>();  // the group before (the other buffer) has been read
         }

@@ -1,6 +1,7 @@
 """Small GPU workload for compute-sanitizer (memcheck / racecheck / synccheck): one C2 slice on
-the default path (K3 TMA + K2), the same slice with K3g forced and with the cp.async K3, one
-c128 GBS slice on K4 (DMMA), and a K1 permute; each checked against the oracle.
+the default path (K3 TMA + K2), the same slice with K3g forced and with the cp.async K3, a 5x5
+grid slice on K2s + K3 (and K3 with four accumulators), one c128 GBS slice on K4 (DMMA), and a
+K1 permute; each checked against the oracle.
 
   compute-sanitizer --tool racecheck python scripts/sanitize_case.py
 """
@@ -37,11 +38,26 @@ def main():
     kinds = [(n["kind"], n.get("tma", 0)) for n in plan.describe_exec("c64")["nodes"]]
     assert (1, 1) in kinds
     one(plan, "c64", 3, ref, 1e-4, "C2 K3-TMA + K2")
-    for env, tag in (("JETB200_TCG_FORCE", "C2 K3g"), ("JETB200_K3_TMA", "C2 K3 cp.async")):
-        os.environ[env] = "1" if env == "JETB200_TCG_FORCE" else "0"
+    for envs, tag in (({"JETB200_TCG_FORCE": "1"}, "C2 K3g"),
+                      ({"JETB200_TCG_FORCE": "1", "JETB200_TCG_SEG": "0"}, "C2 K3g, one segment per chunk (bulk adds)"),
+                      ({"JETB200_K3_TMA": "0"}, "C2 K3 cp.async")):
+        os.environ.update(envs)
         p = jet.Plan.create(net, plan.ssa_path, plan.sliced_labels)
         one(p, "c64", 3, ref, 1e-4, tag)
-        del os.environ[env]
+        for k in envs:
+            del os.environ[k]
+    # K2s (register-resident streaming GETT, with and without 16-B k-pair loads) on a 5x5 grid
+    from circuits import grid_rqc
+    gc = grid_rqc(5, 5, 10, 1)
+    gcb = random_bitstring(25, 2, 1)
+    gcn = jet.Network.from_circuit(gc, gcb)
+    gcp = jet.Plan.greedy(gcn, seed=1, trials=16, n_sliced=4)
+    assert any(n["kind"] == 4 and n["st_vec"] for n in gcp.describe_exec("c64")["nodes"])
+    gcref = contract.slice_values(build_network(gc, gcb), gcp.ssa_path, gcp.sliced_labels, indices=[5])[0]
+    one(gcp, "c64", 5, gcref, 1e-4, "grid K2s + K3")
+    os.environ["JETB200_K3_ACC"] = "4"
+    one(jet.Plan.create(gcn, gcp.ssa_path, gcp.sliced_labels), "c64", 5, gcref, 1e-4, "grid K3 4 accumulators")
+    del os.environ["JETB200_K3_ACC"]
     g = generate_gbs(2, 4, 1, 0.5, 4, seed=5)
     gb = random_bitstring(g.n_wires, 4, 12)
     gnet = jet.Network.from_circuit(g, gb)
