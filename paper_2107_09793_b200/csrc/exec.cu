@@ -52,6 +52,12 @@ struct ExecNode {
   TcgArgs tcg{};
   std::vector<int64_t> tcgA_m, tcgA_k, tcgB_oN, tcgA_oM;  // K3g host strides (emulator)
   std::vector<int64_t> tcB_n, tcB_k;  // K3: B strides of the 7 row bits and the K bits (emulator)
+  // K3g fed by a K1 bit-gather: the operand is first copied into the K3g layout (item bits
+  // lowest); gA/gB = the source strides of the copy's bits (bit j of the copy <- stride), the
+  // copies live in the scratch region at perm_off (B) and perm_off + permA_at (A)
+  bool permA = false, permB = false;
+  GatherArgs gA{}, gB{};
+  int64_t perm_bytes = 0, permA_at = 0, perm_off = 0;
   int64_t v = -1;
   int64_t opA = -1, opB = -1;  // plan node ids (A has the fewer free bits)
   std::vector<std::pair<int, int64_t>> sliceA, sliceB;  // (slice position, element stride) for leaves
@@ -578,6 +584,75 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   for (auto& k : K)
     if (std::find(kc.begin(), kc.end(), k.second) == kc.end()) ko.push_back(k.second);
   if (oN.size() + oM.size() > 31 || ko.size() > 32 || oN.size() > 32 || oM.size() > 32) return false;
+  // K1-fed operands (default; JETB200_TCG_PERM=0 keeps the gathers): an operand whose chunk is
+  // not a few long runs of its own layout is bit-gathered into the K3g layout first -- B as
+  // [7 rows][4 chunk K][chunk-index K][outer N], A as [4 chunk K][tmt M][chunk-index K][outer M]
+  // -- so each item is ONE contiguous TMA-engine copy (the copy costs 16 B per element, against
+  // thousands of FLOP per element on these GEMM-shaped nodes)
+  en.permA = en.permB = false;
+  if (tma_enabled()) {
+    const std::map<int64_t, int64_t> sb0 = sb, sa0 = sa;
+    const char* e = getenv("JETB200_TCG_PERM");
+    const bool allow = !(e && e[0] == '0');
+    const bool force = e && std::string(e) == "force";  // tests: copy whenever an item is not one box
+    auto item_ok = [&](const std::vector<int64_t>& strides, const std::vector<std::pair<int, int64_t>>& sl) {
+      for (auto& x : sl)
+        if (x.second % 2) return false;
+      std::vector<int> r;
+      int nc = 0, cl = 0;
+      return tma_item_dims(strides, &nc, &cl, nullptr, r);
+    };
+    std::vector<int64_t> ib, ia;
+    for (auto b : tN) ib.push_back(sb[b]);
+    for (auto b : kc) ib.push_back(sb[b]);
+    for (auto b : tM) ia.push_back(sa[b]);
+    for (auto b : kc) ia.push_back(sa[b]);
+    // only where the copy is cheap against the node: each B element meets 2^|M| columns of A, so
+    // the copy's 16 B per element is <= ~10% of the MMA time at |M| >= 9 (likewise A with |N|)
+    if (allow && (M.size() >= 9 || force) && !item_ok(ib, en.sliceB)) {
+      std::vector<int64_t> order(tN.begin(), tN.end());
+      order.insert(order.end(), kc.begin(), kc.end());
+      order.insert(order.end(), ko.begin(), ko.end());
+      order.insert(order.end(), oN.begin(), oN.end());
+      if (order.size() == vb.bits.size() && order.size() <= 40) {
+        en.permB = true;
+        en.gB = GatherArgs{};
+        en.gB.n_bits = (int)order.size();
+        en.gB.is_a = 0;
+        for (size_t j = 0; j < order.size(); ++j) {
+          en.gB.s[j] = sb[order[j]];
+          sb[order[j]] = int64_t(1) << j;
+        }
+      }
+    }
+    if (allow && (N.size() >= 9 || force) && !item_ok(ia, en.sliceA)) {
+      std::vector<int64_t> order(kc.begin(), kc.end());
+      order.insert(order.end(), tM.begin(), tM.end());
+      order.insert(order.end(), ko.begin(), ko.end());
+      order.insert(order.end(), oM.begin(), oM.end());
+      if (order.size() == va.bits.size() && order.size() <= 40) {
+        en.permA = true;
+        en.gA = GatherArgs{};
+        en.gA.n_bits = (int)order.size();
+        en.gA.is_a = 1;
+        for (size_t j = 0; j < order.size(); ++j) {
+          en.gA.s[j] = sa[order[j]];
+          sa[order[j]] = int64_t(1) << j;
+        }
+      }
+    }
+    // a copy pays only if it makes BOTH operands TMA-fed: otherwise the gather path runs anyway
+    const bool okB = en.permB || item_ok(ib, en.sliceB), okA = en.permA || item_ok(ia, en.sliceA);
+    if (!(okA && okB) && !force) {
+      sb = sb0;
+      sa = sa0;
+      en.permA = en.permB = false;
+    }
+    const int64_t bB = en.permB ? align_up((int64_t(8) << en.gB.n_bits)) : 0;
+    const int64_t bA = en.permA ? align_up((int64_t(8) << en.gA.n_bits)) : 0;
+    en.permA_at = bB;
+    en.perm_bytes = bA + bB;
+  }
   // Y (expanded A, hi|lo planes) ring depth: the producers run ystages-1 items ahead of the MMAs
   // (2, 3 and 4 measured within 3% of each other on the C5 nodes: not the bound; 2 keeps the
   // deepest raw gather ring)
@@ -653,8 +728,10 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
     std::vector<int> rb_, ra_;
     int nb = 0, na = 0, cb = 0, ca = 0;
     bool even = true;
-    for (auto& x : en.sliceB) even &= (x.second % 2) == 0;
-    for (auto& x : en.sliceA) even &= (x.second % 2) == 0;
+    if (!en.permB)
+      for (auto& x : en.sliceB) even &= (x.second % 2) == 0;
+    if (!en.permA)
+      for (auto& x : en.sliceA) even &= (x.second % 2) == 0;
     t.tma = (tma_enabled() && even && tma_item_dims(ib, &nb, &cb, t.xoffB, rb_) &&
              tma_item_dims(ia, &na, &ca, t.xoffA, ra_)) ? 1 : 0;
     if (t.tma) {
@@ -1215,8 +1292,10 @@ Layout compile(const jt_plan& plan, int esize) {
   int64_t scratch = 0;
   for (ExecNode& en : L.order) {
     if (en.args.splits > 1) scratch = std::max(scratch, align_up(en.n_out * esize * en.args.splits));
+    scratch = std::max(scratch, en.perm_bytes);  // K1-fed K3g operand copies (used within the node)
     en.out_off = L.node_off[en.v];
     en.part_off = L.scratch_base;
+    en.perm_off = L.scratch_base;
   }
   L.scratch_bytes = scratch;
   L.vals_base = align_up(L.scratch_base + L.scratch_bytes);
@@ -1398,6 +1477,18 @@ void emulate_tc(const TcArgs& p, const ExecNode& en, char* ws, const std::vector
 void emulate_tcg(const TcgArgs& p, const ExecNode& en, char* ws, const std::vector<std::pair<int64_t, int64_t>>& off) {
   const float2* A = reinterpret_cast<const float2*>(ws + off[0].first) + off[0].second;
   const float2* B = reinterpret_cast<const float2*>(ws + off[1].first) + off[1].second;
+  // K1-fed operands: the bit-gather into the K3g layout (dst bit j <- source stride s[j])
+  std::vector<float2> pa, pb;
+  auto gather = [](const float2* src, const GatherArgs& g, std::vector<float2>& dst) {
+    dst.resize(size_t(1) << g.n_bits);
+    for (size_t i = 0; i < dst.size(); ++i) {
+      int64_t o = 0;
+      for (int j = 0; j < g.n_bits; ++j) if ((i >> j) & 1) o += g.s[j];
+      dst[i] = src[o];
+    }
+  };
+  if (en.permB) { gather(B, en.gB, pb); B = pb.data(); }
+  if (en.permA) { gather(A, en.gA, pa); A = pa.data(); }
   float2* C = reinterpret_cast<float2*>(ws + off[2].first);
   const int MT = 1 << p.tmt;
   const int64_t nk = int64_t(1) << (int)en.tcB_k.size();
@@ -1579,7 +1670,8 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
       std::fprintf(f, "], \"ncopy\": %d, \"copy_bytes\": %d, \"rofs_row\": [%d, %d, %d, %d, %d, %d, %d]", en.kind == 1 ? en.tc.ncopy : en.tcg.ncopyB,
                    en.kind == 1 ? en.tc.copy_bytes : en.tcg.copyB_bytes, en.tc.rofs_row[0], en.tc.rofs_row[1],
                    en.tc.rofs_row[2], en.tc.rofs_row[3], en.tc.rofs_row[4], en.tc.rofs_row[5], en.tc.rofs_row[6]);
-      std::fprintf(f, ", \"tkc\": %d, \"tma\": %d", en.kind == 1 ? en.tc.tkc : 4, en.kind == 1 ? en.tc.tma : en.tcg.tma);
+      std::fprintf(f, ", \"tkc\": %d, \"tma\": %d, \"permA\": %d, \"permB\": %d", en.kind == 1 ? en.tc.tkc : 4,
+                   en.kind == 1 ? en.tc.tma : en.tcg.tma, en.permA ? 1 : 0, en.permB ? 1 : 0);
     }
     if (en.kind == 4) {
       std::fprintf(f, ", \"st_vec\": %d, \"st_n_lo\": %d, \"st_cols\": %d, \"stN\": [", en.st.vec, en.st.n_lo, en.st.n_cols);
@@ -1710,6 +1802,10 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     en.st.sv = sv;
     en.tc.sv = sv;
     en.tcg.sv = sv;
+    en.gA.sv = sv;
+    en.gB.sv = sv;
+    if (en.permA) en.tcg.sv.nA = 0;  // the K1 copy already holds the slice
+    if (en.permB) en.tcg.sv.nB = 0;
   }
   ex->dtype = dt;
   ex->device = device;
@@ -1794,7 +1890,21 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.A = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opA]);
     t.B = reinterpret_cast<const float2*>(ex->ws + L.node_off[en.opB]);
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
-    ev_begin(ex);
+    ev_begin(ex);  // the node's time includes its K1 copies
+    if (en.permB) {
+      en.gB.src = t.B;
+      en.gB.dst = reinterpret_cast<float2*>(ex->ws + en.perm_off);
+      launch_pdl(view_gather_kernel, dim3(148 * 8), dim3(256), 0, ex->stream, ex->pdl, en.gB);
+      st.kernel_launches++;
+      t.B = en.gB.dst;
+    }
+    if (en.permA) {
+      en.gA.src = t.A;
+      en.gA.dst = reinterpret_cast<float2*>(ex->ws + en.perm_off + en.permA_at);
+      launch_pdl(view_gather_kernel, dim3(148 * 8), dim3(256), 0, ex->stream, ex->pdl, en.gA);
+      st.kernel_launches++;
+      t.A = en.gA.dst;
+    }
     launch_pdl(pick_tcg(t.tmt, t.tma != 0), dim3((unsigned)en.grid_x), dim3(en.block), en.smem, ex->stream, ex->pdl, t);
     ev_end(ex, en);
     st.kernel_launches++;

@@ -46,6 +46,39 @@ struct TcgArgs {
   SliceView sv;
 };
 
+// K1 on the K3g path (the paper's transpose before the GEMM): an operand whose
+// tile / chunk bits do not form a few long runs in its own layout is first copied into the
+// layout K3g wants (item bits lowest, one contiguous run per item) by this bit-gather:
+// dst[i] = src[slice offset + sum_j bit_j(i) * s[j]] for i < 2^n_bits.  Used only for the
+// compute-bound K3g nodes, where the copy's 16 B/element is negligible against the MMA time.
+struct GatherArgs {
+  const float2* src;
+  float2* dst;
+  int32_t n_bits, is_a;
+  int64_t s[40];
+  SliceView sv;
+};
+
+__global__ void __launch_bounds__(256) view_gather_kernel(const __grid_constant__ GatherArgs p) {
+  __shared__ int64_t tab[5][256];
+  for (int i = threadIdx.x; i < 5 * 256; i += blockDim.x) {
+    const int h = i >> 8, v = i & 255;
+    int64_t o = 0;
+    for (int b = 0; b < 8; ++b)
+      if (((v >> b) & 1) && 8 * h + b < p.n_bits) o += p.s[8 * h + b];
+    tab[h][v] = o;
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  const float2* __restrict__ src = p.src + slice_off(p.sv, p.is_a != 0);
+  const int64_t n = int64_t(1) << p.n_bits, stride = (int64_t)gridDim.x * blockDim.x;
+#pragma unroll 4
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    p.dst[i] = __ldg(src + tab[0][i & 255] + tab[1][(i >> 8) & 255] + tab[2][(i >> 16) & 255] +
+                     tab[3][(i >> 24) & 255] + tab[4][(i >> 32) & 255]);
+}
+
 namespace tcg {
 // sum over the set bits j < n of v of stride[j], computed lane-parallel and butterfly-reduced
 __device__ __forceinline__ int64_t bits_sum(int64_t v, int n, const int64_t* stride, int lane) {

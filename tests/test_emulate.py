@@ -127,6 +127,23 @@ def test_emulated_k3g_matches_oracle_c2_slice(jet, monkeypatch):
     assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4
 
 
+def test_emulated_k1_fed_k3g_matches_oracle_c2_slice(jet, monkeypatch):
+    """K3g fed by K1 bit-gathers (JETB200_TCG_PERM=force: every K3g operand whose chunk is not
+    one TMA box is first copied into the K3g layout): the emulated gathers, the single-box TMA
+    landings and the contraction against the oracle on a C2 slice."""
+    monkeypatch.setenv("JETB200_TCG_FORCE", "1")
+    monkeypatch.setenv("JETB200_TCG_PERM", "force")
+    circ, bits = workload("C2")
+    net = jet.Network.from_circuit(circ, bits)
+    plan = jet.Plan.greedy(net, seed=1, trials=64, n_sliced=6, bytes_weight=5.0)
+    nodes = [n for n in plan.describe_exec("c64")["nodes"] if n["kind"] == 2]
+    assert any(n["permA"] for n in nodes) and any(n["permB"] for n in nodes)
+    assert all(n["tma"] for n in nodes if n["permA"] and n["permB"])
+    ref = np.array(contract.slice_values(build_network(circ, bits), plan.ssa_path, plan.sliced_labels, indices=[9]))
+    v = jet.debug_emulate_host(plan, 9, 10, "c64")
+    assert np.max(np.abs(v - ref) / np.abs(ref)) < 1e-4
+
+
 @pytest.mark.parametrize("dim,width,d", [(2, 3, 4), (2, 2, 8), (3, 2, 4)])
 def test_emulated_k4_descriptors_match_oracle_gbs(jet, dim, width, d):
     """K4 (c128 DMMA) shares K2's descriptor format; the emulated descriptors of plans that

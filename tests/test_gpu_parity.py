@@ -405,21 +405,27 @@ def test_c3_fsim_identity_closed_form_full_amplitude(jet):
     assert rel(amp, want) < 1e-4
 
 
-@pytest.mark.parametrize("tmt_max,mincopy,seg", [("6", "4096", "4"), ("7", "4096", "4"), ("7", "16", "4"),
-                                                 ("7", "16", "0"), ("6", "4096", "1")])
-def test_k3g_streamed_operands_parity(jet, c2_plan, monkeypatch, tmt_max, mincopy, seg):
+@pytest.mark.parametrize("tmt_max,mincopy,seg,perm", [("6", "4096", "4", "1"), ("7", "4096", "4", "1"),
+                                                      ("7", "16", "4", "1"), ("7", "16", "0", "1"),
+                                                      ("6", "4096", "1", "1"), ("7", "4096", "4", "force"),
+                                                      ("7", "4096", "0", "force")])
+def test_k3g_streamed_operands_parity(jet, c2_plan, monkeypatch, tmt_max, mincopy, seg, perm):
     """K3g (tcgen05 with both operands streamed, K in 16-complex chunks): force the C2 nodes
     K3 would take onto K3g and compare 8 slices with the oracle (tile columns up to 64 complex
     with two accumulators, or up to 128 with one; seg 0 / 1: accumulation segments of 1 / 2
-    chunks, i.e. the epilogue's bulk FP32 add-reductions of later segments)."""
+    chunks, i.e. the epilogue's bulk FP32 add-reductions of later segments; perm force: every
+    operand whose chunk is not one TMA box bit-gathered into the K3g layout first)."""
     circ, bits, net, plan = c2_plan
     monkeypatch.setenv("JETB200_TCG_FORCE", "1")
     monkeypatch.setenv("JETB200_TCG_SEG", seg)
+    monkeypatch.setenv("JETB200_TCG_PERM", perm)
     monkeypatch.setenv("JETB200_TCG_TMT", tmt_max)
     monkeypatch.setenv("JETB200_TMA_MINCOPY", mincopy)   # 16: every chunk on the TMA engine
     nodes = plan.describe_exec("c64")["nodes"]
     if mincopy == "16":
         assert any(n["kind"] == 2 and n["tma"] for n in nodes)
+    if perm == "force":
+        assert any(n["kind"] == 2 and n["permA"] and n["permB"] and n["tma"] for n in nodes)
     assert [n["kind"] for n in nodes].count(2) >= 10
     assert max(n["tc_tm"] for n in nodes if n["kind"] == 2) == int(tmt_max)
     idx = list(range(0, 64, 8))
