@@ -1,6 +1,6 @@
 """profiles/traffic.json from an ncu launch list (dram__bytes_read.sum + dram__bytes_write.sum per
 launch), per config and kernel class (K3 = gett_tc_kernel, K3G = gett_tcg_kernel, K2 = gett_kernel,
-K4 = gett_dmma_kernel)."""
+K4 = gett_dmma_kernel, K2S = stream_gett_kernel, K1G = view_gather_kernel: the K1 copies feeding K3g)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from launches import load
@@ -10,7 +10,8 @@ per, meta = load(csv_path)
 out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
 d = json.load(open(out_path)) if os.path.exists(out_path) else {}
 entry = {}
-for cls, pat in (("K3", "gett_tc_kernel"), ("K3G", "gett_tcg_kernel"), ("K2", "gett_kernel<"), ("K4", "gett_dmma")):
+for cls, pat in (("K3", "gett_tc_kernel"), ("K3G", "gett_tcg_kernel"), ("K2", "gett_kernel<"), ("K4", "gett_dmma"),
+                 ("K2S", "stream_gett_kernel"), ("K1G", "view_gather_kernel")):
     ls = [m for i, m in per.items() if pat in meta[i][0]]
     if not ls:
         continue
