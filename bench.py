@@ -235,7 +235,7 @@ def oracle_run(circ, bits, path, sliced, indices, goldens, max_slice_s):
                                f"(a complete slice did not finish within {max_slice_s:.0f} s)")}
         secs.append(sec)
         if i in goldens:
-            errs.append(abs(v - goldens[i]) / abs(goldens[i]))
+            errs.append(slice_rel_err(v, goldens[i]))
     tot = sum(secs)
     return {"value": len(indices) / tot, "complete": True, "seconds": [round(x, 2) for x in secs], "flop_sl": fl_sl,
             "golden_max_rel_diff": max(errs) if errs else None,
@@ -358,6 +358,14 @@ def measured_peaks():
         d = json.load(open(p))
         return d.get("hbm_gbs", 6650.0), "measured"
     return 6650.0, "fallback"
+
+
+def slice_rel_err(v, g):
+    """Rule A13 for one slice value: |v - g| / |g|; an oracle value that is exactly 0 -- a
+    structural zero of the GBS network (A13b, P8) -- must come out exactly 0 (error 0, else inf)."""
+    if g == 0:
+        return 0.0 if v == 0 else float("inf")
+    return abs(v - g) / abs(g)
 
 
 def profile_traffic(cfg_name, kernel):
@@ -655,7 +663,7 @@ def run_ours(args, cfg):
                 ex.invalidate()
                 got[i] = ex.contract(i, i + 1, acc, slice_values=True)[0]
         torch.cuda.synchronize()
-        errs = [abs(got[i] - goldens[i]) / abs(goldens[i]) for i in mine]
+        errs = [slice_rel_err(got[i], goldens[i]) for i in mine]
     pt = torch.tensor([max(errs) if errs else 0.0, float(len(errs))], dtype=torch.float64, device="cuda")
     if world > 1:
         pm = pt.clone()
