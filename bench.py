@@ -33,9 +33,10 @@ CONFIGS = {
     # cold at the start), so ms_per_step IS the amplitude time
     "C3": dict(circ="C3", k=10, dtype="c64", sps=1024, workload="sycamore53_m14_2^10slices"),
     # C5 / C4 (BASELINE.json): fixed slice subsets, timed and extrapolated to N_sl.  C5: a 2^12-slice
-    # subset over 8 GPUs = one step of 512 consecutive slices per GPU; C4: 2^6 slices per GPU.
+    # subset over 8 GPUs = one step of 512 consecutive slices per GPU; C4: a 2^6-slice subset over
+    # 8 GPUs = 8 slices per GPU (width 30: 16-GB complex128 intermediates, 1.9e14 FLOP per slice)
     "C5": dict(circ="C5", k=None, dtype="c64", sps=512, cap=30, seeds=2, workload="sycamore53_m20_width30_2^12subset"),
-    "C4": dict(circ="C4", k=None, dtype="c128", sps=64, cap=28, seeds=2, workload="gbs444_d4_width28_2^6subset"),
+    "C4": dict(circ="C4", k=None, dtype="c128", sps=8, cap=30, seeds=2, workload="gbs444_d4_width30_2^6subset"),
     # GBS-88-m1 at cutoff 4 (full amplitude per step) and 8 (sliced)
     "G88d4": dict(circ="G88d4", k=0, dtype="c128", sps=1, seeds=2, workload="gbs88_m1_d4_full_amplitude"),
     "G88d8": dict(circ="G88d8", k=None, dtype="c128", sps=1, cap=30, seeds=2, workload="gbs88_m1_d8_width30_subset"),

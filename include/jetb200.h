@@ -75,6 +75,11 @@ typedef struct {
      1 -> shared-work aware: the executed cost of the one-copy prefix cache,
      sum_v c(v) prod_{pos(l) <= maxpos(S(v))} d_l, with the candidate appended innermost */
   int32_t slice_objective;
+  /* trial generator ("better path"): 0 = randomised greedy only; 1 = every other
+     trial a recursive graph bisection (few labels between the parts, Fiduccia-Mattheyses, random
+     balance band; PAPER.md l.176 uses hypergraph partitioning); 2 = every trial by bisection.
+     Each trial's tree then goes through the same reconfiguration and slicing. */
+  int32_t partition;
 } jt_planner_opts;
 
 /* Cost counters (PAPER.md l.140-146 Eq. sliced_flops, l.205-212 Eq. task_based;

@@ -311,6 +311,143 @@ Tree tree_from_pairs(const BitPool& leaves, int n_leaves, const std::vector<std:
   return T;
 }
 
+// ---------------------------------------------------------------- recursive bisection (f2)
+// A contraction tree from recursive graph bisection (the partitioned paths of PAPER.md l.176 use
+// hypergraph partitioning, CoTenGra/KaHyPar): split the tensor set into two parts with few labels
+// between them (Fiduccia-Mattheyses refinement of a grown region, a few random starts, part
+// sizes within a balance band), contract each part recursively, then the two results.  Every
+// label sits on exactly two tensors, so the hypergraph is a multigraph with edge weight =
+// shared labels.  Cut labels are the labels of the intermediate; its width is what slicing and
+// the roofline objective trade off later.
+GreedyResult partition_once(const BitPool& leaves, int n_leaves, const CostModel& cm,
+                            const std::vector<std::vector<int>>& carriers, uint64_t seed, double imbalance) {
+  SplitMix rng(seed);
+  // leaf adjacency with multiplicities
+  std::vector<std::vector<std::pair<int, int>>> adj(n_leaves);
+  {
+    std::vector<std::unordered_map<int, int>> m(n_leaves);
+    for (const auto& c : carriers)
+      if (c.size() == 2 && c[0] != c[1]) {
+        ++m[c[0]][c[1]];
+        ++m[c[1]][c[0]];
+      }
+    for (int u = 0; u < n_leaves; ++u) {
+      for (auto& kv : m[u]) adj[u].push_back(kv);
+      std::sort(adj[u].begin(), adj[u].end());
+    }
+  }
+  std::vector<int> side(n_leaves, -1), pos(n_leaves, -1);
+  GreedyResult res;
+  int next_id = n_leaves;
+  // bisect the node set S (side[] marks membership via pos[] >= 0 while active)
+  auto bisect = [&](const std::vector<int>& S, std::vector<int>& A, std::vector<int>& B) {
+    const int n = (int)S.size();
+    for (int i = 0; i < n; ++i) pos[S[i]] = i;
+    const double f = 0.5 - imbalance * 0.5 * rng.uniform();
+    const int lo = std::max(1, (int)std::floor(n * f)), hi = n - lo;
+    std::vector<char> best_side;
+    int best_cut = std::numeric_limits<int>::max();
+    const int starts = n > 64 ? 4 : 2;
+    std::vector<char> sd(n);
+    std::vector<int> gain(n);
+    for (int st = 0; st < starts; ++st) {
+      // grow region 0 from a random seed, preferring nodes most connected to it
+      std::fill(sd.begin(), sd.end(), 1);
+      std::vector<int> conn(n, 0);
+      int size0 = 0;
+      const int target = std::max(1, std::min(n - 1, lo));  // the smaller part
+      int u = (int)(rng.next() % (uint64_t)n);
+      while (size0 < target) {
+        sd[u] = 0;
+        ++size0;
+        for (auto& e : adj[S[u]]) {
+          const int j = pos[e.first];
+          if (j >= 0 && j < n && S[j] == e.first && sd[j]) conn[j] += e.second;
+        }
+        int bu = -1, bc = -1;
+        for (int j = 0; j < n; ++j)
+          if (sd[j] && (conn[j] > bc || (conn[j] == bc && (rng.next() & 1)))) { bc = conn[j]; bu = j; }
+        if (bu < 0) break;
+        u = bu;
+      }
+      // FM passes: move the best-gain unlocked node keeping lo <= |part| <= hi, keep the best prefix
+      auto cut_of = [&]() {
+        int c = 0;
+        for (int i = 0; i < n; ++i)
+          for (auto& e : adj[S[i]]) {
+            const int j = pos[e.first];
+            if (j >= 0 && j < n && S[j] == e.first && sd[i] != sd[j]) c += e.second;
+          }
+        return c / 2;
+      };
+      int cut = cut_of();
+      for (int pass = 0; pass < 4; ++pass) {
+        for (int i = 0; i < n; ++i) {
+          int g = 0;
+          for (auto& e : adj[S[i]]) {
+            const int j = pos[e.first];
+            if (j >= 0 && j < n && S[j] == e.first) g += sd[j] != sd[i] ? e.second : -e.second;
+          }
+          gain[i] = g;
+        }
+        std::vector<char> locked(n, 0);
+        std::vector<int> moves;
+        int cur = cut, bestc = cut, bestk = 0, n0 = 0;
+        for (int i = 0; i < n; ++i) n0 += sd[i] == 0;
+        for (int k = 0; k < n; ++k) {
+          int bi = -1, bg = std::numeric_limits<int>::min();
+          for (int i = 0; i < n; ++i) {
+            if (locked[i]) continue;
+            const int n0n = n0 + (sd[i] == 0 ? -1 : 1);
+            if (std::min(n0n, n - n0n) < lo) continue;
+            if (gain[i] > bg) { bg = gain[i]; bi = i; }
+          }
+          if (bi < 0) break;
+          locked[bi] = 1;
+          n0 += sd[bi] == 0 ? -1 : 1;
+          sd[bi] ^= 1;
+          cur -= bg;
+          moves.push_back(bi);
+          for (auto& e : adj[S[bi]]) {
+            const int j = pos[e.first];
+            if (j >= 0 && j < n && S[j] == e.first && !locked[j]) gain[j] += sd[j] == sd[bi] ? -2 * e.second : 2 * e.second;
+          }
+          if (cur < bestc) { bestc = cur; bestk = (int)moves.size(); }
+        }
+        for (int k = (int)moves.size() - 1; k >= bestk; --k) sd[moves[k]] ^= 1;
+        if (bestc >= cut) break;
+        cut = bestc;
+      }
+      if (cut < best_cut) { best_cut = cut; best_side = sd; }
+    }
+    A.clear();
+    B.clear();
+    for (int i = 0; i < n; ++i) (best_side[i] ? B : A).push_back(S[i]);
+    for (int i = 0; i < n; ++i) pos[S[i]] = -1;
+  };
+  std::function<int(const std::vector<int>&)> build = [&](const std::vector<int>& S) -> int {
+    if (S.size() == 1) return S[0];
+    std::vector<int> A, B;
+    if (S.size() == 2) { A = {S[0]}; B = {S[1]}; }
+    else bisect(S, A, B);
+    if (A.empty() || B.empty()) {  // degenerate split: peel one node
+      A.assign(S.begin(), S.end() - 1);
+      B.assign(1, S.back());
+    }
+    const int a = build(A), b = build(B);
+    res.pairs.push_back({a, b});
+    return next_id++;
+  };
+  std::vector<int> all(n_leaves);
+  for (int i = 0; i < n_leaves; ++i) all[i] = i;
+  build(all);
+  Tree T = tree_from_pairs(leaves, n_leaves, res.pairs);
+  std::vector<uint64_t> nomask(leaves.W, 0);
+  res.cost = tree_cost(T, cm, nomask.data(), nullptr);
+  (void)side;
+  return res;
+}
+
 // ---------------------------------------------------------------- subtree reconfiguration
 bool reconf_node(Tree& T, int v, int F, const CostModel& cm, const uint64_t* mask) {
   const int W = T.W;
@@ -718,8 +855,12 @@ void greedy_plan(const jt_network& net0, const jt_planner_opts& o, std::vector<i
         }
         int variant = i % 2;
         double temp = (i < 2) ? 0.0 : temps[(i / 2) % 4];
-        GreedyResult g = greedy_once(leaves, n_leaves, cm, variant, temp,
-                                     o.seed * 0x9E3779B97F4A7C15ULL + (uint64_t)i, carriers);
+        const uint64_t sd = o.seed * 0x9E3779B97F4A7C15ULL + (uint64_t)i;
+        // opts.partition: 1 = every other trial, 2 = every trial by recursive bisection (f2)
+        const bool part = o.partition == 2 || (o.partition == 1 && (i % 2) == 1);
+        const double imbs[4] = {0.0, 0.2, 0.4, 0.6};
+        GreedyResult g = part ? partition_once(leaves, n_leaves, cm, carriers, sd, imbs[(i / 2) % 4])
+                              : greedy_once(leaves, n_leaves, cm, variant, temp, sd, carriers);
         tcost[i] = g.cost;
         tpairs[i] = std::move(g.pairs);
       }

@@ -33,7 +33,8 @@ class PlannerOpts(ctypes.Structure):
                 ("width_cap", c_i32), ("reconf_sweeps", c_i32), ("reconf_leaves", c_i32),
                 ("time_budget_s", c_dbl), ("bytes_weight", c_dbl), ("candidates", c_i32),
                 ("model_hbm_gbs", c_dbl), ("model_cuda_tflops", c_dbl), ("model_tc_tflops", c_dbl),
-                ("model_launch_us", c_dbl), ("model_esize", c_dbl), ("slice_objective", c_i32)]
+                ("model_launch_us", c_dbl), ("model_esize", c_dbl), ("slice_objective", c_i32),
+                ("partition", c_i32)]
 
 
 class Cost(ctypes.Structure):
@@ -219,13 +220,14 @@ class Plan:
     @classmethod
     def greedy(cls, net, seed=1, trials=64, threads=0, n_sliced=0, width_cap=0, reconf_sweeps=-1,
                reconf_leaves=0, time_budget_s=0.0, bytes_weight=0.0, candidates=0, model=None,
-               slice_objective=0):
+               slice_objective=0, partition=0):
         """jt_plan_greedy.  slice_objective: 0 = sliced cost, 1 = shared-work aware (executed
         prefix-cache cost)."""
         m = model or {}
         o = PlannerOpts(seed, trials, threads, n_sliced, width_cap, reconf_sweeps, reconf_leaves, time_budget_s,
                         bytes_weight, candidates, m.get("hbm_gbs", 0.0), m.get("cuda_tflops", 0.0),
-                        m.get("tc_tflops", 0.0), m.get("launch_us", 0.0), m.get("esize", 0.0), slice_objective)
+                        m.get("tc_tflops", 0.0), m.get("launch_us", 0.0), m.get("esize", 0.0), slice_objective,
+                        partition)
         h = c_vp()
         _check(_lib.jt_plan_greedy(net._h, ctypes.byref(o), ctypes.byref(h)))
         return cls(h, net)
@@ -236,7 +238,7 @@ class Plan:
         the labels that maximise shared work (the executed prefix-cache cost)."""
         p = np.asarray(ssa_path, dtype=np.int64).reshape(-1)
         o = PlannerOpts(0, 0, 0, n_sliced, width_cap, -1, 0, 0.0, bytes_weight, 0, 0.0, 0.0, 0.0, 0.0, 0.0,
-                        slice_objective)
+                        slice_objective, 0)
         h = c_vp()
         _check(_lib.jt_plan_slice(net._h, p.ctypes.data_as(P_i64), len(p) // 2, ctypes.byref(o), ctypes.byref(h)))
         return cls(h, net)

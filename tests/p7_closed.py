@@ -13,7 +13,10 @@ the oracle and of the product (plain 2-vectors), so it pins the GPU path at full
 import numpy as np
 
 
-def slice_closed_form(circ, bits, sliced_labels, index):
+def slice_closed_form(circ, bits, sliced_labels, index, absolute=False):
+    """s_sigma of the P7 circuit; absolute=True evaluates the same chains with |U| entries (and
+    real |.| vectors): the sum of the magnitudes of every product term of s_sigma, the scale of the
+    forward rounding error of any summation order (reading A13d)."""
     n, d = circ.n_wires, circ.d
     digits = {}
     rem = index
@@ -33,7 +36,7 @@ def slice_closed_form(circ, bits, sliced_labels, index):
     for g in circ.gates:
         if len(g.wires) == 1:
             q = g.wires[0]
-            v[q] = g.u @ v[q]
+            v[q] = (np.abs(g.u) @ np.abs(v[q])) if absolute else (g.u @ v[q])
             project(q, nxt)
             nxt += 1
         else:
@@ -44,5 +47,5 @@ def slice_closed_form(circ, bits, sliced_labels, index):
                 nxt += 1
     out = 1 + 0j
     for q in range(n):
-        out *= v[q][bits[q]]
-    return out
+        out *= abs(v[q][bits[q]]) if absolute else v[q][bits[q]]
+    return out.real if absolute else out

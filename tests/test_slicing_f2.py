@@ -68,3 +68,23 @@ def test_fixed_path_validation(jet):
     with pytest.raises(jet.JetError) as e:
         jet.Plan.slice_path(net, bad, n_sliced=2)
     assert e.value.code == 3
+
+
+@pytest.mark.parametrize("partition", [1, 2])
+def test_partition_trials_give_exact_valid_plans(jet, partition):
+    """f2 "better path": trials from recursive graph bisection (jt_planner_opts.partition) produce
+    valid SSA paths whose sliced amplitude equals the oracle's unsliced contraction (C1) and the
+    state vector; on C2 the same slicing and reconfiguration apply (width cap honoured)."""
+    from oracle.statevector import amplitude as sv_amplitude
+
+    circ, bits = workload("C1")
+    net = jet.Network.from_circuit(circ, bits)
+    p = jet.Plan.greedy(net, seed=2, trials=32, n_sliced=3, partition=partition)
+    onet = build_network(circ, bits)
+    vals = contract.slice_values(onet, p.ssa_path, p.sliced_labels)
+    ref = sv_amplitude(circ, bits)
+    assert abs(sum(vals) - ref) <= 1e-12 * abs(ref)
+    circ2, bits2 = workload("C2")
+    net2 = jet.Network.from_circuit(circ2, bits2)
+    p2 = jet.Plan.greedy(net2, seed=1, trials=16, n_sliced=-1, width_cap=24, partition=partition)
+    assert p2.cost()["max_width"] <= 24
