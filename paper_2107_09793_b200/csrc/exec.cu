@@ -1616,6 +1616,7 @@ struct jt_exec {
   std::vector<int> ev_kind;                              // 0 = K2, 1 = K3
   bool use_graphs = true;
   bool pdl = true;  // programmatic dependent launch between the kernels of a slice
+  bool pdl_small = false;  // PDL only for the small CUDA-core launches (K2, K2s, reductions, K6)
   std::vector<cudaGraphExec_t> graphs;   // per prefix-cache level j+1 (j = -1..k)
   std::vector<jt_exec_stats> graph_stats;
   double* graph_acc = nullptr;           // accumulator baked into the graphs
@@ -1788,6 +1789,7 @@ jt_exec* exec_create(const jt_plan& plan, jt_dtype dt, int device, void* d_ws, i
     // (profiles/r02_variants_pdl.txt)
     const char* q = std::getenv("JETB200_PDL");
     ex->pdl = q && q[0] == '1';
+    ex->pdl_small = q && std::string(q) == "small";  // JETB200_PDL=small: only K2 / K2s / K6 launches
   }
   const int32_t* dptr = reinterpret_cast<const int32_t*>(static_cast<char*>(d_ws) + ex->L.state_base +
                                                          offsetof(SliceState, digits));
@@ -1915,7 +1917,7 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     t.C = reinterpret_cast<float2*>(ex->ws + en.out_off);
     ev_begin(ex);
     launch_pdl(pick_stream(en.args.tm, en.args.tk), dim3((unsigned)en.grid_x), dim3(en.block), en.smem, ex->stream,
-               ex->pdl, t);
+               ex->pdl || ex->pdl_small, t);
     ev_end(ex, en);
     st.kernel_launches++;
   } else if (en.kind == 1) {
@@ -1936,13 +1938,13 @@ void launch_node(jt_exec* ex, ExecNode& en) {
     dim3 grid((unsigned)en.grid_x, (unsigned)g.splits);
     GettFn fn = en.kind == 3 ? pick_dmma(en.RM, en.RN, g.gauss != 0) : pick_gett<R>(en.RM, en.RN);
     ev_begin(ex);
-    launch_pdl(fn, grid, dim3(en.block), en.smem, ex->stream, ex->pdl, g);
+    launch_pdl(fn, grid, dim3(en.block), en.smem, ex->stream, ex->pdl || ex->pdl_small, g);
     ev_end(ex, en);
     st.kernel_launches++;
     if (g.splits > 1) {
       int64_t n = en.n_out;
       int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-      launch_pdl(reduce_splits_kernel<R>, dim3(blocks), dim3(256), 0, ex->stream, ex->pdl,
+      launch_pdl(reduce_splits_kernel<R>, dim3(blocks), dim3(256), 0, ex->stream, ex->pdl || ex->pdl_small,
                  reinterpret_cast<const C2*>(g.P), reinterpret_cast<C2*>(g.C), n, (int)g.splits);
       st.kernel_launches++;
     }
@@ -1958,12 +1960,12 @@ template <typename R>
 void slice_sequence(jt_exec* ex, int j, double* d_acc) {
   using C2 = typename V2<R>::t;
   SliceState* state = reinterpret_cast<SliceState*>(ex->ws + ex->L.state_base);
-  launch_pdl(advance_slice_kernel, dim3(1), dim3(32), 0, ex->stream, ex->pdl, state, ex->k, ex->d);
+  launch_pdl(advance_slice_kernel, dim3(1), dim3(32), 0, ex->stream, ex->pdl || ex->pdl_small, state, ex->k, ex->d);
   ex->cur_stats->kernel_launches++;
   for (ExecNode& en : ex->L.order)
     if (en.maxpos >= j) launch_node<R>(ex, en);
   const ExecNode& root = ex->L.order.back();
-  launch_pdl(accumulate_kernel<R>, dim3(1), dim3(32), 0, ex->stream, ex->pdl,
+  launch_pdl(accumulate_kernel<R>, dim3(1), dim3(32), 0, ex->stream, ex->pdl || ex->pdl_small,
              reinterpret_cast<const C2*>(ex->ws + root.out_off), d_acc,
              reinterpret_cast<double2*>(ex->ws + ex->L.vals_base), (const SliceState*)state, ex->n_summed,
              ex->k - ex->n_summed, ex->d);
