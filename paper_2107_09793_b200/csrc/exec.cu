@@ -1051,15 +1051,18 @@ View fill_gett(ExecNode& en, std::map<int64_t, int64_t>& sa, std::map<int64_t, i
     g.TX = (1 << (g.tn - 3)) / en.RN;
     g.KG = 1;
     en.block = 32 * g.TX * g.TY;
-    // split-K to fill the machine: choose the split count (<= 8, <= K iterations) with the
-    // smallest wave-quantisation loss over ~148 x (CTAs per SM) slots
+    // split-K to fill the machine: choose the split count (<= 512, <= K iterations / 4) with the
+    // smallest wave-quantisation loss over ~148 x (CTAs per SM) slots, 0.2% per extra split for
+    // the partial sums.  (Round 1 capped it at 8: the C4 width-30 plan's inner-product node --
+    // 2 output tiles, K = 2^24 -- then ran 16 CTAs at 0.5 TFLOP/s, profiles/r02_nodes_C4_k4.txt.)
     const int cps = en.block >= 256 ? 1 : (en.block >= 128 ? 2 : 4);
     const double slots = 148.0 * cps;
     double best = 1e30;
-    for (int64_t s2 = 1; s2 <= std::min<int64_t>(8, g.k_iters); ++s2) {
+    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(512, g.k_iters / 4));
+    for (int64_t s2 = 1; s2 <= smax; ++s2) {
       const double items = (double)(g.n_tiles * s2);
       const double waves = std::ceil(items / slots);
-      const double loss = waves * slots / items * (1.0 + 0.01 * (double)(s2 - 1));
+      const double loss = waves * slots / items * (1.0 + 0.002 * (double)(s2 - 1));
       if (loss < best - 1e-9) { best = loss; splits = s2; }
     }
     const int64_t cbytes = (g.n_tiles << (g.tm + g.tn)) * esize;
