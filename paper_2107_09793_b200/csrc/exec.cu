@@ -694,6 +694,17 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   t.Np = NP;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   t.acc_bufs = NP <= 128 ? 2 : 1;   // 512 TMEM columns = accumulators + 4 X stages of 64
+  // rotating accumulator regions (default; JETB200_TCG_ROT=0 keeps one accumulator): with 256
+  // accumulator columns and K segments, three 128-column regions + 2 X stages (kernels_tcg.cuh
+  // tcg::Rot) so the MMAs never wait for a segment drain
+  t.lg_xs = 2;
+  {
+    const char* e = getenv("JETB200_TCG_ROT");
+    if (!(e && e[0] == '0') && NP == 256 && t.lg_kcs >= 1 && t.lg_kcs < t.lg_kc) {
+      t.rot = 1;
+      t.lg_xs = 1;
+    }
+  }
   t.tmem_cols = 512;
   t.ystages = ystages;
   t.rstages = rstages;
@@ -1674,8 +1685,8 @@ void describe_exec(const jt_plan& plan, jt_dtype dt, const char* path) {
       std::fprintf(f, "], \"ncopy\": %d, \"copy_bytes\": %d, \"rofs_row\": [%d, %d, %d, %d, %d, %d, %d]", en.kind == 1 ? en.tc.ncopy : en.tcg.ncopyB,
                    en.kind == 1 ? en.tc.copy_bytes : en.tcg.copyB_bytes, en.tc.rofs_row[0], en.tc.rofs_row[1],
                    en.tc.rofs_row[2], en.tc.rofs_row[3], en.tc.rofs_row[4], en.tc.rofs_row[5], en.tc.rofs_row[6]);
-      std::fprintf(f, ", \"tkc\": %d, \"tma\": %d, \"permA\": %d, \"permB\": %d", en.kind == 1 ? en.tc.tkc : 4,
-                   en.kind == 1 ? en.tc.tma : en.tcg.tma, en.permA ? 1 : 0, en.permB ? 1 : 0);
+      std::fprintf(f, ", \"tkc\": %d, \"tma\": %d, \"permA\": %d, \"permB\": %d, \"rot\": %d", en.kind == 1 ? en.tc.tkc : 4,
+                   en.kind == 1 ? en.tc.tma : en.tcg.tma, en.permA ? 1 : 0, en.permB ? 1 : 0, en.kind == 2 ? en.tcg.rot : 0);
     }
     if (en.kind == 4) {
       std::fprintf(f, ", \"st_vec\": %d, \"st_n_lo\": %d, \"st_cols\": %d, \"stN\": [", en.st.vec, en.st.n_lo, en.st.n_cols);

@@ -40,6 +40,8 @@ struct TcgArgs {
   int64_t gB[12], gA[12];   // chunk-tile bits (stride order): global strides
   int32_t sB[12], sA[12];   //   ... and raw byte offsets (XOR-combinable)
   int32_t tma;              // 1: chunks arrive by TMA (gett_tcg_kernel<TMT, true>)
+  int32_t rot;              // 1: rotating accumulator regions (see tcg::Rot), 2 X stages
+  int32_t lg_xs;            // log2 of the TMEM X stages (2, or 1 with rot)
   int32_t ncopyB, copyB_bytes, ncopyA, copyA_bytes;  // bulk copies per chunk (TcArgs::ncopy)
   int64_t xoffB[32], xoffA[32];
   int32_t rofsB_n[7], rofsB_k[4], rofsA_m[7], rofsA_k[4];  // TMA landing byte offsets per bit
@@ -93,6 +95,30 @@ __device__ __forceinline__ int64_t bits_sum(int64_t v, int n, const int64_t* str
 // CTAs of one wave) cover 2^lg_bm M tiles x ~148/2^lg_bm N tiles, so each B chunk is read
 // from HBM once per band and served to the band's other CTAs from L2 (and each A chunk to
 // the wave's N tiles), instead of once per M tile.
+// Rotating accumulator regions (p.rot): the 256 accumulator columns of a tile are two halves of
+// 128 (64 complex columns each, MMA N = 128), and three 128-column TMEM regions rotate between
+// them.  The halves' accumulation segments are staggered by half a segment (half 0 restarts at
+// chunk c = 0 mod S, half 1 at c = S/2 mod S), so at every boundary only ONE half needs a fresh
+// region -- the spare one -- while its finished region drains: the MMAs never wait for the
+// epilogue (the single-accumulator layout stalled them for every drain, 12-14% of the C5 nodes).
+// MMA warp and epilogue run this same deterministic schedule: regions are handed back in event
+// order (FIFO), use counts give the mbarrier parities.
+struct Rot {
+  int reg[2], fifo[4], head, tail, use[3];
+  __device__ __forceinline__ void init() {
+    reg[0] = 0; reg[1] = 1; fifo[0] = 2; head = 0; tail = 1;
+    use[0] = 1; use[1] = 1; use[2] = 0;
+  }
+  // take the next region; *before = its uses so far (parity of the release to wait for)
+  __device__ __forceinline__ int acquire(int* before) {
+    const int r = fifo[head & 3];
+    ++head;
+    *before = use[r]++;
+    return r;
+  }
+  __device__ __forceinline__ void release(int r) { fifo[tail & 3] = r; ++tail; }
+};
+
 __device__ __forceinline__ int64_t raster(int64_t t, const TcgArgs& p) {
   const int lb = p.lg_bm;
   const int64_t mlo = t & ((int64_t(1) << lb) - 1);
@@ -117,7 +143,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
   __shared__ int64_t tgb[2][64], tga[2][64];
   __shared__ int32_t tsb[2][64], tsa[2][64];
   __shared__ int64_t dkB[32], dkA[32];  // chunk c -> c+1 offset steps, by trailing ones of c
-  __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[4], tfull[2], tempty[2], rfull[8], rempty[8];
+  __shared__ __align__(8) uint64_t full[4], xempty[4], yempty[4], tfull[4], tempty[4], rfull[8], rempty[8];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned char* base = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
@@ -157,7 +183,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
       tc::mbar_init(&xempty[i], 1);
     }
     for (int i = 0; i < 4; ++i) tc::mbar_init(&yempty[i], 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 128);
     }
@@ -174,7 +200,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
   pdl_wait();
   pdl_launch_dependents();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t xcol0 = (uint32_t)(p.acc_bufs * NP);
+  const uint32_t xcol0 = p.rot ? 384u : (uint32_t)(p.acc_bufs * NP);  // rot: regions 0-383, X 384-511
   const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles << p.lg_kc;
   const int64_t kc_mask = ((int64_t)1 << p.lg_kc) - 1;
@@ -213,9 +239,9 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
     int rst = 0, ys = 0;
     uint32_t rph = 0, yph = 0;
     for (int64_t it = 0; it < items; ++it) {
-      const int xs = (int)(it & 3);
+      const int xs = (int)(it & ((1 << p.lg_xs) - 1));
       tc::mbar_wait(&rfull[rst], rph);
-      tc::mbar_wait(&xempty[xs], (uint32_t)(((it >> 2) & 1) ^ 1));
+      tc::mbar_wait(&xempty[xs], (uint32_t)(((it >> p.lg_xs) & 1) ^ 1));
       tc::mbar_wait(&yempty[ys], yph ^ 1u);
       tc::fence_after();
       // ---- X: this thread's row, half of the chunk -> hi/lo TF32 in TMEM
@@ -395,8 +421,8 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
       tc::bar_sync(1, 256);
       if (it + RS - 1 < items) copy(it + RS - 1);
       cp_async_commit();
-      const int xs = (int)(it & 3);
-      tc::mbar_wait(&xempty[xs], (uint32_t)(((it >> 2) & 1) ^ 1));
+      const int xs = (int)(it & ((1 << p.lg_xs) - 1));
+      tc::mbar_wait(&xempty[xs], (uint32_t)(((it >> p.lg_xs) & 1) ^ 1));
       tc::mbar_wait(&yempty[ys], yph ^ 1u);
       tc::fence_after();
       // ---- X: this thread's row, half of the chunk -> hi/lo TF32 in TMEM
@@ -454,6 +480,64 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
       if (++rst == RS) rst = 0;
       if (++ys == p.ystages) { ys = 0; yph ^= 1u; }
     }
+  } else if (warp == 12 && p.rot) {
+    // ===================== MMA issuer (rotating accumulator regions) =====================
+    const bool leader = lane == 0;
+    const int64_t S = (int64_t)1 << p.lg_kcs, n_kc = (int64_t)1 << p.lg_kc;
+    const uint32_t idesc_h = (p.idesc & ~(0x3Fu << 17)) | ((uint32_t)(128 >> 3) << 17);  // N = 128
+    tcg::Rot R;
+    R.init();
+    bool acc_on[2] = {false, false};
+    int ys = 0;
+    int64_t it = 0;
+    for (int64_t tt = 0; tt < my_tiles; ++tt) {
+      if (tt > 0)
+        for (int h = 0; h < 2; ++h) {
+          int before;
+          R.reg[h] = R.acquire(&before);
+          if (before > 0) tc::mbar_wait(&tempty[R.reg[h]], (uint32_t)((before & 1) ^ 1));
+          acc_on[h] = false;
+        }
+      for (int64_t c = 0; c < n_kc; ++c, ++it) {
+        for (int h = 0; h < 2; ++h) {
+          const bool bnd = c > 0 && (h == 0 ? (c & (S - 1)) == 0 : (c & (S - 1)) == (S >> 1));
+          if (!bnd) continue;
+          if (leader) tc::mma_commit(&tfull[R.reg[h]]);  // the half's segment is complete
+          R.release(R.reg[h]);
+          int before;
+          R.reg[h] = R.acquire(&before);
+          if (before > 0) tc::mbar_wait(&tempty[R.reg[h]], (uint32_t)((before & 1) ^ 1));
+          acc_on[h] = false;
+        }
+        const int xs = (int)(it & 1);
+        tc::mbar_wait(&full[xs], (uint32_t)((it >> 1) & 1));
+        tc::fence_after();
+        if (leader) {
+          const uint32_t xh = tmem + xcol0 + (uint32_t)(xs * 2 * KPC), xl = xh + KPC;
+          const uint32_t yh = tc::smem_u32(Y + ys * 2 * NP * 128), yl = yh + NP * 128;
+#pragma unroll
+          for (int ks = 0; ks < KPC / 8; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t d = tmem + (uint32_t)(R.reg[h] * 128);
+              const uint64_t dyh = tc::sdesc(yh + h * 16384 + ks * 32, 16, 1024, 2);
+              const uint64_t dyl = tc::sdesc(yl + h * 16384 + ks * 32, 16, 1024, 2);
+              tc::mma_tf32_ts(d, xh + ks * 8, dyh, idesc_h, (acc_on[h] || ks > 0) ? 1u : 0u);
+              tc::mma_tf32_ts(d, xh + ks * 8, dyl, idesc_h, 1u);
+              tc::mma_tf32_ts(d, xl + ks * 8, dyh, idesc_h, 1u);
+            }
+          tc::mma_commit(&xempty[xs]);
+          tc::mma_commit(&yempty[ys]);
+        }
+        __syncwarp();
+        acc_on[0] = acc_on[1] = true;
+        if (++ys == p.ystages) ys = 0;
+      }
+      for (int h = 0; h < 2; ++h) {  // tile end: both halves' last segments
+        if (leader) tc::mma_commit(&tfull[R.reg[h]]);
+        R.release(R.reg[h]);
+      }
+    }
   } else if (warp == 12) {
     // ===================== MMA issuer =====================
     const bool leader = lane == 0;
@@ -461,12 +545,12 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
     int ys = 0;
     const int64_t seg_mask = ((int64_t)1 << p.lg_kcs) - 1;
     for (int64_t it = 0; it < items; ++it) {
-      const int xs = (int)(it & 3);
+      const int xs = (int)(it & ((1 << p.lg_xs) - 1));
       const int64_t c = it & seg_mask;  // chunk within the accumulation segment
       const int b = p.acc_bufs == 2 ? (int)(tt & 1) : 0;
       const uint32_t tph = p.acc_bufs == 2 ? (uint32_t)((tt >> 1) & 1) : (uint32_t)(tt & 1);
       if (c == 0) tc::mbar_wait(&tempty[b], tph ^ 1);
-      tc::mbar_wait(&full[xs], (uint32_t)((it >> 2) & 1));
+      tc::mbar_wait(&full[xs], (uint32_t)((it >> p.lg_xs) & 1));
       tc::fence_after();
       if (leader) {
         const uint32_t d = tmem + (uint32_t)(b * NP);
@@ -487,6 +571,82 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
       if (c == seg_mask) ++tt;
       if (++ys == p.ystages) ys = 0;
     }
+  } else if (warp < 4 && p.rot) {
+    // ===================== epilogue (rotating accumulator regions) =====================
+    // the MMA warp's schedule replayed: every segment event (tile, half, region) in order; the
+    // first segment of a half stores its 64 complex columns directly, later ones are bulk-added
+    const int row = warp * 32 + lane;
+    const int64_t S = (int64_t)1 << p.lg_kcs, n_kc = (int64_t)1 << p.lg_kc;
+    tcg::Rot R;
+    R.init();
+    int q = 0;
+    int seg[2] = {0, 0};
+    auto drain = [&](int64_t tt, int h, int r, int u) {
+      tc::mbar_wait(&tfull[r], (uint32_t)((u - 1) & 1));
+      tc::fence_after();
+      const int64_t t = tcg::raster((int64_t)blockIdx.x + tt * gridDim.x, p);
+      float2* out = p.C + (t << (7 + TMT)) + ((int64_t)(64 * h) << 7);
+      const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(r * 128);
+      if (seg[h]++ == 0) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(tbase + (uint32_t)c0, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) out[row + ((int64_t)(c0 / 2 + j) << 7)] = make_float2(v[2 * j], v[2 * j + 1]);
+        }
+        tc::fence_before();
+        tc::mbar_arrive(&tempty[r]);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // stores before the bulk adds
+        return;
+      }
+      if (tid == 0) tc::bulk_wait<0>();  // this half's earlier segments complete
+      float v[16];
+      tc::tmem_ld16(tbase, v);
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 16, ++q) {
+        float2* sb = ES + (q & 1) * 1024;
+        tc::bar_sync(2, 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sb[j * 128 + row] = make_float2(v[2 * j], v[2 * j + 1]);
+        if (c0 + 16 < 128) tc::tmem_ld16(tbase + (uint32_t)(c0 + 16), v);
+        else {
+          tc::fence_before();
+          tc::mbar_arrive(&tempty[r]);
+        }
+        tc::fence_proxy_async();
+        tc::bar_sync(2, 128);
+        if (tid == 0) {
+          tc::bulk_s2g_add_f32(out + ((int64_t)(c0 / 2) << 7), sb, 8192);
+          tc::bulk_commit();
+          tc::bulk_wait_read<1>();
+        }
+      }
+    };
+    for (int64_t tt = 0; tt < my_tiles; ++tt) {
+      seg[0] = seg[1] = 0;
+      if (tt > 0)
+        for (int h = 0; h < 2; ++h) {
+          int before;
+          R.reg[h] = R.acquire(&before);
+        }
+      for (int64_t c = 1; c < n_kc; ++c)
+        for (int h = 0; h < 2; ++h) {
+          const bool bnd = h == 0 ? (c & (S - 1)) == 0 : (c & (S - 1)) == (S >> 1);
+          if (!bnd) continue;
+          const int r = R.reg[h];
+          drain(tt, h, r, R.use[r]);
+          R.release(r);
+          int before;
+          R.reg[h] = R.acquire(&before);
+        }
+      for (int h = 0; h < 2; ++h) {
+        const int r = R.reg[h];
+        drain(tt, h, r, R.use[r]);
+        R.release(r);
+      }
+    }
+    if (tid == 0) tc::bulk_wait<0>();
   } else if (warp < 4) {
     // ===================== epilogue =====================
     // one accumulator drain per K segment of 2^lg_kcs chunks.  The first segment of a tile is

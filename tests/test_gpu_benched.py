@@ -447,3 +447,25 @@ def test_c2_benched_variants_vs_oracle(jet, monkeypatch, env):
     vals = block_values(jet, ex, 0, 64)
     ref = np.array([gold[i] for i in range(64)])
     assert np.max(np.abs(vals - ref) / np.abs(ref)) < 1e-4
+
+
+def test_c5_rotating_accumulators_vs_single(jet, monkeypatch):
+    """K3g rotating accumulator regions (two 128-column halves with staggered K segments, three
+    TMEM regions; the default for segmented 256-column tiles) against the single-accumulator
+    layout (JETB200_TCG_ROT=0) on the benched C5 plan: both golden slices against the oracle
+    (1e-4, reading A13) and against each other (FP32 regrouping of half 1's segments only)."""
+    rec, gold = load("C5")
+    vals = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("JETB200_TCG_ROT", mode)
+        _, _, _, plan = benched_plan(jet, rec)
+        ks = [n for n in plan.describe_exec("c64")["nodes"] if n["kind"] == 2]
+        assert any(n["rot"] for n in ks) == (mode == "1")
+        ex, _ = exec_on_stream(jet, plan, "c64")
+        vals[mode] = {i: block_values(jet, ex, i, i + 1)[0] for i in sorted(gold)}
+        del ex
+    errs = {m: max(slice_err(v[i], gold[i]) for i in gold) for m, v in vals.items()}
+    diff = max(abs(vals["1"][i] - vals["0"][i]) / abs(vals["0"][i]) for i in gold)
+    record("C5_rot_vs_single", {"max_rel_rot": errs["1"], "max_rel_single": errs["0"], "rot_vs_single": diff})
+    assert errs["1"] < 1e-4 and errs["0"] < 1e-4
+    assert diff < 5e-5
