@@ -694,13 +694,15 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   t.Np = NP;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   t.acc_bufs = NP <= 128 ? 2 : 1;   // 512 TMEM columns = accumulators + 4 X stages of 64
-  // rotating accumulator regions (default; JETB200_TCG_ROT=0 keeps one accumulator): with 256
-  // accumulator columns and K segments, three 128-column regions + 2 X stages (kernels_tcg.cuh
-  // tcg::Rot) so the MMAs never wait for a segment drain
+  // rotating accumulator regions (opt-in, JETB200_TCG_ROT=1): with 256 accumulator columns and K
+  // segments, three 128-column regions + 2 X stages (kernels_tcg.cuh tcg::Rot) so the MMAs never
+  // wait for a segment drain.  Correct (tests) but measured slower on the C5 nodes: 186-189 vs
+  // 214-219 TFLOP/s single-accumulator (no-segment ceiling 242-250), i.e. the N = 128 MMAs and
+  // the halved X ring cost more than the drains they hide (profiles/r02_nodes_C5_rot.txt)
   t.lg_xs = 2;
   {
     const char* e = getenv("JETB200_TCG_ROT");
-    if (!(e && e[0] == '0') && NP == 256 && t.lg_kcs >= 1 && t.lg_kcs < t.lg_kc) {
+    if (e && e[0] == '1' && NP == 256 && t.lg_kcs >= 1 && t.lg_kcs < t.lg_kc) {
       t.rot = 1;
       t.lg_xs = 1;
     }

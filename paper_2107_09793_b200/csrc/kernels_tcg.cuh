@@ -100,7 +100,8 @@ __device__ __forceinline__ int64_t bits_sum(int64_t v, int n, const int64_t* str
 // them.  The halves' accumulation segments are staggered by half a segment (half 0 restarts at
 // chunk c = 0 mod S, half 1 at c = S/2 mod S), so at every boundary only ONE half needs a fresh
 // region -- the spare one -- while its finished region drains: the MMAs never wait for the
-// epilogue (the single-accumulator layout stalled them for every drain, 12-14% of the C5 nodes).
+// epilogue (the single-accumulator layout stalls them for every drain, 12-14% of the C5 nodes).
+// Opt-in: measured slower than the single accumulator (N = 128 MMAs, 2 X stages; see exec.cu).
 // MMA warp and epilogue run this same deterministic schedule: regions are handed back in event
 // order (FIFO), use counts give the mbarrier parities.
 struct Rot {

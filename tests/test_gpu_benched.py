@@ -450,10 +450,10 @@ def test_c2_benched_variants_vs_oracle(jet, monkeypatch, env):
 
 
 def test_c5_rotating_accumulators_vs_single(jet, monkeypatch):
-    """K3g rotating accumulator regions (two 128-column halves with staggered K segments, three
-    TMEM regions; the default for segmented 256-column tiles) against the single-accumulator
-    layout (JETB200_TCG_ROT=0) on the benched C5 plan: both golden slices against the oracle
-    (1e-4, reading A13) and against each other (FP32 regrouping of half 1's segments only)."""
+    """K3g rotating accumulator regions (opt-in JETB200_TCG_ROT=1: two 128-column halves with
+    staggered K segments over three TMEM regions) against the default single-accumulator layout
+    on the benched C5 plan: both golden slices against the oracle (1e-4, reading A13) and against
+    each other (FP32 regrouping of half 1's segments only)."""
     rec, gold = load("C5")
     vals = {}
     for mode in ("1", "0"):
