@@ -162,7 +162,9 @@ jt_status jt_network_close(jt_network* net, const int32_t* x);
 jt_status jt_network_close_batch(jt_network* net, const int32_t* x, const int32_t* open_wires, int32_t n_open);
 /* Counts of the raw network (kets + gates + bras) and labels. */
 jt_status jt_network_info(const jt_network* net, int64_t* n_tensors, int64_t* n_labels);
-/* Neutral JSON file: wires, d, per tensor its labels (data are not written). */
+/* Neutral JSON file: wires, d, per tensor its labels and its data (row-major over those labels,
+   interleaved re, im, 17 significant digits).  Tests compare it element by element with the
+   oracle's own network build (row a1); the oracle never reads it as an input. */
 jt_status jt_network_export(const jt_network* net, const char* path);
 void jt_network_destroy(jt_network* net);
 

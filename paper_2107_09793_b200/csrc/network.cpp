@@ -98,6 +98,16 @@ void network_export(const jt_network* net, const char* path) {
     for (size_t i = 0; i < ls.size(); ++i) f << (i ? ", " : "") << ls[i];
     f << "]";
   }
+  // tensor data, row-major over the labels in the order above, interleaved re, im (exact:
+  // 17 significant digits round-trip a double)
+  f << "], \"data\": [";
+  f.precision(17);
+  for (size_t t = 0; t < net->tensors.size(); ++t) {
+    f << (t ? ", " : "") << "[";
+    const auto& dv = net->tensors[t].data;
+    for (size_t i = 0; i < dv.size(); ++i) f << (i ? ", " : "") << dv[i].real() << ", " << dv[i].imag();
+    f << "]";
+  }
   f << "]}\n";
 }
 

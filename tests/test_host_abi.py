@@ -124,3 +124,31 @@ def test_planner_width_cap(jet):
     plan = jet.Plan.greedy(net, seed=1, trials=16, n_sliced=-1, width_cap=18)
     co = plan.cost()
     assert co["max_width"] <= 18 and co["n_sliced"] > 0
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_network_export_matches_oracle_network(name, tmp_path):
+    """Row a1 pinned at full size: the product's closed network (jt_network_export, labels and
+    data) equals the oracle's own build from the same circuit (oracle/network.py),
+    tensor by tensor, label order and every complex entry exactly (both copy the generator's gate
+    matrices; the product's absorption happens later, in the plan)."""
+    import json
+
+    import numpy as np
+
+    from circuits import workload
+    from oracle.network import build_network
+    from paper_2107_09793_b200 import jet
+
+    circ, bits = workload(name)
+    net = jet.Network.from_circuit(circ, bits)
+    p = tmp_path / "net.json"
+    net.export(str(p))
+    d = json.load(open(p))
+    onet = build_network(circ, bits)
+    assert d["n_wires"] == circ.n_wires and d["d"] == circ.d and d["closed"]
+    assert len(d["tensors"]) == onet.n_tensors == len(d["data"])
+    for t in range(onet.n_tensors):
+        assert tuple(d["tensors"][t]) == tuple(onet.labels[t]), t
+        flat = np.asarray(d["data"][t], dtype=np.float64).view(np.complex128)
+        assert np.array_equal(flat, np.asarray(onet.tensors[t], dtype=np.complex128).reshape(-1)), t
