@@ -6,6 +6,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.log; echo "rc=$?" >> gpurun_out/bench_ref.log
+timeout 600 python scripts/bench_permute.py > gpurun_out/permute.json 2> gpurun_out/permute.log
 CFG=C3 SPS=2 TAG=k3 KREGEX='gett_tc_kernel' timeout 1500 bash scripts/gpu_prof.sh
 CFG=C3 SPS=2 TAG=k2s KREGEX='stream_gett' timeout 900 bash scripts/gpu_prof.sh
 CFG=C5 SPS=1 TAG=k3g KREGEX='gett_tcg' timeout 1500 bash scripts/gpu_prof.sh
