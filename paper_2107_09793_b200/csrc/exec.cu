@@ -701,6 +701,10 @@ bool plan_tcg(ExecNode& en, const View& va, const View& vb, int esize, View& out
   // the halved X ring cost more than the drains they hide (profiles/r02_nodes_C5_rot.txt)
   t.lg_xs = 2;
   {
+    const char* e = getenv("JETB200_TCG_EPI");  // "warp": per-warp segment drains (A/B knob)
+    t.epi_warp = (e && std::string(e) == "warp") ? 1 : 0;
+  }
+  {
     const char* e = getenv("JETB200_TCG_ROT");
     if (e && e[0] == '1' && NP == 256 && t.lg_kcs >= 1 && t.lg_kcs < t.lg_kc) {
       t.rot = 1;

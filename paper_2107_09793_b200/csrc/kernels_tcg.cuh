@@ -42,6 +42,7 @@ struct TcgArgs {
   int32_t tma;              // 1: chunks arrive by TMA (gett_tcg_kernel<TMT, true>)
   int32_t rot;              // 1: rotating accumulator regions (see tcg::Rot), 2 X stages
   int32_t lg_xs;            // log2 of the TMEM X stages (2, or 1 with rot)
+  int32_t epi_warp;         // 1: later segments drained per warp (own staging, 256-B bulk adds)
   int32_t ncopyB, copyB_bytes, ncopyA, copyA_bytes;  // bulk copies per chunk (TcArgs::ncopy)
   int64_t xoffB[32], xoffA[32];
   int32_t rofsB_n[7], rofsB_k[4], rofsA_m[7], rofsA_k[4];  // TMA landing byte offsets per bit
@@ -683,6 +684,37 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
         if (lg_seg > 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // stores before the bulk adds
         continue;
       }
+      if (p.epi_warp) {
+        // per-warp drain: the warp's 32 rows of 8 columns -> its own 2-KB staging buffer (two
+        // per warp) -> 8 bulk FP32 adds of 256 B (one per column) by lane 0; no CTA barrier
+        float2* wsb = ES + warp * 512;
+        if (lane == 0) tc::bulk_wait<0>();  // this warp's earlier segments complete
+        __syncwarp();
+        float v[16];
+        tc::tmem_ld16(tbase, v);
+#pragma unroll 1
+        for (int c0 = 0; c0 < NP; c0 += 16, ++q) {
+          float2* sb = wsb + (q & 1) * 256;
+          __syncwarp();  // lane 0 waited for this buffer's previous read
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sb[j * 32 + lane] = make_float2(v[2 * j], v[2 * j + 1]);
+          if (c0 + 16 < NP) tc::tmem_ld16(tbase + (uint32_t)(c0 + 16), v);
+          else {
+            tc::fence_before();
+            tc::mbar_arrive(&tempty[b]);
+          }
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              tc::bulk_s2g_add_f32(out + ((int64_t)(c0 / 2 + j) << 7) + warp * 32, sb + j * 32, 256);
+            tc::bulk_commit();
+            tc::bulk_wait_read<1>();
+          }
+        }
+        continue;
+      }
       if (tid == 0) tc::bulk_wait<0>();  // earlier segments' adds complete
       float v[16];
       tc::tmem_ld16(tbase, v);
@@ -706,7 +738,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tcg_kernel(const __gr
         }
       }
     }
-    if (tid == 0) tc::bulk_wait<0>();
+    if (tid == 0 || (p.epi_warp && lane == 0)) tc::bulk_wait<0>();
   }
   tc::fence_before();
   __syncthreads();
