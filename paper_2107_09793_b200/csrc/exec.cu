@@ -295,7 +295,13 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   // columns each, or one CTA whose shared memory is padded past half of the SM.  (Two CTAs of
   // one grid sized for one per SM co-resided through shared memory, the second blocking in
   // tcgen05.alloc until the first finished: +2.2 s per C3 amplitude under PDL.)
-  int acc_bufs = (2 * Np + 2 * 2 * Kpc <= 512) ? 2 : 1;
+  // pairN (JETB200_K3_PAIRN=1): N = 16 one-chunk tiles issue 2 MMAs per K step (see TcArgs.pairN)
+  // on accumulators twice as wide
+  bool pairN = false;
+  if (const char* e = std::getenv("JETB200_K3_PAIRN"))
+    pairN = e[0] == '1' && swz && n_kc == 1 && Np == 16 && (2 << tm) == Np;
+  const int acc_w = pairN ? 2 * Np : Np;
+  int acc_bufs = (2 * acc_w + 2 * 2 * Kpc <= 512) ? 2 : 1;
   // JETB200_K3_ACC=4: four accumulators when MMA N <= 16 (one-chunk tiles of tm = 3: the MMA can
   // run up to four tiles ahead of the epilogue)
   if (const char* e = std::getenv("JETB200_K3_ACC"))
@@ -307,9 +313,9 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   // JETB200_K3_CTAS=1/2 forces the count.
   int ctas = (Np <= 16 || n_kc >= 2) ? 2 : 1;
   if (const char* e = std::getenv("JETB200_K3_CTAS")) ctas = std::max(1, std::min(2, atoi(e)));
-  const bool two = ctas == 2 && acc_bufs * Np + 2 * 2 * Kpc <= 256;
+  const bool two = ctas == 2 && acc_bufs * acc_w + 2 * 2 * Kpc <= 256;
   const int cols_budget = two ? 256 : 512;
-  int xstages = std::min(4, (cols_budget - acc_bufs * Np) / (2 * Kpc));
+  int xstages = std::min(4, (cols_budget - acc_bufs * acc_w) / (2 * Kpc));
   if (xstages < 2) return false;
   const int rbytes = 128 * (8 << tkc);
   const int64_t ybytes = 2LL * n_kc * yplane;
@@ -349,9 +355,11 @@ bool plan_tc(ExecNode& en, const View& va, const View& vb, int esize, View& out)
   if (const char* e = std::getenv("JETB200_DEBUG_K3_PASSES"))  // diagnostic only: MMA-count sweep
     if (e[0] == '1') t.passes = 1;
   t.acc_bufs = acc_bufs;
+  t.pairN = pairN ? 1 : 0;
+  t.acc_w = acc_w;
   t.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t cols = 32;
-  while ((int)cols < acc_bufs * Np + xstages * 2 * Kpc) cols <<= 1;
+  while ((int)cols < acc_bufs * acc_w + xstages * 2 * Kpc) cols <<= 1;
   if (!two) cols = 512;
   t.tmem_cols = cols;
   // chunk-tile bits in B-stride order with their byte offsets in the raw landing stage:

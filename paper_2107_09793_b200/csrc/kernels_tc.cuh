@@ -56,6 +56,10 @@ struct TcArgs {
                                                //    -> gather k-pairs as 16-B copies
   int32_t tma;                                 // 1: items arrive by TMA bulk copies (gett_tc_kernel<TKC, true>)
   int32_t mlow;                                // output layout [M bits][7 row bits][outer] (else [rows][M][outer])
+  int32_t pairN;                               // 1: N = 16 one-chunk tiles issue Xhi * [Yhi | Ylo] as ONE
+                                               // N = 32 MMA (Ylo plane right after Yhi) plus Xlo * Yhi:
+                                               // 2 MMAs per K step instead of 3; the epilogue adds the halves
+  int32_t acc_w;                               // TMEM columns per accumulator (Np, or 2 * Np with pairN)
   int32_t passes;                              // MMA products per K step: 3 (3xTF32); 1 only for the
                                                // JETB200_DEBUG_K3_PASSES=1 diagnostic (hi*hi, wrong digits)
   int32_t ncopy, copy_bytes;                   // bulk copies per item (the stride-1 run each) and their size
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t xcol0 = (uint32_t)(p.acc_bufs * p.Np);  // first TMEM column of the X stages
+  const uint32_t xcol0 = (uint32_t)(p.acc_bufs * p.acc_w);  // first TMEM column of the X stages
   const int64_t my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles * p.n_kc;
   const uint32_t layout = p.swz ? 2u : 0u;
@@ -510,17 +514,29 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
       tc::mbar_wait(&xfull[xs], xph);
       tc::fence_after();
       if (leader) {
-        const uint32_t d = tmem + (uint32_t)(b * p.Np);
+        const uint32_t d = tmem + (uint32_t)(b * p.acc_w);
         const uint32_t xh = tmem + xcol0 + (uint32_t)(xs * 2 * KPC), xl = xh + KPC;
         const uint32_t yh = tc::smem_u32(Yhi + c * p.yplane), yl = tc::smem_u32(Ylo + c * p.yplane);
+        if (p.pairN) {
+          // Xhi * [Yhi | Ylo] (N = 2 Np: the Ylo plane follows Yhi in shared memory) into columns
+          // [0, 2 Np), Xlo * Yhi (N = Np) into [0, Np); the epilogue adds column j + Np to j
+          const uint32_t idesc2 = (p.idesc & ~(0x3Fu << 17)) | ((uint32_t)((2 * p.Np) >> 3) << 17);
 #pragma unroll
-        for (int ks = 0; ks < KPC / 8; ++ks) {
-          const uint64_t dyh = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
-          const uint64_t dyl = tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout);
-          tc::mma_tf32_ts(d, xh + ks * 8, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
-          if (p.passes == 3) {
-            tc::mma_tf32_ts(d, xh + ks * 8, dyl, p.idesc, 1u);
-            tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
+          for (int ks = 0; ks < KPC / 8; ++ks) {
+            const uint64_t dyh = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
+            tc::mma_tf32_ts(d, xh + ks * 8, dyh, idesc2, (c > 0 || ks > 0) ? 1u : 0u);
+            tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);  // after the N = 2 Np MMA: always accumulate
+          }
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < KPC / 8; ++ks) {
+            const uint64_t dyh = tc::sdesc(yh + ks * kstep, lbo, p.sbo_y, layout);
+            const uint64_t dyl = tc::sdesc(yl + ks * kstep, lbo, p.sbo_y, layout);
+            tc::mma_tf32_ts(d, xh + ks * 8, dyh, p.idesc, (c > 0 || ks > 0) ? 1u : 0u);
+            if (p.passes == 3) {
+              tc::mma_tf32_ts(d, xh + ks * 8, dyl, p.idesc, 1u);
+              tc::mma_tf32_ts(d, xl + ks * 8, dyh, p.idesc, 1u);
+            }
           }
         }
         tc::mma_commit(&xempty[xs]);                     // TMEM X stage free once these finish
@@ -546,7 +562,13 @@ __global__ void __launch_bounds__(TMA ? 448 : 416, 1) gett_tc_kernel(const __gri
       float2* out = p.C + (t << (7 + p.tm));
       for (int c0 = 0; c0 < p.Np; c0 += 16) {
         float v[16];
-        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.Np + c0), v);
+        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.acc_w + c0), v);
+        if (p.pairN) {  // + the Xhi * Ylo half
+          float w[16];
+          tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * p.acc_w + p.Np + c0), w);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += w[j];
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int m = c0 / 2 + j;

@@ -435,7 +435,8 @@ def test_k2s_and_k3_tma_grid_parity(jet, monkeypatch, grid):
 
 
 @pytest.mark.parametrize("env", [{"JETB200_K3_MLOW": "1"}, {"JETB200_TMA_MINCOPY": "16"},
-                                 {"JETB200_K3_TMA": "0"}, {"JETB200_PDL": "1"}, {"JETB200_K3_ACC": "4"}])
+                                 {"JETB200_K3_TMA": "0"}, {"JETB200_PDL": "1"}, {"JETB200_K3_ACC": "4"},
+                                 {"JETB200_K3_PAIRN": "1"}])
 def test_c2_benched_variants_vs_oracle(jet, monkeypatch, env):
     """The opt-in layout / item-path / launch-mode variants on the benched C2 plan: all 64 slices
     against the oracle goldens (1e-4)."""
